@@ -1,0 +1,142 @@
+"""CPU oracle for the PERKS stencil time loop (arXiv 2204.02064).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+package.  The product path (``paper_2204_02064_b200``) never imports it and
+shares no code with it (the oracle is plain C in ``stencil_oracle.c``; this
+file only marshals numpy arrays into it).
+
+What it computes: T out-of-place applications of the stencil operator
+``x(c)^{k+1} = sum_p w_p x(c+d_p)^k`` (PAPER.md P:182-187 Eq. ``iterative``,
+P:204-213 Eq. ``iterativeStencil``), first term a rounded multiply, the rest
+fused multiply-adds in list order, in the storage dtype, FRAME or PERIODIC
+boundary (DESIGN.md "Readings" R1-R9).
+
+Pins: ``tests/test_oracle_pins.py`` (identity, shift closed form, constant
+fixed point, Fourier-mode decay, exact-rational brute force, linearity,
+composability, maximum principle).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "stencil_oracle.c")
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+BC_FRAME = 0
+BC_PERIODIC = 1
+
+_ERR = {1: "INVALID_ARGUMENT", 2: "INVALID_DOMAIN", 3: "OOM"}
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int):
+        super().__init__(f"oracle error {code} ({_ERR.get(code, '?')})")
+        self.code = code
+        self.name = _ERR.get(code, "?")
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc: -O2 -mfma -ffp-contract=off (no fast-math)."""
+    if (not force and os.path.exists(_LIB_PATH)
+            and os.path.getmtime(_LIB_PATH) >= os.path.getmtime(_SRC)):
+        return _LIB_PATH
+    tmp = _LIB_PATH + f".tmp{os.getpid()}"
+    cmd = ["gcc", "-O2", "-mfma", "-ffp-contract=off", "-fno-fast-math", "-fopenmp",
+           "-std=c11", "-shared", "-fPIC", "-o", tmp, _SRC, "-lm"]
+    subprocess.check_call(cmd)
+    os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is None:
+            lib = ctypes.CDLL(build())
+            i64p = ctypes.POINTER(ctypes.c_int64)
+            i32p = ctypes.POINTER(ctypes.c_int32)
+            for name in ("oracle_stencil_f64", "oracle_stencil_f32"):
+                f = getattr(lib, name)
+                f.restype = ctypes.c_int
+                f.argtypes = [ctypes.c_int, i64p, ctypes.c_int, i32p, ctypes.c_void_p,
+                              ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                              ctypes.c_int]
+            for name in ("oracle_one_step_at_f64", "oracle_one_step_at_f32"):
+                f = getattr(lib, name)
+                f.restype = ctypes.c_int
+                f.argtypes = [ctypes.c_int, i64p, ctypes.c_int, i32p, ctypes.c_void_p,
+                              ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, i64p,
+                              ctypes.c_void_p]
+            lib.oracle_max_threads.restype = ctypes.c_int
+            _lib = lib
+    return _lib
+
+
+def _prep(u0: np.ndarray, offsets, weights, ndim):
+    if u0.dtype not in (np.float32, np.float64):
+        raise TypeError("oracle supports float32/float64 only")
+    u0 = np.ascontiguousarray(u0)
+    if ndim is None:
+        ndim = u0.ndim
+    shape = u0.shape
+    if ndim == 2:
+        if u0.ndim != 2:
+            raise ValueError("2D oracle expects a [ny][nx] array")
+        ext = (shape[1], shape[0], 1)
+    elif ndim == 3:
+        if u0.ndim != 3:
+            raise ValueError("3D oracle expects a [nz][ny][nx] array")
+        ext = (shape[2], shape[1], shape[0])
+    else:
+        raise ValueError("ndim must be 2 or 3")
+    offs = np.ascontiguousarray(np.asarray(offsets, dtype=np.int32).reshape(-1, 3))
+    # R6: weights rounded ONCE to the storage dtype (numpy casts round-to-nearest-even).
+    w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64).astype(u0.dtype))
+    if w.shape[0] != offs.shape[0]:
+        raise ValueError("offsets/weights length mismatch")
+    return u0, ndim, np.asarray(ext, dtype=np.int64), offs, w
+
+
+def run(u0: np.ndarray, offsets, weights, steps: int, bc: int = BC_FRAME,
+        nthreads: int = 1, ndim: int | None = None) -> np.ndarray:
+    """Return x^steps for initial field ``u0`` (C order [z][y][x] or [y][x])."""
+    lib = _load()
+    u0, ndim, ext, offs, w = _prep(u0, offsets, weights, ndim)
+    out = np.empty_like(u0)
+    fn = lib.oracle_stencil_f64 if u0.dtype == np.float64 else lib.oracle_stencil_f32
+    st = fn(ndim, ext.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), offs.shape[0],
+            offs.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), w.ctypes.data,
+            int(bc), int(steps), u0.ctypes.data, out.ctypes.data, int(nthreads))
+    if st != 0:
+        raise OracleError(st)
+    return out
+
+
+def one_step_at(x: np.ndarray, offsets, weights, cells: np.ndarray, bc: int = BC_FRAME,
+                ndim: int | None = None) -> np.ndarray:
+    """One application of the operator evaluated only at linear cell indices ``cells``."""
+    lib = _load()
+    x, ndim, ext, offs, w = _prep(x, offsets, weights, ndim)
+    cells = np.ascontiguousarray(np.asarray(cells, dtype=np.int64))
+    vals = np.empty(cells.shape[0], dtype=x.dtype)
+    fn = lib.oracle_one_step_at_f64 if x.dtype == np.float64 else lib.oracle_one_step_at_f32
+    st = fn(ndim, ext.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), offs.shape[0],
+            offs.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), w.ctypes.data, int(bc),
+            x.ctypes.data, cells.shape[0], cells.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+            vals.ctypes.data)
+    if st != 0:
+        raise OracleError(st)
+    return vals
+
+
+def max_threads() -> int:
+    return int(_load().oracle_max_threads())

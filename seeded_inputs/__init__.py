@@ -1,0 +1,154 @@
+"""Seeded synthetic inputs shared by the oracle side and the CUDA side.
+
+This module holds NONE of the method's arithmetic: it only produces initial
+fields and coefficient lists.  Both ``oracle/`` (via the tests) and the product
+benchmarks draw their inputs from here, so the two paths see identical bytes.
+
+Field recipe (SURVEY §8(c) reading 13): the paper's
+StencilGen data is unavailable, so every cell gets a counter-based
+value ``u0[i] = 1 + m(i) * 2^-p`` where ``m(i)`` is the top ``p`` bits of
+``splitmix64(seed XOR i)`` and ``i`` the GLOBAL C-order linear index
+(z*ny*nx + y*nx + x).  ``p`` = 52 (f64) / 23 (f32) gives exactly representable
+values in [1, 2); ``p`` = 10 gives 10-bit dyadic values for exact-rational tests.
+Because the generator is counter based, each rank of a slab decomposition can
+produce its own slab (``z_offset``) and the concatenation equals the global field.
+
+Coefficient presets (reading 2): dyadic, convex, summing to exactly 1, listed in
+the canonical accumulation order (reading 5):
+  * 2d5pt   W,E,S,C,N             C=1/2, others 1/8          (Fig. 6 order)
+  * 2d9pt   3x3 box, (dy,dx) lexicographic, w=(2-|dx|)(2-|dy|)/16
+  * 3d7pt   W,E,S,C,N,B,F         C=1/4, others 1/8
+  * 3d27pt  3x3x3 box, (dz,dy,dx) lexicographic, w=prod(2-|d|)/64
+"""
+from __future__ import annotations
+
+import numpy as np
+
+SEED = 0x220402064
+_GOLDEN = np.uint64(0x9E3779B97F4A7C15)
+_M1 = np.uint64(0xBF58476D1CE4E5B9)
+_M2 = np.uint64(0x94D049BB133111EB)
+
+
+def splitmix64(x: np.ndarray) -> np.ndarray:
+    """Vectorised splitmix64 finaliser on uint64 (wrapping arithmetic)."""
+    z = x.astype(np.uint64, copy=True)
+    with np.errstate(over="ignore"):
+        z += _GOLDEN
+        z ^= z >> np.uint64(30)
+        z *= _M1
+        z ^= z >> np.uint64(27)
+        z *= _M2
+        z ^= z >> np.uint64(31)
+    return z
+
+
+def _bits_for(dtype, bits):
+    if bits is not None:
+        return bits
+    return 52 if np.dtype(dtype) == np.float64 else 23
+
+
+def field(shape, dtype=np.float64, seed: int = SEED, bits: int | None = None,
+          index_offset: int = 0) -> np.ndarray:
+    """Field of ``shape`` (C order) with values 1 + m*2^-bits in [1,2)."""
+    dtype = np.dtype(dtype)
+    p = _bits_for(dtype, bits)
+    n = int(np.prod(shape))
+    out = np.empty(n, dtype=dtype)
+    chunk = 1 << 24
+    for s in range(0, n, chunk):
+        e = min(n, s + chunk)
+        idx = np.arange(s + index_offset, e + index_offset, dtype=np.uint64)
+        z = splitmix64(idx ^ np.uint64(seed))
+        m = (z >> np.uint64(64 - p)).astype(np.float64)
+        out[s:e] = (1.0 + m * 2.0 ** (-p)).astype(dtype)
+    return out.reshape(shape)
+
+
+def field_torch(shape, dtype, device, seed: int = SEED, bits: int | None = None,
+                index_offset: int = 0):
+    """Same values as :func:`field`, generated with torch int64 ops on ``device``.
+
+    int64 arithmetic wraps like uint64; logical right shifts are emulated with a
+    mask, so the bit pattern equals the numpy uint64 version exactly.
+    """
+    import torch
+
+    tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.float32): torch.float32}[np.dtype(dtype)]
+    p = _bits_for(dtype, bits)
+    n = 1
+    for s_ in shape:
+        n *= int(s_)
+
+    def c64(v):  # uint64 constant -> int64 with the same bits
+        v = int(v) & 0xFFFFFFFFFFFFFFFF
+        return v - (1 << 64) if v >= (1 << 63) else v
+
+    def lsr(z, k):
+        return (z >> k) & ((1 << (64 - k)) - 1)
+
+    out = torch.empty(n, dtype=tdt, device=device)
+    chunk = 1 << 26
+    for s in range(0, n, chunk):
+        e = min(n, s + chunk)
+        z = torch.arange(s + index_offset, e + index_offset, dtype=torch.int64, device=device)
+        z = z ^ c64(seed)
+        z = z + c64(_GOLDEN)
+        z = (z ^ lsr(z, 30)) * c64(_M1)
+        z = (z ^ lsr(z, 27)) * c64(_M2)
+        z = z ^ lsr(z, 31)
+        m = lsr(z, 64 - p).to(torch.float64)
+        out[s:e] = (1.0 + m * 2.0 ** (-p)).to(tdt)
+    return out.reshape(tuple(int(s_) for s_ in shape))
+
+
+# ---------------------------------------------------------------- presets
+
+def preset(name: str):
+    """Return (offsets [(dx,dy,dz)...], weights [float]) in canonical order."""
+    if name == "2d5pt":
+        offs = [(-1, 0, 0), (1, 0, 0), (0, -1, 0), (0, 0, 0), (0, 1, 0)]   # W,E,S,C,N
+        w = [1 / 8, 1 / 8, 1 / 8, 1 / 2, 1 / 8]
+    elif name == "2d9pt":
+        offs, w = [], []
+        for dy in (-1, 0, 1):
+            for dx in (-1, 0, 1):
+                offs.append((dx, dy, 0))
+                w.append((2 - abs(dx)) * (2 - abs(dy)) / 16)
+    elif name == "3d7pt":
+        offs = [(-1, 0, 0), (1, 0, 0), (0, -1, 0), (0, 0, 0), (0, 1, 0), (0, 0, -1), (0, 0, 1)]
+        w = [1 / 8, 1 / 8, 1 / 8, 1 / 4, 1 / 8, 1 / 8, 1 / 8]                # W,E,S,C,N,B,F
+    elif name == "3d27pt":
+        offs, w = [], []
+        for dz in (-1, 0, 1):
+            for dy in (-1, 0, 1):
+                for dx in (-1, 0, 1):
+                    offs.append((dx, dy, dz))
+                    w.append((2 - abs(dx)) * (2 - abs(dy)) * (2 - abs(dz)) / 64)
+    else:
+        raise KeyError(name)
+    return offs, w
+
+
+PRESET_NDIM = {"2d5pt": 2, "2d9pt": 2, "3d7pt": 3, "3d27pt": 3}
+
+
+def random_convex_weights(npts: int, dtype=np.float64, seed: int = 7) -> list[float]:
+    """Random positive weights (seeded), normalised to sum ~1, then dtype-rounded."""
+    rng = np.random.default_rng(seed)
+    w = rng.uniform(0.5, 1.5, size=npts)
+    w = w / w.sum()
+    return [float(v) for v in w.astype(dtype)]
+
+
+# ---------------------------------------------------------------- configs
+
+# BASELINE.json configs; C5 is per-GPU slab, global z = 1024*N.
+CONFIGS = {
+    "C1": dict(stencil="2d5pt", dtype="f64", shape=(128, 128), steps=100),
+    "C2": dict(stencil="2d9pt", dtype="f32", shape=(3072, 3072), steps=1000),
+    "C3": dict(stencil="3d7pt", dtype="f64", shape=(256, 256, 256), steps=1000),
+    "C4": dict(stencil="3d27pt", dtype="f32", shape=(512, 512, 512), steps=500),
+    "C5": dict(stencil="3d7pt", dtype="f64", shape=(1024, 1024, 1024), steps=100),
+}
