@@ -1,0 +1,106 @@
+// common.cuh — device helpers shared by every kernel of the PERKS stencil library (sm_100a).
+// Product code: nothing here is shared with oracle/ (the CPU oracle is independent C).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#ifndef PERKS_DEVINL
+#define PERKS_DEVINL __device__ __forceinline__
+#endif
+
+namespace perks {
+
+// --------------------------------------------------------------------- arithmetic
+// Reading R5: first term one rounded multiply, later terms one fused multiply-add each.
+// The _rn intrinsics pin the rounding (no contraction/reassociation by the compiler).
+PERKS_DEVINL float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+PERKS_DEVINL double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+PERKS_DEVINL float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+PERKS_DEVINL double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+// --------------------------------------------------------------------- vectors
+template <typename T, int V> struct VecT;
+template <> struct VecT<float, 1> { using type = float; };
+template <> struct VecT<float, 2> { using type = float2; };
+template <> struct VecT<float, 4> { using type = float4; };
+template <> struct VecT<double, 1> { using type = double; };
+template <> struct VecT<double, 2> { using type = double2; };
+
+template <typename T, int V>
+PERKS_DEVINL void vload(T (&v)[V], const T *p) {
+  using VT = typename VecT<T, V>::type;
+  VT t = *reinterpret_cast<const VT *>(p);
+  const T *s = reinterpret_cast<const T *>(&t);
+#pragma unroll
+  for (int i = 0; i < V; i++) v[i] = s[i];
+}
+template <typename T, int V>
+PERKS_DEVINL void vstore(T *p, const T (&v)[V]) {
+  using VT = typename VecT<T, V>::type;
+  VT t;
+  T *d = reinterpret_cast<T *>(&t);
+#pragma unroll
+  for (int i = 0; i < V; i++) d[i] = v[i];
+  *reinterpret_cast<VT *>(p) = t;
+}
+// L2-only (bypass L1) loads for data produced by other CTAs during the same launch.
+template <typename T> PERKS_DEVINL T ld_cg(const T *p) { return __ldcg(p); }
+template <typename T> PERKS_DEVINL void st_cg(T *p, T v) { __stcg(p, v); }
+
+// --------------------------------------------------------------------- cp.async
+PERKS_DEVINL uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// 16-byte async copy global->shared, L2 only; src_bytes < 16 zero-fills the rest.
+PERKS_DEVINL void cp_async16(void *sdst, const void *gsrc, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(sdst)),
+               "l"(gsrc), "r"(src_bytes)
+               : "memory");
+}
+PERKS_DEVINL void cp_async8(void *sdst, const void *gsrc, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(sdst)),
+               "l"(gsrc), "r"(src_bytes)
+               : "memory");
+}
+PERKS_DEVINL void cp_async4(void *sdst, const void *gsrc, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(smem_u32(sdst)),
+               "l"(gsrc), "r"(src_bytes)
+               : "memory");
+}
+template <int BYTES> PERKS_DEVINL void cp_async(void *sdst, const void *gsrc, bool valid) {
+  if constexpr (BYTES == 16) cp_async16(sdst, gsrc, valid ? 16 : 0);
+  else if constexpr (BYTES == 8) cp_async8(sdst, gsrc, valid ? 8 : 0);
+  else cp_async4(sdst, gsrc, valid ? 4 : 0);
+}
+PERKS_DEVINL void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N> PERKS_DEVINL void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// --------------------------------------------------------------------- device-wide sync
+PERKS_DEVINL unsigned ld_acquire_gpu(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+PERKS_DEVINL void st_release_gpu(unsigned *p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+PERKS_DEVINL void red_release_gpu(unsigned *p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+// Grid barrier on a monotonically increasing counter (reset to 0 before the launch).
+// Every CTA calls it with the same `target` = (barrier index + 1) * gridDim.x.
+// CTA-level __syncthreads + one releasing arrive per CTA + acquiring spin (P:1068 grid.sync).
+PERKS_DEVINL void grid_barrier(unsigned *ctr, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    red_release_gpu(ctr, 1u);
+    while (ld_acquire_gpu(ctr) < target) {
+    }
+  }
+  __syncthreads();
+}
+
+}  // namespace perks

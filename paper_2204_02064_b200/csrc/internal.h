@@ -1,0 +1,68 @@
+// internal.h — host-side structures shared by the C-ABI layer (api.cu) and the kernel
+// launchers (k2d_stream.cu, k3d_stream.cu, k2d_perks.cu, k3d_perks.cu).  Not installed.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "../../include/perks/perks_stencil.h"
+
+namespace perks {
+
+struct Problem {
+  int ndim;
+  int64_t nx, ny, nz;
+  int shape;          // ShapeId
+  perks_dtype dtype;
+  perks_bc bc;
+  int npts;
+  double wd[27];      // weights rounded to f64 (identity)
+  float wf[27];       // weights rounded once to f32 (reading R6)
+  int device;
+  int num_sms;
+  int max_smem_optin;
+  size_t elem() const { return dtype == PERKS_F64 ? 8 : 4; }
+  int64_t cells() const { return nx * ny * nz; }
+};
+
+// One launchable plan for a variant.
+struct Plan {
+  perks_variant variant = PERKS_AUTO;
+  bool ok = false;
+  const char *why = "";       // reason when !ok
+  int grid = 0, block = 0, ctas_per_sm = 0;
+  int tile[3] = {0, 0, 0};
+  int regs = 0, smem = 0;
+  int64_t units = 0;          // work units per step
+  int zchunk = 0;             // planes per unit (3D)
+  int cfg = 0;                // index of the kernel configuration
+  int64_t cached_reg = 0, cached_smem = 0;
+  double dram_bytes_step = 0, halo_bytes_step = 0;
+  size_t ws_bytes = 0;
+  char name[64] = {0};
+};
+
+inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+// ---- launchers (return cudaSuccess or the failing CUDA error) ----
+// 2D row-strip streaming kernels: host-loop (a) and persistent (b).
+Plan plan_stream2d(const Problem &p, perks_variant v);
+cudaError_t run_stream2d(const Problem &p, const Plan &pl, const void *in, void *out, void *ws,
+                         int64_t steps, cudaStream_t s);
+// 3D plane streaming kernels: host-loop (a) and persistent (b).
+Plan plan_stream3d(const Problem &p, perks_variant v);
+cudaError_t run_stream3d(const Problem &p, const Plan &pl, const void *in, void *out, void *ws,
+                         int64_t steps, cudaStream_t s);
+// PERKS (c), 2D, domain resident on chip.
+Plan plan_perks2d(const Problem &p);
+cudaError_t run_perks2d(const Problem &p, const Plan &pl, const void *in, void *out, void *ws,
+                        int64_t steps, cudaStream_t s);
+// PERKS (c), 3D, partially cached plane streaming.
+Plan plan_perks3d(const Problem &p);
+cudaError_t run_perks3d(const Problem &p, const Plan &pl, const void *in, void *out, void *ws,
+                        int64_t steps, cudaStream_t s);
+
+// Environment override helper (sweeps only): returns def if unset.
+int env_int(const char *name, int def);
+
+}  // namespace perks
