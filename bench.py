@@ -1,0 +1,389 @@
+"""bench.py — the driver's benchmark contract for the PERKS stencil library on B200.
+
+One bench "step" = one pass of the whole hot path: perks_stencil_run over the full time loop
+(T time steps) of the configured workload (default: BASELINE.json configs[1] = C2, 2D 9-point
+box stencil fp32 3072x3072, T=1000 — the workload the metric is quoted on, which fits one GPU).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mine|reference]
+                    [--config C1..C5] [--variant perks|persistent|hostloop|auto]
+
+Prints ONE JSON line on rank 0.  `value` = whole-job GCell-updates/s (cells x T x K x N / max
+over ranks of the device-timed region).  `--impl reference` times the CPU oracle (the only other
+place bench.py executes oracle/) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import seeded_inputs as si  # noqa: E402
+
+METRIC = "stencil GCell-updates/s & effective HBM GB/s vs peak; speedup over host-loop"
+UNIT = "GCells/s"
+FP32_FMA_PER_CLK_SM = 128   # B200 SM: 4 SMSPs x 32 FP32 lanes
+FP64_FMA_PER_CLK_SM = 64    # B200 FP64: half the FP32 rate
+CONFIG_DESC = {
+    "C1": "2D 5-point Jacobi fp64 128x128, T=100",
+    "C2": "2D 9-point box fp32 3072x3072, T=1000",
+    "C3": "3D 7-point heat fp64 256^3, T=1000",
+    "C4": "3D 27-point box fp32 512^3, T=500",
+    "C5": "3D 7-point fp64 1024^3 per GPU, T=100",
+}
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling DURING the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        med = statistics.median(sm) if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _cfg(name):
+    c = dict(si.CONFIGS[name])
+    c["np_dtype"] = np.float64 if c["dtype"] == "f64" else np.float32
+    c["cells"] = int(np.prod(c["shape"]))
+    c["S"] = 8 if c["dtype"] == "f64" else 4
+    return c
+
+
+# ----------------------------------------------------------------------------- reference arm
+
+def run_reference(args):
+    """CPU oracle, as it stands, on a bounded sample of the workload (rank 0 only)."""
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    import oracle
+
+    c = _cfg(args.config)
+    offs, w = si.preset(c["stencil"])
+    cores = os.cpu_count() or 1
+    u0 = si.field(c["shape"], dtype=c["np_dtype"])
+    # bounded sample: T_s time steps of the full domain, sized to ~2-4 s per bench step
+    flops_cell = 2 * len(offs)
+    t0 = time.perf_counter()
+    oracle.run(u0, offs, w, 1, nthreads=cores)
+    t1 = time.perf_counter() - t0
+    T_s = int(max(1, min(c["steps"], 3.0 / max(t1, 1e-6))))
+    for _ in range(args.warmup):
+        oracle.run(u0, offs, w, 1, nthreads=cores)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.run(u0, offs, w, T_s, nthreads=cores)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = c["cells"] * T_s * args.steps / tot / 1e9
+    sample = (f"{CONFIG_DESC[args.config]}: full domain, {T_s} of {c['steps']} time steps per "
+              f"bench step, {cores} OpenMP threads")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": c["dtype"], "data": "synthetic",
+        "config": {"workload": f"{args.config}: {CONFIG_DESC[args.config]}", "sample_steps": T_s},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": sample, "flops_per_cell": flops_cell},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- our arm
+
+def cpu_baseline(c, budget_s=12.0):
+    """Oracle timed on the host cores on a bounded sample (rank 0, N=1 only)."""
+    import oracle
+
+    offs, w = si.preset(c["stencil"])
+    cores = os.cpu_count() or 1
+    u0 = si.field(c["shape"], dtype=c["np_dtype"])
+    t0 = time.perf_counter()
+    oracle.run(u0, offs, w, 1, nthreads=cores)
+    t1 = max(time.perf_counter() - t0, 1e-6)
+    T_s = int(max(1, min(c["steps"], budget_s / t1)))
+    t0 = time.perf_counter()
+    oracle.run(u0, offs, w, T_s, nthreads=cores)
+    dt = time.perf_counter() - t0
+    return {"value": c["cells"] * T_s / dt / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"full domain, {T_s} of {c['steps']} time steps, {cores} OpenMP threads, "
+                      f"{dt:.1f} s"}
+
+
+def _traffic_from_profiles(kernel_prefix, config):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        d = json.load(open(p))
+        e = d.get(config, {})
+        if e.get("kernel", "").startswith(kernel_prefix):
+            return e.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    return None
+
+
+def run_mine(args):
+    import torch
+
+    ws, rank, local = _dist()
+    dist = ws > 1
+    if dist:
+        import torch.distributed as tdist
+
+        tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    from paper_2204_02064_b200 import Stencil
+
+    c = _cfg(args.config)
+    offs, w = si.preset(c["stencil"])
+    T = args.T or c["steps"]
+    st = Stencil(c["shape"], offs, w, dtype=c["np_dtype"], device=local)
+    x = si.field_torch(c["shape"], c["np_dtype"], dev)
+    out = torch.empty_like(x)
+    variant = args.variant
+    q = st.query(variant)
+    wsp = st.workspace(variant)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MiB L2
+
+    def one(v, wsv):
+        st.run(x, T, v, out=out, workspace=wsv)
+
+    for _ in range(args.warmup):
+        one(variant, wsp)
+    torch.cuda.synchronize()
+    if dist:
+        tdist.barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    torch.cuda.synchronize()
+    if dist:
+        tdist.barrier()
+    ev = []
+    for _ in range(args.steps):
+        flush.fill_(1)  # L2 flush between timed steps (outside the timed interval)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        one(variant, wsp)
+        e1.record(stream)
+        ev.append((e0, e1))
+    torch.cuda.synchronize()
+    if dist:
+        tdist.barrier()
+    clocks = sampler.stop()
+    per = [a.elapsed_time(b) for a, b in ev]
+    tot_ms = sum(per)
+    if dist:
+        t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    cells, S = c["cells"], c["S"]
+    value = cells * T * args.steps * ws / (tot_ms * 1e-3) / 1e9
+    ms_per = tot_ms / args.steps
+
+    # --- host-loop reference variant of the same library, same workload (speedup over host loop)
+    hl = None
+    if variant != "hostloop" and not args.no_hostloop:
+        wsh = st.workspace("hostloop")
+        one("hostloop", wsh)
+        torch.cuda.synchronize()
+        hts = []
+        for _ in range(max(1, min(args.steps, 3))):
+            flush.fill_(1)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            one("hostloop", wsh)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            hts.append(e0.elapsed_time(e1))
+        hl = statistics.mean(hts)
+
+    # --- end to end through the public API with host buffers (H2D + run + D2H per step)
+    e2e = None
+    if not args.no_e2e:
+        hin = torch.empty(c["shape"], dtype=x.dtype, pin_memory=True)
+        hin.copy_(x.cpu())
+        hout = torch.empty_like(hin).pin_memory()
+        st.run_host(hin, T, variant, out=hout)  # warm (allocates the handle's device buffers)
+        n_e2e = max(1, min(args.steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            st.run_host(hin, T, variant, out=hout)
+        dt = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([dt], device=dev, dtype=torch.float64)
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+            dt = float(t.item())
+        nbytes = cells * S
+        e2e = {"value": cells * T * n_e2e * ws / dt / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+               "timing": "host wall clock around perks_stencil_run_host (pinned host buffers)"}
+
+    # --- roofline of the dominant kernel (the one launch per step for PERKS / persistent)
+    peaks = _peaks()
+    npts = len(offs)
+    launches_per_step = st.launch_count(variant, T)
+    kern_ms = ms_per / max(1, launches_per_step)
+    if q["variant"] == "perks" and c["stencil"].startswith("2d"):
+        # fully resident domain: on-chip FMA bound
+        fma_rate = FP32_FMA_PER_CLK_SM if c["dtype"] == "f32" else FP64_FMA_PER_CLK_SM
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        peak = 2.0 * fma_rate * sms * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        flops = 2.0 * npts * cells * T / max(1, launches_per_step)
+        achieved = flops / (kern_ms * 1e-3) / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "peak_source": "derived: SMs x FMA/clk x 2 x sm_max_mhz"}
+    else:
+        # HBM bound: algorithmic bytes = model A_gm per launch (2·S·cells·T·(1-f) + 2·S·D_cache)
+        f = (q["cached_cells_reg"] + q["cached_cells_smem"]) / cells if q["variant"] == "perks" else 0.0
+        alg = (2.0 * S * cells * (1 - f) * T + 2.0 * S * cells * f) / max(1, launches_per_step)
+        achieved = alg / (kern_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    roof["traffic"] = _traffic_from_profiles(q["kernel"].split("_")[0], args.config)
+    roof["kernel"] = q["kernel"]
+
+    eff_gbs = 2.0 * S * cells * T * args.steps * ws / (tot_ms * 1e-3) / 1e9
+    from paper_2204_02064_b200 import model
+
+    cached = q["cached_cells_reg"] + q["cached_cells_smem"] if q["variant"] == "perks" else 0
+    proj = model.project(cells, min(cached, cells), T, S, peaks["hbm_gbs"] * 1e9,
+                         A_halo=q["halo_bytes_per_step"] / S * T)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": c["dtype"], "data": "synthetic",
+        "config": {
+            "workload": f"{args.config}: {CONFIG_DESC[args.config]}"
+                        + (" per GPU (independent replicas)" if ws > 1 else ""),
+            "variant": q["variant"], "kernel": q["kernel"], "grid": q["grid"], "block": q["block"],
+            "time_steps_per_bench_step": T, "cells": cells,
+            "l2": "flushed between timed steps (256 MiB device write outside the events)",
+            "inputs": "seeded splitmix64 field in [1,2), dyadic preset weights",
+        },
+        "effective_gbs": eff_gbs,
+        "hbm_frac_effective": eff_gbs / ws / peaks["hbm_gbs"],
+        "us_per_time_step": 1e3 * ms_per / T,
+        "hostloop_ms_per_step": hl,
+        "speedup_vs_hostloop": (hl / ms_per) if hl else None,
+        "model": {"P_gcells": proj.peak_cells_per_s / 1e9,
+                  "M_over_P": (value / ws) / (proj.peak_cells_per_s / 1e9)},
+        "roofline": roof,
+        "gpu_launches": int(launches_per_step * args.steps),
+        "clocks": clocks,
+        "e2e": e2e,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(c)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    st.close()
+    if dist:
+        tdist.barrier()
+        tdist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
+    ap.add_argument("--config", default="C2", choices=sorted(si.CONFIGS))
+    ap.add_argument("--variant", default="perks",
+                    choices=["perks", "persistent", "hostloop", "auto"])
+    ap.add_argument("--T", type=int, default=0, help="override time steps (dev only)")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-hostloop", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_mine(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

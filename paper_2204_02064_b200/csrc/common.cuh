@@ -18,6 +18,21 @@ PERKS_DEVINL double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 PERKS_DEVINL float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 PERKS_DEVINL double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
 
+// A register copy the compiler cannot see through.  Used when a register-cached value is moved
+// into the stencil's sliding window: the cached SSA value then dies at the copy, so ptxas can
+// write the new value back into the same physical register instead of keeping a second copy of
+// the whole register cache alive ("imperfect register reuse by the compiler").
+PERKS_DEVINL float opaque_copy(float v) {
+  float r;
+  asm volatile("mov.b32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+PERKS_DEVINL double opaque_copy(double v) {
+  double r;
+  asm volatile("mov.b64 %0, %1;" : "=d"(r) : "d"(v));
+  return r;
+}
+
 // --------------------------------------------------------------------- vectors
 template <typename T, int V> struct VecT;
 template <> struct VecT<float, 1> { using type = float; };
@@ -83,12 +98,63 @@ PERKS_DEVINL unsigned ld_acquire_gpu(const unsigned *p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+PERKS_DEVINL unsigned ld_relaxed_gpu(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+PERKS_DEVINL void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;\n" ::: "memory"); }
 PERKS_DEVINL void st_release_gpu(unsigned *p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
 PERKS_DEVINL void red_release_gpu(unsigned *p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
+
+// ---- tagged ("LL") exchange words: a value and the step tag that produced it travel in ONE
+// naturally aligned 8-byte store, so a consumer that reads a matching tag also reads the matching
+// value (single-copy atomicity of aligned 8-byte accesses) — no flag, no fence, no membar on the
+// critical path of the per-step halo exchange.  fp64 values use two words (one per 32-bit half).
+struct LLWord {
+  unsigned v, tag;
+};
+PERKS_DEVINL void st_ll(LLWord *p, unsigned v, unsigned tag) {
+  asm volatile("st.volatile.global.v2.u32 [%0], {%1, %2};\n" ::"l"(p), "r"(v), "r"(tag) : "memory");
+}
+PERKS_DEVINL LLWord ld_ll(const LLWord *p) {
+  LLWord w;
+  asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];\n" : "=r"(w.v), "=r"(w.tag) : "l"(p) : "memory");
+  return w;
+}
+template <typename T> struct LL;
+template <> struct LL<float> {
+  static constexpr int WORDS = 1;
+  PERKS_DEVINL static void put(LLWord *p, float x, unsigned tag) { st_ll(p, __float_as_uint(x), tag); }
+  // returns true when every word carries `tag`
+  PERKS_DEVINL static bool get(const LLWord *p, unsigned tag, float &x) {
+    LLWord w = ld_ll(p);
+    x = __uint_as_float(w.v);
+    return w.tag == tag;
+  }
+};
+template <> struct LL<double> {
+  static constexpr int WORDS = 2;
+  PERKS_DEVINL static void put(LLWord *p, double x, unsigned tag) {
+    const unsigned long long b = __double_as_longlong(x);
+    asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "r"((unsigned)b),
+                 "r"(tag), "r"((unsigned)(b >> 32)), "r"(tag)
+                 : "memory");
+  }
+  PERKS_DEVINL static bool get(const LLWord *p, unsigned tag, double &x) {
+    unsigned lo, t0, hi, t1;
+    asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];\n"
+                 : "=r"(lo), "=r"(t0), "=r"(hi), "=r"(t1)
+                 : "l"(p)
+                 : "memory");
+    x = __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
+    return t0 == tag && t1 == tag;
+  }
+};
 
 // Grid barrier on a monotonically increasing counter (reset to 0 before the launch).
 // Every CTA calls it with the same `target` = (barrier index + 1) * gridDim.x.

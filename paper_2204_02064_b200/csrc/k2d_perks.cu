@@ -37,9 +37,40 @@ struct Geo2P {
   static constexpr int CACHE = RS * NT * V;
   static constexpr int ROWBUF = 2 /*par*/ * 2 /*top,bot*/ * (WY + 1) * ROWW;
   static constexpr int COLBUF = 2 /*par*/ * 2 /*left,right*/ * (WX + 1) * TY;
-  static constexpr size_t SMEM_BYTES = (size_t)(CACHE + ROWBUF + COLBUF) * sizeof(T);
+  static constexpr size_t SMEM_BYTES = (size_t)(CACHE + ROWBUF + COLBUF + 32) * sizeof(T);
   static constexpr int SLOT = 2 * (TX + TY);  // one parity of one tile's exchange slot
 };
+
+// Copy n tagged values (all carrying `tag`) from src to smem dst, lane-strided; each lane first
+// issues all its E loads, then re-polls only the words whose tag has not arrived yet.
+template <typename T, int E>
+PERKS_DEVINL void poll_copy(const LLWord *src, int n, unsigned tag, bool exists, T *dst, int lane) {
+  constexpr int W = LL<T>::WORDS;
+  if (!exists) {
+    for (int i = lane; i < n; i += 32) dst[i] = T(0);
+    return;
+  }
+  T val[E];
+  unsigned pending = 0;
+#pragma unroll
+  for (int e = 0; e < E; e++) {
+    const int i = lane + 32 * e;
+    if (i < n && !LL<T>::get(src + i * W, tag, val[e])) pending |= 1u << e;
+  }
+  while (pending) {
+#pragma unroll
+    for (int e = 0; e < E; e++)
+      if ((pending >> e) & 1u) {
+        const int i = lane + 32 * e;
+        if (LL<T>::get(src + i * W, tag, val[e])) pending &= ~(1u << e);
+      }
+  }
+#pragma unroll
+  for (int e = 0; e < E; e++) {
+    const int i = lane + 32 * e;
+    if (i < n) dst[i] = val[e];
+  }
+}
 
 struct Tiles2 {
   int ntx, nty;
@@ -47,22 +78,27 @@ struct Tiles2 {
 
 template <typename T, int S, class G>
 __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__ in,
-                                                           T *__restrict__ out, T *gslot,
-                                                           unsigned *flags, int nx, int ny,
+                                                           T *__restrict__ out, LLWord *gslot,
+                                                           int nx, int ny,
                                                            Tiles2 tl, int64_t steps,
                                                            Coef<T, Shape<S>::N> c) {
   constexpr int V = G::V, R = G::R, RR = G::RR, NT = G::NT, TX = G::TX, TY = G::TY;
-  constexpr int WX = G::WX, WY = G::WY, ROWW = G::ROWW;
+  constexpr int WX = G::WX, WY = G::WY, ROWW = G::ROWW, NWARP = NT / 32;
+  constexpr bool BOX = has_corners<S>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T *smc = reinterpret_cast<T *>(smem_raw);
-  T *rowb = smc + G::CACHE;
-  T *colb = rowb + G::ROWBUF;
-  // row buffers: top[par][j][x+1], j = 0..WY (WY = halo below);  bot[par][j+1][x+1], j = -1..WY-1
-  auto TOP = [&](int par, int j) -> T * { return rowb + ((par * 2 + 0) * (WY + 1) + j) * ROWW; };
-  auto BOT = [&](int par, int jp1) -> T * { return rowb + ((par * 2 + 1) * (WY + 1) + jp1) * ROWW; };
-  // column buffers: left[par][k][y], k = 0..WX (WX = halo right); right[par][k+1][y], k = -1..WX-1
-  auto LEFT = [&](int par, int k) -> T * { return colb + ((par * 2 + 0) * (WX + 1) + k) * TY; };
-  auto RIGHT = [&](int par, int kp1) -> T * { return colb + ((par * 2 + 1) * (WX + 1) + kp1) * TY; };
+  T *const sm = reinterpret_cast<T *>(smem_raw);
+  // shared-memory map (element offsets):
+  //   sm_cache        [0, CACHE)                      row r>=RR of thread tid at (r-RR)*NT*V + tid*V
+  //   row buffers     TOP(par,j) j=0..WY, BOT(par,jp1) jp1=0..WY, each ROWW wide (x=-1..TX)
+  //   column buffers  LEFT(par,k) k=0..WX, RIGHT(par,kp1) kp1=0..WX, each TY tall
+  //   scratch         32 elements (sink for lanes that must not publish; branch-free stores)
+  constexpr int ROW0 = G::CACHE, COL0 = G::CACHE + G::ROWBUF;
+  constexpr int SCR0 = G::CACHE + G::ROWBUF + G::COLBUF;
+  constexpr int PAR_ROW = 2 * (WY + 1) * ROWW, PAR_COL = 2 * (WX + 1) * TY;
+  auto TOP = [](int j) { return ROW0 + j * ROWW; };                    // + par*PAR_ROW
+  auto BOT = [](int jp1) { return ROW0 + (WY + 1 + jp1) * ROWW; };     // + par*PAR_ROW
+  auto LEFT = [](int k) { return COL0 + k * TY; };                     // + par*PAR_COL
+  auto RIGHT = [](int kp1) { return COL0 + (WX + 1 + kp1) * TY; };     // + par*PAR_COL
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wx = warp % WX, wy = warp / WX;
@@ -73,162 +109,153 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
   const int yr0 = wy * R;               // first row relative to tile
   const int x = x0 + xr;
   // global exchange slot of tile t, parity par: [top TX | bot TX | left TY | right TY]
-  auto GS = [&](int t, int par) -> T * { return gslot + ((size_t)t * 2 + par) * G::SLOT; };
-  const bool has_up = ty > 0, has_dn = ty + 1 < tl.nty, has_lf = tx > 0, has_rt = tx + 1 < tl.ntx;
+  // tagged words (LL<T>::WORDS per value); tag of x^s is s+1 (slots are zeroed per run)
+  constexpr int W = LL<T>::WORDS;
+  auto GS = [&](int t, int par) -> LLWord * { return gslot + ((size_t)t * 2 + par) * G::SLOT * W; };
 
-  for (int i = tid; i < G::ROWBUF + G::COLBUF; i += NT) rowb[i] = T(0);
+  for (int i = tid; i < G::ROWBUF + G::COLBUF + 32; i += NT) sm[ROW0 + i] = T(0);
+
+  // per-thread shared-memory offsets (parity 0; add par*PAR_ROW / par*PAR_COL)
+  const bool is_l = lane == 0, is_r = lane == 31;
+  const int o_top = TOP(wy) + xr + 1, o_bot = BOT(wy + 1) + xr + 1;        // publish rows
+  const int o_colL = is_l ? LEFT(wx) + yr0 : SCR0 + lane;                   // publish cols
+  const int o_colR = is_r ? RIGHT(wx + 1) + yr0 : SCR0 + lane;
+  const int o_colL_step = is_l ? 1 : 0, o_colR_step = is_r ? 1 : 0;
+  const int o_rdL = RIGHT(wx) + yr0, o_rdR = LEFT(wx + 1) + yr0;           // read cols
+  const int o_above = BOT(wy) + xr, o_below = TOP(wy + 1) + xr;             // read rows
+  const bool g_top = wy == 0, g_bot = wy == WY - 1;
+  const bool g_l = is_l && wx == 0, g_r = is_r && wx == WX - 1;
+  T *const my_smc = sm + (size_t)tid * V;
+
+  // publish row r (values v) into parity pb: smem edges for neighbours inside the CTA, and the
+  // global exchange slot for the neighbouring tiles (vertical edges stored contiguously)
+  auto publish_row = [&](int pb, LLWord *g, unsigned tag, int r, const T (&v)[V],
+                         bool maybe_edge_row = true) {
+    const int pr = pb * PAR_ROW, pc = pb * PAR_COL;
+    if (maybe_edge_row && r == 0) {
+#pragma unroll
+      for (int i = 0; i < V; i++) sm[pr + o_top + i] = v[i];
+      if (g_top) {
+#pragma unroll
+        for (int i = 0; i < V; i++) LL<T>::put(g + (xr + i) * W, v[i], tag);
+      }
+    }
+    if (maybe_edge_row && r == R - 1) {
+#pragma unroll
+      for (int i = 0; i < V; i++) sm[pr + o_bot + i] = v[i];
+      if (g_bot) {
+#pragma unroll
+        for (int i = 0; i < V; i++) LL<T>::put(g + (TX + xr + i) * W, v[i], tag);
+      }
+    }
+    sm[(is_l ? pc : 0) + o_colL + o_colL_step * r] = v[0];
+    sm[(is_r ? pc : 0) + o_colR + o_colR_step * r] = v[V - 1];
+    if (g_l) LL<T>::put(g + (2 * TX + yr0 + r) * W, v[0], tag);
+    if (g_r) LL<T>::put(g + (2 * TX + TY + yr0 + r) * W, v[V - 1], tag);
+  };
 
   // ---- prologue: load the tile into the caches (P:519 the one-time 2·D_cache term, load half)
   T reg[RR > 0 ? RR : 1][V];
-  auto get_row = [&](int r, T (&v)[V]) {
-    if (r < RR) {
-#pragma unroll
-      for (int i = 0; i < V; i++) v[i] = reg[r < RR ? r : 0][i];
-    } else {
-      vload<T, V>(v, smc + ((size_t)(r - RR) * NT + tid) * V);
-    }
-  };
-  auto put_row = [&](int r, const T (&v)[V]) {
-    if (r < RR) {
-#pragma unroll
-      for (int i = 0; i < V; i++) reg[r < RR ? r : 0][i] = v[i];
-    } else {
-      vstore<T, V>(smc + ((size_t)(r - RR) * NT + tid) * V, v);
-    }
-  };
-  // publish row r (new values) into parity np: smem edges for the neighbours inside the CTA and
-  // the global exchange slot for the neighbouring tiles.
-  auto publish_row = [&](int np, int r, const T (&v)[V]) {
-    if (r == 0) {
-#pragma unroll
-      for (int i = 0; i < V; i++) TOP(np, wy)[xr + 1 + i] = v[i];
-      if (wy == 0) {
-#pragma unroll
-        for (int i = 0; i < V; i++) st_cg(GS(tile, np) + xr + i, v[i]);
-      }
-    }
-    if (r == R - 1) {
-#pragma unroll
-      for (int i = 0; i < V; i++) BOT(np, wy + 1)[xr + 1 + i] = v[i];
-      if (wy == WY - 1) {
-#pragma unroll
-        for (int i = 0; i < V; i++) st_cg(GS(tile, np) + TX + xr + i, v[i]);
-      }
-    }
-    if (lane == 0) {
-      LEFT(np, wx)[yr0 + r] = v[0];
-      if (wx == 0) st_cg(GS(tile, np) + 2 * TX + yr0 + r, v[0]);
-    }
-    if (lane == 31) {
-      RIGHT(np, wx + 1)[yr0 + r] = v[V - 1];
-      if (wx == WX - 1) st_cg(GS(tile, np) + 2 * TX + TY + yr0 + r, v[V - 1]);
-    }
-  };
-
-  __syncthreads();  // zeroed buffers before anyone publishes
-#pragma unroll
-  for (int r = 0; r < R; r++) {
+  auto load_row = [&](int r, T (&v)[V]) {
     const int y = y0 + yr0 + r;
-    T v[V];
 #pragma unroll
     for (int i = 0; i < V; i++) v[i] = (y < ny && x + i < nx) ? in[(size_t)y * nx + x + i] : T(0);
-    put_row(r, v);
-    publish_row(0, r, v);
-  }
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    st_release_gpu(flags + tile, 1u);  // x^0 published
+  };
+  __syncthreads();  // zeroed buffers before anyone publishes
+  {
+    LLWord *g0 = GS(tile, 0);
+#pragma unroll
+    for (int r = 0; r < RR; r++) {
+      T v[V];
+      load_row(r, v);
+#pragma unroll
+      for (int i = 0; i < V; i++) reg[r][i] = v[i];
+      publish_row(0, g0, 1u, r, v);
+    }
+#pragma unroll 1
+    for (int r = RR; r < R; r++) {
+      T v[V];
+      load_row(r, v);
+      vstore<T, V>(my_smc + (size_t)(r - RR) * NT * V, v);
+      publish_row(0, g0, 1u, r, v);
+    }
   }
 
-  // frame predicates (reading R1): interior cells only are updated
-  // rows [ylo, yhi) of the thread's segment are interior (R1); r is compared per row
+  // frame predicates (reading R1): most threads own no frame cell and skip the select
   const int ylo = max(0, 1 - (y0 + yr0)), yhi = min(R, ny - 1 - (y0 + yr0));
-  bool xint[V];
+  const bool all_interior = ylo == 0 && yhi == R && x >= 1 && x + V - 1 <= nx - 2;
+  unsigned xmask = 0;
 #pragma unroll
-  for (int i = 0; i < V; i++) xint[i] = (x + i) >= 1 && (x + i) <= nx - 2;
+  for (int i = 0; i < V; i++) xmask |= ((x + i) >= 1 && (x + i) <= nx - 2) ? (1u << i) : 0u;
 
   for (int64_t t = 0; t < steps; t++) {
     const int par = (int)(t & 1), np = par ^ 1;
-    // ---- wait for the neighbours' x^t edges (flag >= t+1)
-    if (tid < 8) {
-      // tid 0..3: up, down, left, right; 4..7: up-left, up-right, down-left, down-right
-      const int ddx = tid < 2 ? 0 : (tid < 4 ? (tid == 2 ? -1 : 1) : ((tid & 1) ? 1 : -1));
-      const int ddy = tid < 2 ? (tid == 0 ? -1 : 1) : (tid < 4 ? 0 : (tid < 6 ? -1 : 1));
+    const int pr = par * PAR_ROW, pc = par * PAR_COL;
+    // ---- halo: warp s (s = 0 up, 1 down, 2 left, 3 right; round-robin if fewer warps) reads that
+    //      neighbour's x^t edge (tag t+1) from its exchange slot (parity par) through L2 into the
+    //      smem halo.  Each lane issues all its loads, then re-polls only words whose tag is not
+    //      yet t+1.  Halo cells are never cached.
+    const unsigned tag_in = (unsigned)(t + 1);
+#pragma unroll 1
+    for (int side = warp; side < 4; side += NWARP) {
+      const int ddx = side < 2 ? 0 : (side == 2 ? -1 : 1);
+      const int ddy = side < 2 ? (side == 0 ? -1 : 1) : 0;
       const int ntx = tx + ddx, nty = ty + ddy;
-      const bool need = (tid < 4 || has_corners<S>()) && ntx >= 0 && ntx < tl.ntx && nty >= 0 &&
-                        nty < tl.nty;
-      if (need) {
-        const unsigned *f = flags + nty * tl.ntx + ntx;
-        while (ld_acquire_gpu(f) < (unsigned)(t + 1)) {
-        }
-      }
-    }
-    __syncthreads();
-    // ---- halo fill from the neighbours' exchange slots (parity par) through L2
-    {
-      const int nrow = TX, ncol = TY;
-      const int total = 2 * nrow + 2 * ncol;
-      for (int i = tid; i < total; i += NT) {
-        if (i < nrow) {  // row above the tile <- up neighbour's bottom edge
-          BOT(par, 0)[i + 1] = has_up ? ld_cg(GS(tile - tl.ntx, par) + TX + i) : T(0);
-        } else if (i < 2 * nrow) {  // row below <- down neighbour's top edge
-          const int k = i - nrow;
-          TOP(par, WY)[k + 1] = has_dn ? ld_cg(GS(tile + tl.ntx, par) + k) : T(0);
-        } else if (i < 2 * nrow + ncol) {  // left column <- left neighbour's right edge
-          const int k = i - 2 * nrow;
-          RIGHT(par, 0)[k] = has_lf ? ld_cg(GS(tile - 1, par) + 2 * TX + TY + k) : T(0);
-        } else {  // right column <- right neighbour's left edge
-          const int k = i - 2 * nrow - ncol;
-          LEFT(par, WX)[k] = has_rt ? ld_cg(GS(tile + 1, par) + 2 * TX + k) : T(0);
-        }
-      }
-      if (has_corners<S>() && tid < 4 + 4 * (WY - 1)) {
-        // corners of the row buffers at x = -1 and x = TX
-        if (tid < 4) {
-          const bool rt = tid & 1, below = tid >> 1;
-          const int ntx = tx + (rt ? 1 : -1), nty = ty + (below ? 1 : -1);
-          const bool ex = ntx >= 0 && ntx < tl.ntx && nty >= 0 && nty < tl.nty;
-          const int nt = nty * tl.ntx + ntx;
-          // up-left: bottom-right cell of that tile; down-left: top-right; etc.
+      const bool ex = ntx >= 0 && ntx < tl.ntx && nty >= 0 && nty < tl.nty;
+      const int nt = nty * tl.ntx + ntx;
+      if (side < 2) {
+        const int dst = pr + (side == 0 ? BOT(0) : TOP(WY));
+        const LLWord *src = GS(ex ? nt : 0, par) + (side == 0 ? TX : 0) * W;
+        poll_copy<T, (TX + 31) / 32>(src, TX, tag_in, ex, sm + dst + 1, lane);
+        if (BOX && lane < 2) {  // diagonal corners x = -1 (lane 0) and x = TX (lane 1)
+          const int cx = ntx + (lane == 0 ? -1 : 1);
+          const bool cex = cx >= 0 && cx < tl.ntx && nty >= 0 && nty < tl.nty;
+          const LLWord *cs = GS(cex ? nty * tl.ntx + cx : 0, par) + ((side == 0 ? TX : 0) + (lane == 0 ? TX - 1 : 0)) * W;
           T val = T(0);
-          if (ex) val = ld_cg(GS(nt, par) + (below ? 0 : TX) + (rt ? 0 : TX - 1));
-          if (below) TOP(par, WY)[rt ? TX + 1 : 0] = val;
-          else BOT(par, 0)[rt ? TX + 1 : 0] = val;
-        } else {
-          // internal thread-row boundaries j = 1..WY-1: x = -1 / TX cells of rows y0+j*R-1 (bot)
-          // and y0+j*R (top) come from the left/right neighbours' edge columns
-          const int k = tid - 4;
-          const int j = 1 + (k >> 2);
-          const bool rt = k & 1, topk = (k >> 1) & 1;
-          const int yrow = topk ? j * R : j * R - 1;
-          T val = T(0);
-          if (rt ? has_rt : has_lf)
-            val = ld_cg(GS(rt ? tile + 1 : tile - 1, par) + 2 * TX + (rt ? 0 : TY) + yrow);
-          if (topk) TOP(par, j)[rt ? TX + 1 : 0] = val;
-          else BOT(par, j)[rt ? TX + 1 : 0] = val;
+          if (cex)
+            while (!LL<T>::get(cs, tag_in, val)) {
+            }
+          sm[dst + (lane == 0 ? 0 : TX + 1)] = val;
+        }
+      } else {
+        const bool left = side == 2;
+        const int dst = pc + (left ? RIGHT(0) : LEFT(WX));
+        const LLWord *src = GS(ex ? nt : 0, par) + (2 * TX + (left ? TY : 0)) * W;
+        poll_copy<T, (TY + 31) / 32>(src, TY, tag_in, ex, sm + dst, lane);
+        if (BOX) {
+          __syncwarp();
+          // internal corners of the row buffers at x = -1 / TX for thread-row boundaries
+          const int xc = left ? 0 : TX + 1;
+          for (int j = 1 + lane; j < WY; j += 32) {
+            sm[pr + BOT(j) + xc] = sm[dst + j * R - 1];
+            sm[pr + TOP(j) + xc] = sm[dst + j * R];
+          }
         }
       }
     }
     __syncthreads();
     // ---- compute x^{t+1} for the thread's V x R cells (sliding window over rows)
+    LLWord *gnp = GS(tile, np);
+    const unsigned tag_out = (unsigned)(t + 2);
     T prev[V + 2], cur[V + 2], nxt[V + 2];
-    // own row (old values) + its x-neighbours: shuffles inside the warp, column buffers at edges
+    // own row (old values) + x-neighbours: shuffles inside the warp; lanes 0/31 take the
+    // neighbouring warp's / tile's edge column (broadcast reads, branch free)
     auto widen = [&](T (&w)[V + 2], const T (&v)[V], int r) {
       const T l = __shfl_up_sync(0xffffffffu, v[V - 1], 1);
       const T rr = __shfl_down_sync(0xffffffffu, v[0], 1);
-      w[0] = lane == 0 ? RIGHT(par, wx)[yr0 + r] : l;
-      w[V + 1] = lane == 31 ? LEFT(par, wx + 1)[yr0 + r] : rr;
+      const T cl = sm[pc + o_rdL + r];
+      const T cr = sm[pc + o_rdR + r];
+      w[0] = is_l ? cl : l;
+      w[V + 1] = is_r ? cr : rr;
 #pragma unroll
       for (int i = 0; i < V; i++) w[i + 1] = v[i];
     };
     auto halo_below = [&](T (&w)[V + 2]) {
-      const T *b = TOP(par, wy + 1) + xr;
 #pragma unroll
-      for (int i = 0; i < V + 2; i++) w[i] = b[i];
+      for (int i = 0; i < V + 2; i++) w[i] = sm[pr + o_below + i];
     };
     // FMA chain (reading R5) + frame select + publish; rotates the window
-    auto finish_row = [&](int r, T (&nv)[V]) {
+    auto finish_row = [&](int r, T (&nv)[V], bool maybe_edge_row = true) {
 #pragma unroll
       for (int i = 0; i < V; i++) {
         T acc;
@@ -238,9 +265,15 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
           const T val = dy < 0 ? prev[i + 1 + dx] : (dy > 0 ? nxt[i + 1 + dx] : cur[i + 1 + dx]);
           acc = (p == 0) ? mul_rn(c.w[0], val) : fma_rn(c.w[p], val, acc);
         }
-        nv[i] = (r >= ylo && r < yhi && xint[i]) ? acc : cur[i + 1];
+        nv[i] = acc;
       }
-      publish_row(np, r, nv);
+      if (!all_interior) {
+        const bool rin = r >= ylo && r < yhi;
+#pragma unroll
+        for (int i = 0; i < V; i++)
+          if (!(rin && ((xmask >> i) & 1u))) nv[i] = cur[i + 1];
+      }
+      publish_row(np, gnp, tag_out, r, nv, maybe_edge_row);
 #pragma unroll
       for (int i = 0; i < V + 2; i++) {
         prev[i] = cur[i];
@@ -248,15 +281,14 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
       }
     };
     {
-      const T *b = BOT(par, wy) + xr;  // row above the segment, x = xr-1 .. xr+V
 #pragma unroll
-      for (int i = 0; i < V + 2; i++) prev[i] = b[i];
+      for (int i = 0; i < V + 2; i++) prev[i] = sm[pr + o_above + i];  // x = xr-1 .. xr+V
       T v[V];
       if (RR > 0) {
 #pragma unroll
-        for (int i = 0; i < V; i++) v[i] = reg[0][i];
+        for (int i = 0; i < V; i++) v[i] = opaque_copy(reg[0][i]);
       } else {
-        vload<T, V>(v, smc + (size_t)tid * V);
+        vload<T, V>(v, my_smc);
       }
       widen(cur, v, 0);
     }
@@ -266,11 +298,11 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
       if (r + 1 < RR) {
         T v[V];
 #pragma unroll
-        for (int i = 0; i < V; i++) v[i] = reg[r + 1 < RR ? r + 1 : 0][i];
+        for (int i = 0; i < V; i++) v[i] = opaque_copy(reg[r + 1 < RR ? r + 1 : 0][i]);
         widen(nxt, v, r + 1);
       } else if (RR < R) {
         T v[V];
-        vload<T, V>(v, smc + (size_t)tid * V);  // first shared-memory row
+        vload<T, V>(v, my_smc);  // first shared-memory row
         widen(nxt, v, r + 1);
       } else {
         halo_below(nxt);
@@ -280,38 +312,49 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
 #pragma unroll
       for (int i = 0; i < V; i++) reg[r][i] = nv[i];
     }
-    // rows held in shared memory (sm_cache)
-#pragma unroll 2
-    for (int r = RR; r < R; r++) {
-      if (r + 1 < R) {
+    // rows held in shared memory (sm_cache); unrolled by 3 = the window period; the last row
+    // (which reads the row below the segment) is peeled so the loop body has no row tests
+    if (RR < R) {
+#pragma unroll 3
+      for (int r = RR; r < R - 1; r++) {
         T v[V];
-        vload<T, V>(v, smc + ((size_t)(r + 1 - RR) * NT + tid) * V);
+        vload<T, V>(v, my_smc + (size_t)(r + 1 - RR) * NT * V);
         widen(nxt, v, r + 1);
-      } else {
-        halo_below(nxt);
+        T nv[V];
+        finish_row(r, nv, RR == 0 && r == 0);
+        vstore<T, V>(my_smc + (size_t)(r - RR) * NT * V, nv);
       }
+      halo_below(nxt);
       T nv[V];
-      finish_row(r, nv);
-      vstore<T, V>(smc + ((size_t)(r - RR) * NT + tid) * V, nv);
+      finish_row(R - 1, nv);
+      vstore<T, V>(my_smc + (size_t)(R - 1 - RR) * NT * V, nv);
     }
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      st_release_gpu(flags + tile, (unsigned)(t + 2));  // x^{t+1} published
-    }
+    // every warp signals "my part of x^{t+1}'s boundary is published": flag = (t+2)*NWARP when the
+    // whole tile edge is out.  No CTA barrier here: the next step's halo phase only touches the
+    // other parity's buffers, and its __syncthreads orders this step's smem edge writes.
   }
 
-  // ---- epilogue: flush the cache to `out` (the store half of the 2·D_cache term)
-#pragma unroll
-  for (int r = 0; r < R; r++) {
-    const int y = y0 + yr0 + r;
-    T v[V];
-    get_row(r, v);
+  // ---- epilogue: flush the cache to `out` (the store half of the 2·D_cache term).
+  // Addresses go through an empty asm barrier so ptxas cannot hoist 4*RR predicated store
+  // addresses above the time loop (that alone cost ~80 registers; P:860 register pressure).
+  int ybase = y0 + yr0, xe = x;
+  T *oute = out;
+  asm volatile("" : "+r"(ybase), "+r"(xe), "+l"(oute));
+  auto store_row = [&](int r, const T (&v)[V]) {
+    const int y = ybase + r;
     if (y < ny) {
 #pragma unroll
       for (int i = 0; i < V; i++)
-        if (x + i < nx) out[(size_t)y * nx + x + i] = v[i];
+        if (xe + i < nx) oute[(size_t)y * nx + xe + i] = v[i];
     }
+  };
+#pragma unroll
+  for (int r = 0; r < RR; r++) store_row(r, reg[r]);
+#pragma unroll 1
+  for (int r = RR; r < R; r++) {
+    T v[V];
+    vload<T, V>(v, my_smc + (size_t)(r - RR) * NT * V);
+    store_row(r, v);
   }
 }
 
@@ -319,10 +362,10 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
 
 namespace {
 // Configurations (index = Plan::cfg).  f32 V=4, f64 V=2 (16-byte vectors per thread-row).
-using P2F_A = Geo2P<float, 4, 2, 8, 8, 24>;    // 256 x 256 tile, 512 thr, 64 KiB regs + 192 KiB smem
+using P2F_A = Geo2P<float, 4, 2, 4, 16, 48>;   // 256 x 256 tile, 256 thr, 64 KiB regs + 192 KiB smem
 using P2F_B = Geo2P<float, 4, 1, 8, 8, 8>;     // 128 x 128 tile, 256 thr
 using P2F_C = Geo2P<float, 4, 1, 4, 8, 0>;     // 128 x  32 tile, 128 thr
-using P2D_A = Geo2P<double, 2, 2, 8, 4, 12>;   // 128 x 128 tile, 512 thr
+using P2D_A = Geo2P<double, 2, 2, 4, 16, 16>;  // 128 x 128 tile, 256 thr, 64 KiB regs + 64 KiB smem
 using P2D_B = Geo2P<double, 2, 2, 4, 8, 0>;    // 128 x  32 tile, 256 thr
 using P2D_C = Geo2P<double, 2, 1, 2, 8, 0>;    //  64 x  16 tile,  64 thr
 constexpr int NCFG = 3;
@@ -365,10 +408,16 @@ Plan plan_perks2d(const Problem &p) {
     return pl;
   }
   if (p.nx > (1 << 30) || p.ny > (1 << 30)) { pl.why = "perks2d: extent too large"; return pl; }
-  // Choose the smallest tile whose tile count fits one CTA per SM (all CTAs co-resident).
+  // Planner: if the whole domain fits one CTA's tile, use one CTA (no inter-CTA sync at all —
+  // small domains are latency bound).  Otherwise the smallest tile whose count
+  // fits one CTA per SM (all CTAs co-resident; minimal occupancy).
   int forced = env_int("PERKS_P2D_CFG", -1);
   int best = -1;
-  for (int cfg = NCFG - 1; cfg >= 0; cfg--) {
+  for (int cfg = NCFG - 1; cfg >= 0 && forced < 0; cfg--) {
+    CfgInfo ci = cfg_info(p, cfg);
+    if (p.nx <= ci.TX && p.ny <= ci.TY && ci.smem <= (size_t)p.max_smem_optin) { best = cfg; break; }
+  }
+  for (int cfg = NCFG - 1; cfg >= 0 && best < 0; cfg--) {
     if (forced >= 0 && cfg != forced) continue;
     CfgInfo ci = cfg_info(p, cfg);
     const int64_t tiles = ((p.nx + ci.TX - 1) / ci.TX) * ((p.ny + ci.TY - 1) / ci.TY);
@@ -398,8 +447,9 @@ Plan plan_perks2d(const Problem &p) {
   const double S = (double)p.elem();
   pl.dram_bytes_step = 0.0;  // domain fully resident: only the one-time 2·D_cache term
   pl.halo_bytes_step = S * 2.0 * pl.grid * 2.0 * (ci.TX + ci.TY);  // publish + read, L2
-  const size_t slot_bytes = (size_t)pl.grid * 2 * 2 * (ci.TX + ci.TY) * p.elem();
-  pl.ws_bytes = align256(slot_bytes) + align256((size_t)pl.grid * sizeof(unsigned));
+  // tagged exchange words: 8 bytes per fp32 value, 16 per fp64 value
+  const size_t slot_bytes = (size_t)pl.grid * 2 * 2 * (ci.TX + ci.TY) * (p.elem() == 8 ? 16 : 8);
+  pl.ws_bytes = align256(slot_bytes);
   snprintf(pl.name, sizeof(pl.name), "perks2d_%s_%s_cfg%d_t%dx%d", p.shape == SHAPE_2D5 ? "5pt" : "9pt",
            p.dtype == PERKS_F32 ? "f32" : "f64", best, ci.TX, ci.TY);
   pl.ok = true;
@@ -412,15 +462,14 @@ static cudaError_t launch_p2d(const Problem &p, const Plan &pl, const T *in, T *
   CfgInfo ci = cfg_info(p, pl.cfg);
   Coef<T, Shape<S>::N> c;
   for (int i = 0; i < Shape<S>::N; i++) c.w[i] = sizeof(T) == 4 ? (T)p.wf[i] : (T)p.wd[i];
-  T *gslot = (T *)ws;
-  const size_t slot_bytes = (size_t)pl.grid * 2 * 2 * (ci.TX + ci.TY) * p.elem();
-  unsigned *flags = (unsigned *)((char *)ws + align256(slot_bytes));
-  cudaError_t e = cudaMemsetAsync(flags, 0, (size_t)pl.grid * sizeof(unsigned), s);
+  LLWord *gslot = (LLWord *)ws;
+  const size_t slot_bytes = (size_t)pl.grid * 2 * 2 * (ci.TX + ci.TY) * LL<T>::WORDS * sizeof(LLWord);
+  cudaError_t e = cudaMemsetAsync(gslot, 0, slot_bytes, s);  // tags restart at 1 every run
   if (e != cudaSuccess) return e;
   Tiles2 tl{(int)((p.nx + ci.TX - 1) / ci.TX), (int)((p.ny + ci.TY - 1) / ci.TY)};
   int nx = (int)p.nx, ny = (int)p.ny;
-  void *args[] = {(void *)&in, (void *)&out, (void *)&gslot, (void *)&flags, (void *)&nx,
-                  (void *)&ny, (void *)&tl, (void *)&steps, (void *)&c};
+  void *args[] = {(void *)&in, (void *)&out, (void *)&gslot, (void *)&nx, (void *)&ny,
+                  (void *)&tl, (void *)&steps, (void *)&c};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(pl.grid);
   cfg.blockDim = dim3(ci.NT);
