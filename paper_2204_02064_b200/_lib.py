@@ -9,7 +9,8 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libperks_stencil.so")
+# PERKS_LIB_PATH overrides the library (development sweeps of compile-time tile parameters only)
+LIB_PATH = os.environ.get("PERKS_LIB_PATH") or os.path.join(_PKG, "libperks_stencil.so")
 
 PERKS_OK = 0
 STATUS_NAMES = {

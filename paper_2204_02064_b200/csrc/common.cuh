@@ -87,6 +87,10 @@ template <int BYTES> PERKS_DEVINL void cp_async(void *sdst, const void *gsrc, bo
   else if constexpr (BYTES == 8) cp_async8(sdst, gsrc, valid ? 8 : 0);
   else cp_async4(sdst, gsrc, valid ? 4 : 0);
 }
+// Bulk L2 prefetch of [p, p+bytes) (16-byte aligned address and size; sm_90+).
+PERKS_DEVINL void prefetch_l2(const void *p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
 PERKS_DEVINL void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N> PERKS_DEVINL void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");

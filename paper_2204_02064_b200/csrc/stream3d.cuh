@@ -3,12 +3,21 @@
 // thread computes the cells in a vertical direction".
 //
 // A CTA owns an xy tile of TX x TY cells (TX = 32*V: one warp spans x; TY = NWARP*R) and a z range.
-// Planes arrive in increasing z into a ring of NS shared-memory slots (cp.async, NS-1 planes in
-// flight).  Each slot holds the tile plus a one-cell halo ring; rows are padded so the interior
+// Planes arrive in increasing z into a ring of NS shared-memory slots with NS-1 planes in flight.
+// Each slot holds the tile plus a one-cell halo ring; rows are padded by PAD = 16 B so the interior
 // starts 16-byte aligned.  Thread (lane, warp) owns V x R cells of every plane.  When plane q is
 // resident, the chain terms of outputs q+1 / q / q-1 that read plane q are applied in list order
 // (stages A/B/C of shapes.cuh), so each plane is read from shared memory once per thread.
+//
+// Two loaders fill the ring:
+//   * TMA (Blackwell/Hopper tensor-memory accelerator): ONE thread issues one 3D tensor box
+//     {P, TY+2, 1} per plane (cp.async.bulk.tensor, out-of-bounds cells zero-filled by hardware)
+//     completing on the slot's mbarrier — no per-thread address arithmetic in the plane loop.
+//     Requires 16-byte aligned rows (nx*S % 16 == 0).
+//   * cp.async (fallback for ragged nx): every thread copies its own cells.
 #pragma once
+#include <cuda.h>
+
 #include "common.cuh"
 #include "shapes.cuh"
 
@@ -20,18 +29,73 @@ struct Geo3D {
   static constexpr int NT = 32 * NWARP;
   static constexpr int TX = 32 * V, TY = NWARP * R;
   static constexpr int PAD = 16 / (int)sizeof(T);  // interior starts 16-B aligned
-  static constexpr int P = TX + 2 * PAD;             // row pitch (elements)
+  static constexpr int P = TX + 2 * PAD;             // row pitch (elements) = TMA box width
   static constexpr int ROWS = TY + 2;
-  static constexpr int SLOT = ROWS * P;              // elements per slot
-  static constexpr size_t SLOT_BYTES = (size_t)SLOT * sizeof(T);
+  static constexpr int SLOT_RAW = ROWS * P;
+  static constexpr int SLOT = (SLOT_RAW * (int)sizeof(T) + 127) / 128 * 128 / (int)sizeof(T);
+  static constexpr size_t SLOT_BYTES = (size_t)SLOT * sizeof(T);  // 128-B multiple (TMA dst)
+  static constexpr unsigned BOX_BYTES = (unsigned)(SLOT_RAW * sizeof(T));
+  static constexpr unsigned ROW_BYTES = (unsigned)(P * sizeof(T));
   static_assert(V * (int)sizeof(T) == 16, "one 16-byte vector per thread per row");
   static_assert(NT >= 2 * ROWS, "halo-column loaders");
+  static_assert(P <= 256 && ROWS <= 256, "TMA box dims <= 256");
 };
 
 struct Dom3 {
   int nx, ny, nz;
 };
 
+// TMA descriptors of the (up to) three buffers a run reads: 0 = in, 1 = out, 2 = tmp.
+struct Maps3 {
+  CUtensorMap box[3];  // box {P, ROWS, 1}: a whole tile plane with its halo ring
+  CUtensorMap row[3];  // box {P, 1, 1}: one halo row (cached planes)
+};
+
+// ---------------------------------------------------------------- mbarrier / TMA primitives
+PERKS_DEVINL void mbar_init(uint64_t *b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+PERKS_DEVINL void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+PERKS_DEVINL void mbar_arrive_tx(uint64_t *b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+PERKS_DEVINL void mbar_arrive(uint64_t *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+// arrive when all of this thread's prior cp.async copies have landed
+PERKS_DEVINL void mbar_arrive_cpasync(uint64_t *b) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+PERKS_DEVINL void mbar_wait(uint64_t *b, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+// 1D bulk async copy global -> shared (16-B aligned, size multiple of 16), completes on `bar`.
+PERKS_DEVINL void bulk_load(void *sdst, const void *gsrc, unsigned bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(sdst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+PERKS_DEVINL void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+PERKS_DEVINL void tma_load_3d(void *sdst, const CUtensorMap *map, int x, int y, int z, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+          smem_u32(sdst)),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ---------------------------------------------------------------- cp.async loader (fallback)
 // Issue cp.async copies of plane q of `src` (tile origin x0,y0) into `slot`.  Cells outside the
 // domain are zero-filled (they only feed frame cells, whose results are discarded).
 // If `halo_only`, only the one-cell ring around the tile is fetched (PERKS cached planes).
@@ -44,7 +108,6 @@ PERKS_DEVINL void issue_plane(T *slot, const T *__restrict__ src, const Dom3 &d,
   const T *base = src + (zin ? (size_t)q * pl : 0);
   const int x = x0 + lane * G::V;
   const bool xin = x < d.nx;
-  // own rows (tile interior)
   // one row segment of V cells: a 16-byte copy when rows are vector aligned (nx % V == 0),
   // else V element copies with per-element bounds (ragged nx)
   const bool vec = (d.nx % G::V) == 0;
@@ -87,6 +150,7 @@ PERKS_DEVINL void issue_plane(T *slot, const T *__restrict__ src, const Dom3 &d,
   }
 }
 
+// ---------------------------------------------------------------- compute
 // Neighbourhood of the thread's V x R cells in one resident plane:
 // nb[j][i] = cell (x - 1 + i, y - 1 + j) for j in [0, R+2), i in [0, V+2).
 template <typename T, class G>
@@ -99,8 +163,9 @@ PERKS_DEVINL void read_nb(const T *slot, T (&nb)[G::R + 2][G::V + 2]) {
     vload<T, G::V>(v, row + G::PAD + lane * G::V);
     const T l = __shfl_up_sync(0xffffffffu, v[G::V - 1], 1);
     const T r = __shfl_down_sync(0xffffffffu, v[0], 1);
-    nb[j][0] = lane == 0 ? row[G::PAD - 1] : l;
-    nb[j][G::V + 1] = lane == 31 ? row[G::PAD + G::TX] : r;
+    const T el = row[G::PAD - 1 + (lane == 31 ? G::TX + 1 : 0)];  // one broadcast-free LDS
+    nb[j][0] = lane == 0 ? el : l;
+    nb[j][G::V + 1] = lane == 31 ? el : r;
 #pragma unroll
     for (int i = 0; i < G::V; i++) nb[j][i + 1] = v[i];
   }
@@ -134,11 +199,16 @@ struct StreamState {
   T accB[G::R][G::V];  // output q
   T accC[G::R][G::V];  // output q-1
   T cm1[G::R][G::V];   // centre of the previous plane (q-1)
+  PERKS_DEVINL void zero() {
+#pragma unroll
+    for (int r = 0; r < G::R; r++)
+#pragma unroll
+      for (int i = 0; i < G::V; i++) accA[r][i] = accB[r][i] = accC[r][i] = cm1[r][i] = T(0);
+  }
 };
 
-// Process the arrival of plane q (resident in `slot`): finish output q-1 (returned in `out`,
-// frame cells replaced by their old value), advance outputs q and q+1, rotate the state.
-// `center_out` receives the centre values of plane q (the thread's own cells).
+// Process the arrival of plane q (resident in `slot`): finish output q-1 (returned in `out`),
+// advance outputs q and q+1, rotate the state.  `center_q` receives plane q's own cells.
 template <typename T, int S, class G>
 PERKS_DEVINL void arrival(StreamState<T, G> &st, const T *slot, const Coef<T, Shape<S>::N> &c,
                           T (&out)[G::R][G::V], T (&center_q)[G::R][G::V]) {
@@ -168,72 +238,192 @@ PERKS_DEVINL void arrival(StreamState<T, G> &st, const T *slot, const Coef<T, Sh
     }
 }
 
-// Frame select + store of output plane o.  `old` = the plane's step-k values (centre).
+// Per-thread, per-unit constants for stores and frame selection (computed once per unit).
+template <class G>
+struct ThreadTile {
+  int x, y;          // first owned cell
+  bool xin;          // x < nx (vector start inside the domain)
+  bool inner;        // all owned cells interior in x and y (no frame select needed)
+  bool vec;          // rows 16-byte aligned: vector stores
+  PERKS_DEVINL void init(const Dom3 &d, int x0, int y0) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    x = x0 + lane * G::V;
+    y = y0 + warp * G::R;
+    xin = x < d.nx;
+    inner = x >= 1 && x + G::V - 1 <= d.nx - 2 && y >= 1 && y + G::R - 1 <= d.ny - 2;
+    vec = (d.nx % G::V) == 0;
+  }
+};
+
+// Frame select (reading R1) of output plane o; `old` = its step-k values (centre).
 template <typename T, class G>
-PERKS_DEVINL void store_plane(T *__restrict__ dst, const Dom3 &d, int o, int x0, int y0,
-                              const T (&val)[G::R][G::V], const T (&old)[G::R][G::V]) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int x = x0 + lane * G::V;
-  if (x >= d.nx) return;
+PERKS_DEVINL void frame_select(const Dom3 &d, const ThreadTile<G> &tt, int o, T (&val)[G::R][G::V],
+                               const T (&old)[G::R][G::V]) {
   const bool zint = o >= 1 && o <= d.nz - 2;
+  if (zint && tt.inner) return;
+#pragma unroll
+  for (int r = 0; r < G::R; r++) {
+    const int y = tt.y + r;
+    const bool yint = zint && y >= 1 && y <= d.ny - 2;
+#pragma unroll
+    for (int i = 0; i < G::V; i++)
+      if (!(yint && (tt.x + i) >= 1 && (tt.x + i) <= d.nx - 2)) val[r][i] = old[r][i];
+  }
+}
+
+// Store the thread's cells of plane o (already frame-selected).
+template <typename T, class G>
+PERKS_DEVINL void store_cells(T *__restrict__ dst, const Dom3 &d, const ThreadTile<G> &tt, int o,
+                              const T (&v)[G::R][G::V]) {
+  if (!tt.xin) return;
   T *base = dst + (size_t)o * d.nx * d.ny;
 #pragma unroll
   for (int r = 0; r < G::R; r++) {
-    const int y = y0 + warp * G::R + r;
+    const int y = tt.y + r;
     if (y >= d.ny) break;
-    const bool yint = zint && y >= 1 && y <= d.ny - 2;
-    T v[G::V];
-#pragma unroll
-    for (int i = 0; i < G::V; i++) {
-      const bool inter = yint && (x + i) >= 1 && (x + i) <= d.nx - 2;
-      v[i] = inter ? val[r][i] : old[r][i];
-    }
-    if ((d.nx % G::V) == 0) {
-      vstore<T, G::V>(base + (size_t)y * d.nx + x, v);
+    if (tt.vec) {
+      vstore<T, G::V>(base + (size_t)y * d.nx + tt.x, v[r]);
     } else {
 #pragma unroll
       for (int i = 0; i < G::V; i++)
-        if (x + i < d.nx) base[(size_t)y * d.nx + x + i] = v[i];
+        if (tt.x + i < d.nx) base[(size_t)y * d.nx + tt.x + i] = v[r][i];
     }
   }
 }
 
-// Stream one unit (tile x0,y0; planes [zs, ze)) of one time step from src to dst.
-// All slots must be free on entry (caller synchronises); leaves no copies in flight that target
-// slots still being read.
-template <typename T, int S, class G>
-PERKS_DEVINL void stream_unit(T *smem, const T *__restrict__ src, T *__restrict__ dst,
-                              const Dom3 &d, int x0, int y0, int zs, int ze,
-                              const Coef<T, Shape<S>::N> &c) {
+// ---------------------------------------------------------------- ring (TMA or cp.async)
+// Arrival counter `gk` runs across units and steps: slot = gk % NS, mbarrier parity = (gk/NS)&1.
+template <typename T, class G, bool TMA>
+struct Ring {
+  T *slots;        // NS slots
+  uint64_t *bars;  // NS mbarriers (TMA)
+  unsigned gk;     // arrivals consumed so far (this CTA)
+
+  PERKS_DEVINL T *slot(unsigned k) const { return slots + (size_t)(k % G::NS) * G::SLOT; }
+  PERKS_DEVINL uint64_t *bar(unsigned k) const { return bars + (k % G::NS); }
+
+  // one-time init (all threads call; thread 0 initialises the barriers)
+  PERKS_DEVINL void init(T *s, uint64_t *b, unsigned col_arrivals) {
+    slots = s;
+    bars = b;
+    gk = 0;
+    if (TMA && threadIdx.x == 0) {
+      for (int i = 0; i < G::NS; i++) mbar_init(bars + i, 1 + col_arrivals);
+      mbar_fence_init();
+    }
+    __syncthreads();
+  }
+
+  // Full plane q of buffer `src` (TMA map `map`) into the slot of arrival k.
+  PERKS_DEVINL void issue_full(unsigned k, const T *src, const CUtensorMap *map, const Dom3 &d,
+                               int q, int x0, int y0, bool col_arrive) {
+    if constexpr (TMA) {
+      if (threadIdx.x == 0) {
+        fence_proxy_async();  // order earlier generic smem writes to this slot before the TMA
+        mbar_arrive_tx(bar(k), G::BOX_BYTES);
+        tma_load_3d(slot(k), map, x0 - G::PAD, y0 - 1, q, bar(k));
+      }
+      if (col_arrive && threadIdx.x >= 32 && threadIdx.x < 32 + 2 * G::TY) mbar_arrive(bar(k));
+    } else {
+      issue_plane<T, G>(slot(k), src, d, q, x0, y0, false);
+      cp_async_commit();
+    }
+  }
+  // Halo ring only of plane q into `dst_slot` (PERKS cached plane), completing on arrival k.
+  // TMA path: the two halo rows (corners included) by 1D bulk copies clipped to the domain
+  // (cells outside stay stale: they only feed frame cells, whose results are discarded); the
+  // two halo columns by per-thread cp.async of warp 1 (arrive.noinc on the slot's mbarrier).
+  PERKS_DEVINL void issue_halo(unsigned k, T *dst_slot, const T *src, const Dom3 &d, int q, int x0,
+                               int y0) {
+    if constexpr (TMA) {
+      if (threadIdx.x == 0) {
+        fence_proxy_async();
+        const bool zin = q >= 0 && q < d.nz;
+        const int xa = max(x0 - G::PAD, 0), xb = min(x0 + G::TX + G::PAD, d.nx);
+        const unsigned rb = (unsigned)((xb - xa) * (int)sizeof(T));
+        const bool top = zin && y0 >= 1, bot = zin && y0 + G::TY < d.ny;
+        mbar_arrive_tx(bar(k), (top ? rb : 0u) + (bot ? rb : 0u));
+        const size_t pl = (size_t)d.nx * d.ny;
+        if (top)
+          bulk_load(dst_slot + (xa - (x0 - G::PAD)), src + (size_t)q * pl + (size_t)(y0 - 1) * d.nx + xa, rb, bar(k));
+        if (bot)
+          bulk_load(dst_slot + (G::ROWS - 1) * G::P + (xa - (x0 - G::PAD)),
+                    src + (size_t)q * pl + (size_t)(y0 + G::TY) * d.nx + xa, rb, bar(k));
+      }
+      if (threadIdx.x >= 32 && threadIdx.x < 32 + 2 * G::TY) {
+        const int t = threadIdx.x - 32;
+        const int j = 1 + (t >> 1);
+        const bool right = t & 1;
+        const int y = y0 - 1 + j;
+        const int xx = right ? x0 + G::TX : x0 - 1;
+        const bool ok = q >= 0 && q < d.nz && y < d.ny && xx >= 0 && xx < d.nx;
+        const T *g = ok ? src + ((size_t)q * d.ny + y) * d.nx + xx : src;
+        cp_async<(int)sizeof(T)>(dst_slot + j * G::P + (right ? G::PAD + G::TX : G::PAD - 1), g, ok);
+        mbar_arrive_cpasync(bar(k));
+      }
+    } else {
+      issue_plane<T, G>(dst_slot, src, d, q, x0, y0, true);
+      cp_async_commit();
+    }
+  }
+  // Past the unit's last plane: cp.async commits an empty group so wait_group counting stays
+  // uniform; the TMA ring simply does not use the arrival index (indices stay contiguous).
+  PERKS_DEVINL void issue_none() {
+    if constexpr (!TMA) cp_async_commit();
+  }
+  // Wait until arrival k's data is resident and visible to all threads.
+  PERKS_DEVINL void wait(unsigned k) {
+    if constexpr (TMA) {
+      mbar_wait(bar(k), (k / G::NS) & 1u);
+      __syncthreads();  // also: everyone is done with the slot the next issue overwrites
+    } else {
+      cp_async_wait<G::NS - 2>();
+      __syncthreads();
+    }
+  }
+  PERKS_DEVINL void drain() {
+    if constexpr (!TMA) cp_async_wait<0>();
+  }
+};
+
+// Stream one unit (tile x0,y0; planes [zs, ze)) of one time step from src to dst (no caching).
+// Arrivals q = zs-1 .. ze; NS-1 planes in flight.
+template <typename T, int S, class G, bool TMA>
+PERKS_DEVINL void stream_unit(Ring<T, G, TMA> &ring, const T *__restrict__ src,
+                              const CUtensorMap *map, T *__restrict__ dst, const Dom3 &d, int x0,
+                              int y0, int zs, int ze, const Coef<T, Shape<S>::N> &c,
+                              bool col_arrive = false) {
   constexpr int D = G::NS - 1;
-  const int q0 = zs - 1, qn = ze;  // arrivals q0..qn inclusive
-  const int narr = qn - q0 + 1;
+  const int q0 = zs - 1;
+  const int narr = ze - zs + 2;
+  const unsigned k0 = ring.gk;
+  ThreadTile<G> tt;
+  tt.init(d, x0, y0);
 #pragma unroll
   for (int k = 0; k < D; k++) {
-    if (k < narr) issue_plane<T, G>(smem + (size_t)(k % G::NS) * G::SLOT, src, d, q0 + k, x0, y0, false);
-    cp_async_commit();
+    if (k < narr) ring.issue_full(k0 + k, src, map, d, q0 + k, x0, y0, col_arrive);
+    else ring.issue_none();
   }
   StreamState<T, G> st;
-#pragma unroll
-  for (int r = 0; r < G::R; r++)
-#pragma unroll
-    for (int i = 0; i < G::V; i++) st.accA[r][i] = st.accB[r][i] = st.accC[r][i] = st.cm1[r][i] = T(0);
+  st.zero();
   for (int k = 0; k < narr; k++) {
     const int q = q0 + k;
-    cp_async_wait<D - 1>();
-    __syncthreads();
-    if (k + D < narr)
-      issue_plane<T, G>(smem + (size_t)((k + D) % G::NS) * G::SLOT, src, d, q + D, x0, y0, false);
-    cp_async_commit();
+    ring.wait(k0 + k);
+    if (k + D < narr) ring.issue_full(k0 + k + D, src, map, d, q + D, x0, y0, col_arrive);
+    else ring.issue_none();
     T out[G::R][G::V], cq[G::R][G::V];
-    arrival<T, S, G>(st, smem + (size_t)(k % G::NS) * G::SLOT, c, out, cq);
-    if (q - 1 >= zs) store_plane<T, G>(dst, d, q - 1, x0, y0, out, st.cm1);
+    arrival<T, S, G>(st, ring.slot(k0 + k), c, out, cq);
+    if (q - 1 >= zs) {
+      frame_select<T, G>(d, tt, q - 1, out, st.cm1);
+      store_cells<T, G>(dst, d, tt, q - 1, out);
+    }
 #pragma unroll
     for (int r = 0; r < G::R; r++)
 #pragma unroll
       for (int i = 0; i < G::V; i++) st.cm1[r][i] = cq[r][i];
   }
-  cp_async_wait<0>();
+  ring.gk = k0 + narr;
+  ring.drain();
 }
 
 }  // namespace perks
