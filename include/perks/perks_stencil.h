@@ -123,6 +123,46 @@ perks_status perks_stencil_query(perks_stencil_t h, perks_variant variant, perks
 perks_status perks_stencil_launch_count(perks_stencil_t h, perks_variant variant, int64_t steps,
                                         int64_t *launches);
 
+/* ---- Multi-GPU slab decomposition (the paper's distributed suggestion) ----
+ * The global 3D domain is split along z (the slowest axis) into `nranks` slabs, rank r owning
+ * global planes [z_r, z_r + local nz).  `local` describes THIS rank's slab exactly as for
+ * perks_stencil_create (extent = {nx, ny, local nz}, local nz >= 2; nx*S a multiple of 16).
+ * The FRAME applies only at the global faces (rank 0's first plane, rank nranks-1's last plane);
+ * every other slab face is updated with the neighbour's plane as its halo, so the N-slab result
+ * equals the single-GPU result on the global domain bit-exactly (reading R12).
+ * Exchange: every step, the CTAs that produce a slab's first/last plane store it straight into
+ * the neighbour's library-owned ghost plane (P2P over NVLink when the neighbour is another GPU;
+ * ghost planes double-buffered by exchange parity) and then bump the neighbour's arrival counter
+ * with a system-scope release; only the CTAs that read a ghost plane wait (system-scope acquire),
+ * so the exchange overlaps the interior planes.  No NCCL call is on the data path.
+ * Ownership: the library allocates the ghost planes + counters (cudaMalloc, exportable by CUDA
+ * IPC) at create_dist and frees them at destroy.  Ranks must call perks_stencil_run collectively
+ * (same variant, same steps) after connecting; a rank that is not connected returns
+ * PERKS_ERR_COMM.  Device-side waits carry a watchdog (~10 s) that traps instead of hanging. */
+#define PERKS_DIST_BLOB_BYTES 128
+
+perks_status perks_stencil_create_dist(const perks_stencil_desc *local, int device, int rank,
+                                       int nranks, perks_stencil_t *out);
+/* Write this rank's connection blob (PERKS_DIST_BLOB_BYTES bytes, host memory): an IPC handle of
+ * the ghost/counter allocation plus its geometry.  Exchange blobs with the neighbours by any
+ * means (bench.py and the tests use torch.distributed all_gather). */
+perks_status perks_stencil_dist_export(perks_stencil_t h, void *blob);
+/* Connect to rank-1 (`lower_blob`) and rank+1 (`upper_blob`); pass NULL for a missing neighbour
+ * (rank 0's lower, rank nranks-1's upper).  Blobs from the same process are used as plain device
+ * pointers (peer access enabled if on another device); others are opened with cudaIpcOpenMemHandle.
+ * Geometry/dtype/rank mismatches return PERKS_ERR_COMM. */
+perks_status perks_stencil_dist_connect(perks_stencil_t h, const void *lower_blob,
+                                        const void *upper_blob);
+/* Run `n` handles that all live on ONE device together (single-GPU emulation of n slabs, used by
+ * the tests).  Host loop: the step kernels of all handles are interleaved in step order on
+ * `stream`.  Persistent/PERKS: one kernel per handle on its own internal stream, all resident
+ * together (create the handles with PERKS_NUM_SMS = SMs/n so their grids fit), joined back into
+ * `stream`.  Arrays are indexed like `hs`; semantics per handle as perks_stencil_run. */
+perks_status perks_stencil_run_group(const perks_stencil_t *hs, int n, perks_variant variant,
+                                     const void *const *d_in, void *const *d_out,
+                                     void *const *d_workspace, const size_t *workspace_bytes,
+                                     int64_t steps, void *stream);
+
 perks_status perks_stencil_destroy(perks_stencil_t h);
 const char *perks_status_string(perks_status s);
 /* Thread-local last cudaError_t behind PERKS_ERR_CUDA (0 if none). */

@@ -86,8 +86,12 @@ const Plan &get_plan(perks_stencil_s *h, perks_variant v) {
     Plan pl;
     if (v == PERKS_HOSTLOOP || v == PERKS_PERSISTENT)
       pl = p.ndim == 2 ? plan_stream2d(p, v) : plan_stream3d(p, v);
-    else if (v == PERKS_PERKS)
-      pl = p.ndim == 2 ? plan_perks2d(p) : plan_perks3d(p);
+    else if (v == PERKS_PERKS && p.ndim == 2) {
+      pl = plan_perks2d_cluster(p);  // small domains: one cluster, registers only
+      if (pl.ok) pl.family = 1;
+      else pl = plan_perks2d(p);
+    } else if (v == PERKS_PERKS)
+      pl = plan_perks3d(p);
     h->plans[i] = pl;
     h->planned[i] = true;
   }
@@ -181,6 +185,8 @@ perks_status perks_stencil_create(const perks_stencil_desc *d, int device, perks
     e = cudaDeviceGetAttribute(&p.num_sms, cudaDevAttrMultiProcessorCount, device);
     if (e == cudaSuccess)
       e = cudaDeviceGetAttribute(&p.max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    if (e == cudaSuccess)
+      e = cudaDeviceGetAttribute(&p.smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
     if (e != cudaSuccess) { delete h; return cuda_fail(e); }
     const int force_sms = env_int("PERKS_NUM_SMS", 0);  // sweeps only
     if (force_sms > 0 && force_sms < p.num_sms) p.num_sms = force_sms;
@@ -265,8 +271,11 @@ perks_status perks_stencil_run(perks_stencil_t h, perks_variant v, const void *d
                       : run_stream3d(p, pl, d_in, d_out, d_ws, steps, s);
       break;
     case PERKS_PERKS:
-      e = p.ndim == 2 ? run_perks2d(p, pl, d_in, d_out, d_ws, steps, s)
-                      : run_perks3d(p, pl, d_in, d_out, d_ws, steps, s);
+      if (p.ndim == 2)
+        e = pl.family == 1 ? run_perks2d_cluster(p, pl, d_in, d_out, steps, s)
+                           : run_perks2d(p, pl, d_in, d_out, d_ws, steps, s);
+      else
+        e = run_perks3d(p, pl, d_in, d_out, d_ws, steps, s);
       break;
     default:
       return PERKS_ERR_INVALID_ARGUMENT;

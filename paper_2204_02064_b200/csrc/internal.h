@@ -21,6 +21,7 @@ struct Problem {
   int device;
   int num_sms;
   int max_smem_optin;
+  int smem_per_sm;
   size_t elem() const { return dtype == PERKS_F64 ? 8 : 4; }
   int64_t cells() const { return nx * ny * nz; }
 };
@@ -36,6 +37,7 @@ struct Plan {
   int64_t units = 0;          // work units per step
   int zchunk = 0;             // planes per unit (3D)
   int cfg = 0;                // index of the kernel configuration
+  int family = 0;             // kernel family within a variant (2D PERKS: 0 tiles, 1 cluster)
   int64_t cached_reg = 0, cached_smem = 0;
   double dram_bytes_step = 0, halo_bytes_step = 0;
   size_t ws_bytes = 0;
@@ -57,6 +59,10 @@ cudaError_t run_stream3d(const Problem &p, const Plan &pl, const void *in, void 
 Plan plan_perks2d(const Problem &p);
 cudaError_t run_perks2d(const Problem &p, const Plan &pl, const void *in, void *out, void *ws,
                         int64_t steps, cudaStream_t s);
+// PERKS (c), 2D small domains: the whole domain in one thread-block cluster's registers.
+Plan plan_perks2d_cluster(const Problem &p);
+cudaError_t run_perks2d_cluster(const Problem &p, const Plan &pl, const void *in, void *out,
+                                int64_t steps, cudaStream_t s);
 // PERKS (c), 3D, partially cached plane streaming.
 Plan plan_perks3d(const Problem &p);
 cudaError_t run_perks3d(const Problem &p, const Plan &pl, const void *in, void *out, void *ws,

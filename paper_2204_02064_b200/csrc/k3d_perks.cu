@@ -36,6 +36,9 @@
 #ifndef PERKS_P3D_NRP
 #define PERKS_P3D_NRP 4
 #endif
+#ifndef PERKS_P3D_MINB
+#define PERKS_P3D_MINB 1
+#endif
 
 namespace perks {
 
@@ -114,7 +117,7 @@ PERKS_DEVINL void copy_cells(T (&a)[G::R][G::V], const T (&b)[G::R][G::V]) {
 }
 
 template <typename T, int S, bool TMA>
-__global__ void __launch_bounds__(KP3_THREADS, 1) perks3d_kernel(
+__global__ void __launch_bounds__(KP3_THREADS, PERKS_P3D_MINB) perks3d_kernel(
     const T *__restrict__ in, T *out, T *tmp, const __grid_constant__ Maps3 maps, Dom3 d,
     P3Units u, int64_t steps, unsigned *bar, Coef<T, Shape<S>::N> c) {
   using G = typename GP3Sel<T>::G;
@@ -142,7 +145,7 @@ __global__ void __launch_bounds__(KP3_THREADS, 1) perks3d_kernel(
   ThreadTile<G> tt;
   tt.init(d, x0, y0);
 
-  T reg[NRP][G::R][G::V];
+  T reg[NRP > 0 ? NRP : 1][G::R][G::V];
   // ---- prologue: cached planes from `in` (one-time load half of 2·D_cache)
   {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -213,7 +216,7 @@ __global__ void __launch_bounds__(KP3_THREADS, 1) perks3d_kernel(
         if (nreg > 0 && k == 1) slot_put<T, G>(ring.slot(k0 + 2), reg[0]);
         copy_cells<T, G>(st.cm1, cq);
       }
-      if (nreg > 0) {
+      if (NRP > 0 && nreg > 0) {
         // phase B: REG planes j = 0..NRP-1 (arrival k = 2 + j), statically indexed
 #pragma unroll
         for (int j = 0; j < NRP; j++) {
@@ -236,7 +239,7 @@ __global__ void __launch_bounds__(KP3_THREADS, 1) perks3d_kernel(
           step_arrival(k, outv, cq);
           frame_select<T, G>(d, tt, zr0 + NRP - 1, outv, st.cm1);
           publish_perimeter<T, G>(dst, d, zr0 + NRP - 1, x0, y0, outv);
-          copy_cells<T, G>(reg[NRP - 1], outv);
+          copy_cells<T, G>(reg[NRP > 0 ? NRP - 1 : 0], outv);
           copy_cells<T, G>(st.cm1, cq);
           k++;
         }
@@ -315,16 +318,18 @@ Plan plan_perks3d(const Problem &p) {
   const P3Geo g = p.dtype == PERKS_F32 ? p3geo<float>() : p3geo<double>();
   void *k = p.dtype == PERKS_F32 ? kp3<float>(p.shape, tma) : kp3<double>(p.shape, tma);
   P3Units u{};
-  p3_units(p, g, p.num_sms, u);
+  const int cps = PERKS_P3D_MINB;  // CTAs per SM
+  p3_units(p, g, cps * p.num_sms, u);
   const int units = u.tx * u.ty * u.nzc;
-  const int grid = std::min(units, p.num_sms);
+  const int grid = std::min(units, cps * p.num_sms);
   // cache budget: whatever shared memory the ring leaves (one CTA per SM); REG planes if the chunk
   // has room after its first and last (never cached) planes
   const int eligible = std::max(0, u.zc - 2);
   const int forced_nsm = env_int("PERKS_P3D_NSM", -1);
   u.nreg = (eligible >= g.NRP && env_int("PERKS_P3D_NOREG", 0) == 0) ? g.NRP : 0;
   const size_t ring = (size_t)g.NS * g.slot_bytes + 128;
-  int nsm = (int)(((size_t)p.max_smem_optin - ring) / g.slot_bytes);
+  const size_t per_cta = std::min<size_t>((size_t)p.max_smem_optin, (size_t)p.smem_per_sm / cps - 1024);
+  int nsm = (int)((per_cta - ring) / g.slot_bytes);
   nsm = std::max(0, std::min(nsm, eligible - u.nreg));
   if (forced_nsm >= 0) nsm = std::min(nsm, forced_nsm);
   u.nsm = nsm;
@@ -336,10 +341,10 @@ Plan plan_perks3d(const Problem &p) {
   if (cudaFuncGetAttributes(&fa, k) != cudaSuccess) { pl.why = "cudaFuncGetAttributes"; return pl; }
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, g.NT, smem);
-  if (occ < 1) { pl.why = "perks3d: not co-resident"; return pl; }
+  if (occ < cps) { pl.why = "perks3d: not co-resident"; return pl; }
   pl.grid = grid;
   pl.block = g.NT;
-  pl.ctas_per_sm = 1;
+  pl.ctas_per_sm = cps;
   pl.tile[0] = g.TX; pl.tile[1] = g.TY; pl.tile[2] = u.zc;
   pl.regs = fa.numRegs;
   pl.smem = (int)smem;
@@ -369,7 +374,7 @@ static cudaError_t launch_p3(const Problem &p, const Plan &pl, const T *in, T *o
   for (int i = 0; i < Shape<S>::N; i++) c.w[i] = sizeof(T) == 4 ? (T)p.wf[i] : (T)p.wd[i];
   Dom3 d{(int)p.nx, (int)p.ny, (int)p.nz};
   P3Units u{};
-  p3_units(p, g, p.num_sms, u);
+  p3_units(p, g, PERKS_P3D_MINB * p.num_sms, u);
   const bool tma = (pl.cfg >> 30) & 1;
   u.nreg = (pl.cfg >> 16) & 0x3fff;
   u.nsm = pl.cfg & 0xffff;

@@ -29,6 +29,7 @@ static_assert(G3Sel<float>::G::NT == K3D_THREADS && G3Sel<double>::G::NT == K3D_
 
 struct Units3 {
   int tx, ty, nzc, zc;
+  int rev;  // zig-zag experiment: 1 = reversed unit order (odd steps)
 };
 
 PERKS_DEVINL void unit_coords(const Units3 &u, int id, int tile_x, int tile_y, int &x0, int &y0,
@@ -55,7 +56,8 @@ __global__ void __launch_bounds__(K3D_THREADS) hostloop3d_kernel(const T *__rest
   Ring<T, G, TMA> ring;
   ring.init(reinterpret_cast<T *>(smem_raw), ring_bars<G>(smem_raw), 0);
   int x0, y0, zs;
-  unit_coords(u, blockIdx.x, G::TX, G::TY, x0, y0, zs);
+  const int nunits = u.tx * u.ty * u.nzc;
+  unit_coords(u, u.rev ? nunits - 1 - (int)blockIdx.x : (int)blockIdx.x, G::TX, G::TY, x0, y0, zs);
   const int ze = min(zs + u.zc, d.nz);
   stream_unit<T, S, G, TMA>(ring, src, &maps.box[src_idx], dst, d, x0, y0, zs, ze, c);
 }
@@ -76,7 +78,7 @@ __global__ void __launch_bounds__(K3D_THREADS) persistent3d_kernel(
     T *dst = ((steps - 1 - t) & 1) == 0 ? out : tmp;
     for (int id = blockIdx.x; id < nunits; id += gridDim.x) {
       int x0, y0, zs;
-      unit_coords(u, id, G::TX, G::TY, x0, y0, zs);
+      unit_coords(u, (u.rev && (t & 1)) ? nunits - 1 - id : id, G::TX, G::TY, x0, y0, zs);
       const int ze = min(zs + u.zc, d.nz);
       __syncthreads();  // slots of the previous unit are free
       stream_unit<T, S, G, TMA>(ring, src, &maps.box[src_idx], dst, d, x0, y0, zs, ze, c);
@@ -213,7 +215,8 @@ static cudaError_t launch3d(const Problem &p, const Plan &pl, const T *in, T *ou
   Coef<T, Shape<S>::N> c;
   for (int i = 0; i < Shape<S>::N; i++) c.w[i] = sizeof(T) == 4 ? (T)p.wf[i] : (T)p.wd[i];
   Dom3 d{(int)p.nx, (int)p.ny, (int)p.nz};
-  Units3 u{(int)((p.nx + G::TX - 1) / G::TX), (int)((p.ny + G::TY - 1) / G::TY), 0, pl.zchunk};
+  Units3 u{(int)((p.nx + G::TX - 1) / G::TX), (int)((p.ny + G::TY - 1) / G::TY), 0, pl.zchunk, 0};
+  const int zigzag = env_int("PERKS_ZIGZAG", 0);
   u.nzc = (int)((p.nz + u.zc - 1) / u.zc);
   const size_t smem = (size_t)pl.smem;
   const bool tma = pl.cfg == 1;
@@ -226,6 +229,7 @@ static cudaError_t launch3d(const Problem &p, const Plan &pl, const T *in, T *ou
       const bool src_out = t > 0 && ((steps - t) & 1) == 0;
       const T *src = t == 0 ? in : (src_out ? out : tmp);
       int src_idx = t == 0 ? 0 : (src_out ? 1 : 2);
+      u.rev = zigzag && (t & 1);
       T *dst = (((steps - 1 - t) & 1) == 0) ? out : tmp;
       void *args[] = {(void *)&src, (void *)&maps, (void *)&src_idx, (void *)&dst, (void *)&d,
                       (void *)&u, (void *)&c};
@@ -235,6 +239,7 @@ static cudaError_t launch3d(const Problem &p, const Plan &pl, const T *in, T *ou
     return cudaSuccess;
   }
   void *k = tma ? (void *)persistent3d_kernel<T, S, true> : (void *)persistent3d_kernel<T, S, false>;
+  u.rev = zigzag;
   cudaError_t e = cudaMemsetAsync(bar, 0, 256, s);
   if (e != cudaSuccess) return e;
   void *args[] = {(void *)&in, (void *)&out, (void *)&tmp, (void *)&maps, (void *)&d, (void *)&u,

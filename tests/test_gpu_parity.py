@@ -54,7 +54,7 @@ def _check(gpu, ref, u0, dtype, exact=True):
         assert nbad == 0, f"{nbad} cells differ from the oracle (max rel {rel})"
 
 
-CASES_2D = [(3, 3), (5, 7), (17, 33), (67, 131), (130, 260), (257, 300)]
+CASES_2D = [(3, 3), (5, 7), (17, 33), (67, 131), (128, 128), (130, 260), (257, 300), (500, 100)]
 CASES_3D = [(3, 3, 3), (5, 6, 7), (9, 17, 33), (20, 35, 70), (34, 40, 132)]
 
 
@@ -170,3 +170,21 @@ def test_run_host_e2e():
     ref = oracle.run(u0, offs, w, 6)
     assert np.array_equal(got, ref)
     st.close()
+
+
+@pytest.mark.parametrize("shape,dtype,name", [((128, 128), np.float64, "2d5pt"),
+                                              ((500, 250), np.float32, "2d9pt"),
+                                              ((9, 33), np.float64, "2d9pt")])
+def test_small_domain_uses_cluster_kernel(shape, dtype, name):
+    """Small 2D domains run in one thread-block cluster (registers + DSMEM halo, cluster barrier),
+    bit-exact vs the oracle for a long run (T=100, the C1 step count)."""
+    _need_gpu()
+    from paper_2204_02064_b200 import Stencil
+    offs, w = si.preset(name)
+    st = Stencil(shape, offs, w, dtype=dtype)
+    q = st.query("perks")
+    st.close()
+    assert q["kernel"].startswith("perks2d_cluster"), q
+    u0 = si.field(shape, dtype=dtype, seed=404)
+    ref = oracle.run(u0, offs, w, 100, nthreads=4)
+    _check(_run_gpu(u0, name, w, 100, "perks"), ref, u0, dtype)
