@@ -5,11 +5,11 @@ loop as three sm_100a execution variants (host loop / persistent / PERKS) behind
 ``Stencil`` and ``run`` load the CUDA library on first use and raise if it is missing — there
 is no CPU fallback.  ``model`` (the paper's §4 performance model) is pure Python.
 """
-__all__ = ["Stencil", "run", "VARIANTS", "model", "build"]
+__all__ = ["Stencil", "run", "run_group", "VARIANTS", "model", "build"]
 
 
 def __getattr__(name):
-    if name in ("Stencil", "run"):
+    if name in ("Stencil", "run", "run_group"):
         from . import stencil
 
         return getattr(stencil, name)

@@ -20,6 +20,7 @@ STATUS_NAMES = {
 }
 F32, F64 = 0, 1
 BC_FRAME, BC_PERIODIC = 0, 1
+DIST_BLOB_BYTES = 128  # PERKS_DIST_BLOB_BYTES
 VARIANTS = {"auto": 0, "hostloop": 1, "persistent": 2, "perks": 3}
 VARIANT_NAMES = {v: k for k, v in VARIANTS.items()}
 
@@ -66,6 +67,14 @@ SIGNATURES = {
     "perks_stencil_query": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.POINTER(PlanInfo)]),
     "perks_stencil_launch_count": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.c_int64,
                                                   ctypes.POINTER(ctypes.c_int64)]),
+    "perks_stencil_create_dist": (ctypes.c_int, [ctypes.POINTER(Desc), ctypes.c_int, ctypes.c_int,
+                                                 ctypes.c_int, ctypes.POINTER(_VP)]),
+    "perks_stencil_dist_export": (ctypes.c_int, [_VP, _VP]),
+    "perks_stencil_dist_connect": (ctypes.c_int, [_VP, _VP, _VP]),
+    "perks_stencil_run_group": (ctypes.c_int, [ctypes.POINTER(_VP), ctypes.c_int, ctypes.c_int,
+                                               ctypes.POINTER(_VP), ctypes.POINTER(_VP),
+                                               ctypes.POINTER(_VP), ctypes.POINTER(ctypes.c_size_t),
+                                               ctypes.c_int64, _VP]),
     "perks_stencil_destroy": (ctypes.c_int, [_VP]),
     "perks_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "perks_last_cuda_error": (ctypes.c_int, []),

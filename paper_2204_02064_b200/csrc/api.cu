@@ -4,11 +4,14 @@
 // error kept in a thread-local (perks_last_cuda_error).
 #include <cuda_runtime.h>
 
+#include <unistd.h>
+
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
+#include <vector>
 
 #include "internal.h"
 #include "shapes.cuh"
@@ -25,8 +28,31 @@ using namespace perks;
 
 static thread_local int g_last_cuda = 0;
 
+// Multi-GPU slab state of a handle (device side in dist.cuh).
+struct DistState {
+  bool on = false, connected = false;
+  void *alloc = nullptr;          // ghost planes G[4][ny][nx] + counters [2] (one cudaMalloc)
+  size_t ghost_bytes = 0, alloc_bytes = 0;
+  void *lo_base = nullptr, *hi_base = nullptr;  // neighbours' allocations mapped here
+  bool lo_ipc = false, hi_ipc = false;          // opened with cudaIpcOpenMemHandle
+  unsigned long long xbase = 0;   // exchanges done so far (each run of T steps does T + 1)
+};
+
+// Connection blob (PERKS_DIST_BLOB_BYTES): what a neighbour needs to map our ghost planes.
+struct DistBlob {
+  uint32_t magic, version;
+  int32_t pid, device, rank, nranks;
+  int64_t nx, ny;
+  int32_t dtype, pad;
+  uint64_t dev_ptr, ghost_bytes;
+  cudaIpcMemHandle_t ipc;
+};
+static_assert(sizeof(DistBlob) <= PERKS_DIST_BLOB_BYTES, "blob size");
+constexpr uint32_t kBlobMagic = 0x504b5344u;  // "PKSD"
+
 struct perks_stencil_s {
   Problem p;
+  DistState dist;
   std::mutex mu;
   Plan plans[4];
   bool planned[4] = {false, false, false, false};
@@ -34,6 +60,7 @@ struct perks_stencil_s {
   void *h_in = nullptr, *h_out = nullptr, *h_ws = nullptr;
   size_t h_ws_bytes = 0;
   cudaStream_t h_stream = nullptr;
+  std::vector<cudaStream_t> g_streams;  // run_group: this handle's private launch stream
 };
 
 namespace {
@@ -78,6 +105,8 @@ int find_shape(int ndim, const int32_t *off, int n) {
   return -1;
 }
 
+bool dist_perks_ok(perks_stencil_s *h);
+
 const Plan &get_plan(perks_stencil_s *h, perks_variant v) {
   std::lock_guard<std::mutex> lk(h->mu);
   const int i = (int)v;
@@ -100,8 +129,27 @@ const Plan &get_plan(perks_stencil_s *h, perks_variant v) {
 
 perks_variant resolve(perks_stencil_s *h, perks_variant v) {
   if (v != PERKS_AUTO) return v;
+  if (h->dist.on && !dist_perks_ok(h)) return PERKS_PERSISTENT;
   if (get_plan(h, PERKS_PERKS).ok) return PERKS_PERKS;
   return PERKS_PERSISTENT;
+}
+
+bool dist_perks_ok(perks_stencil_s *h) { return get_plan(h, PERKS_PERKS).ok && get_plan(h, PERKS_PERKS).family == 2; }
+
+DistRun dist_run(perks_stencil_s *h) {
+  DistRun r;
+  const DistState &ds = h->dist;
+  const Problem &p = h->p;
+  r.ghost = ds.alloc;
+  r.ctr = (unsigned long long *)((char *)ds.alloc + ds.ghost_bytes);
+  r.lo_ghost = ds.lo_base;
+  r.hi_ghost = ds.hi_base;
+  r.lo_ctr = ds.lo_base ? (unsigned long long *)((char *)ds.lo_base + ds.ghost_bytes) : nullptr;
+  r.hi_ctr = ds.hi_base ? (unsigned long long *)((char *)ds.hi_base + ds.ghost_bytes) : nullptr;
+  r.has_lo = p.rank > 0;
+  r.has_hi = p.rank < p.nranks - 1;
+  r.xbase = ds.xbase;
+  return r;
 }
 
 bool valid_variant(perks_variant v) {
@@ -132,7 +180,8 @@ const char *perks_status_string(perks_status s) {
   return "PERKS_ERR_UNKNOWN";
 }
 
-perks_status perks_stencil_create(const perks_stencil_desc *d, int device, perks_stencil_t *out) {
+static perks_status create_impl(const perks_stencil_desc *d, int device, int rank, int nranks,
+                                perks_stencil_t *out) {
   if (!d || !out) return PERKS_ERR_INVALID_ARGUMENT;
   *out = nullptr;
   if (d->ndim != 2 && d->ndim != 3) return PERKS_ERR_INVALID_ARGUMENT;
@@ -179,6 +228,8 @@ perks_status perks_stencil_create(const perks_stencil_desc *d, int device, perks
     p.wf[i] = (float)d->weights[i];  // reading R6: rounded once (RN-even) to the storage dtype
   }
   p.device = device;
+  p.rank = rank;
+  p.nranks = nranks;
   {
     DeviceGuard g(device);
     if (!g.ok) { delete h; return cuda_fail(cudaGetLastError()); }
@@ -192,6 +243,107 @@ perks_status perks_stencil_create(const perks_stencil_desc *d, int device, perks
     if (force_sms > 0 && force_sms < p.num_sms) p.num_sms = force_sms;
   }
   *out = h;
+  return PERKS_OK;
+}
+
+perks_status perks_stencil_create(const perks_stencil_desc *d, int device, perks_stencil_t *out) {
+  return create_impl(d, device, 0, 1, out);
+}
+
+perks_status perks_stencil_create_dist(const perks_stencil_desc *d, int device, int rank, int nranks,
+                                       perks_stencil_t *out) {
+  if (!d || !out || nranks < 1 || rank < 0 || rank >= nranks) return PERKS_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  if (d->ndim != 3) return d->ndim == 2 ? PERKS_ERR_UNSUPPORTED : PERKS_ERR_INVALID_ARGUMENT;
+  // a slab face with a neighbour is interior: the local slab needs only 2 planes (R9 applies to
+  // the global extent, which is >= 2 * nranks >= 3 for nranks >= 2)
+  perks_stencil_desc dd = *d;
+  const int64_t nz_local = d->extent[2];
+  if (nranks > 1) {
+    if (nz_local < 2) return PERKS_ERR_INVALID_DOMAIN;
+    if ((d->extent[0] * (d->dtype == PERKS_F64 ? 8 : 4)) % 16 != 0) return PERKS_ERR_UNSUPPORTED;
+    dd.extent[2] = nz_local < 3 ? 3 : nz_local;  // validate x/y and the point set as usual
+  }
+  perks_status st = create_impl(&dd, device, rank, nranks, out);
+  if (st != PERKS_OK) return st;
+  perks_stencil_s *h = *out;
+  h->p.nz = nz_local;
+  if (nranks == 1) return PERKS_OK;
+  DistState &ds = h->dist;
+  ds.on = true;
+  DeviceGuard g(device);
+  ds.ghost_bytes = align256((size_t)4 * h->p.nx * h->p.ny * h->p.elem());
+  ds.alloc_bytes = ds.ghost_bytes + 256;
+  cudaError_t e = cudaMalloc(&ds.alloc, ds.alloc_bytes);
+  if (e == cudaSuccess) e = cudaMemset(ds.alloc, 0, ds.alloc_bytes);
+  if (e != cudaSuccess) {
+    perks_stencil_destroy(h);
+    *out = nullptr;
+    return cuda_fail(e);
+  }
+  return PERKS_OK;
+}
+
+perks_status perks_stencil_dist_export(perks_stencil_t h, void *blob) {
+  if (!h || !blob || !h->dist.on) return PERKS_ERR_INVALID_ARGUMENT;
+  DeviceGuard g(h->p.device);
+  DistBlob b;
+  std::memset(&b, 0, sizeof(b));
+  b.magic = kBlobMagic;
+  b.version = 1;
+  b.pid = (int32_t)getpid();
+  b.device = h->p.device;
+  b.rank = h->p.rank;
+  b.nranks = h->p.nranks;
+  b.nx = h->p.nx;
+  b.ny = h->p.ny;
+  b.dtype = (int32_t)h->p.dtype;
+  b.dev_ptr = (uint64_t)(uintptr_t)h->dist.alloc;
+  b.ghost_bytes = h->dist.ghost_bytes;
+  cudaError_t e = cudaIpcGetMemHandle(&b.ipc, h->dist.alloc);
+  if (e != cudaSuccess) return cuda_fail(e);
+  std::memset(blob, 0, PERKS_DIST_BLOB_BYTES);
+  std::memcpy(blob, &b, sizeof(b));
+  return PERKS_OK;
+}
+
+static perks_status map_peer(perks_stencil_s *h, const void *blob, int want_rank, void **base, bool *ipc) {
+  DistBlob b;
+  std::memcpy(&b, blob, sizeof(b));
+  const Problem &p = h->p;
+  if (b.magic != kBlobMagic || b.version != 1 || b.rank != want_rank || b.nranks != p.nranks ||
+      b.nx != p.nx || b.ny != p.ny || b.dtype != (int32_t)p.dtype || b.ghost_bytes != h->dist.ghost_bytes)
+    return PERKS_ERR_COMM;
+  if (b.pid == (int32_t)getpid()) {
+    if (b.device != p.device) {
+      int ok = 0;
+      cudaDeviceCanAccessPeer(&ok, p.device, b.device);
+      if (!ok) return PERKS_ERR_COMM;
+      cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else if (e != cudaSuccess) return cuda_fail(e);
+    }
+    *base = (void *)(uintptr_t)b.dev_ptr;
+    *ipc = false;
+    return PERKS_OK;
+  }
+  cudaError_t e = cudaIpcOpenMemHandle(base, b.ipc, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return cuda_fail(e);
+  *ipc = true;
+  return PERKS_OK;
+}
+
+perks_status perks_stencil_dist_connect(perks_stencil_t h, const void *lower, const void *upper) {
+  if (!h || !h->dist.on) return PERKS_ERR_INVALID_ARGUMENT;
+  const Problem &p = h->p;
+  if ((p.rank > 0) != (lower != nullptr) || (p.rank < p.nranks - 1) != (upper != nullptr))
+    return PERKS_ERR_INVALID_ARGUMENT;
+  if (h->dist.connected) return PERKS_ERR_INVALID_ARGUMENT;
+  DeviceGuard g(p.device);
+  perks_status st = PERKS_OK;
+  if (lower && (st = map_peer(h, lower, p.rank - 1, &h->dist.lo_base, &h->dist.lo_ipc)) != PERKS_OK) return st;
+  if (upper && (st = map_peer(h, upper, p.rank + 1, &h->dist.hi_base, &h->dist.hi_ipc)) != PERKS_OK) return st;
+  h->dist.connected = true;
   return PERKS_OK;
 }
 
@@ -264,6 +416,15 @@ perks_status perks_stencil_run(perks_stencil_t h, perks_variant v, const void *d
   }
   if ((((uintptr_t)d_in) & 15) != 0 || (((uintptr_t)d_out) & 15) != 0) return PERKS_ERR_INVALID_ARGUMENT;
   cudaError_t e = cudaSuccess;
+  if (h->dist.on) {
+    if (!h->dist.connected) return PERKS_ERR_COMM;
+    DistRun dr = dist_run(h);
+    if (v == PERKS_PERKS) e = run_perks3d(p, pl, d_in, d_out, d_ws, steps, s, &dr);
+    else e = run_stream3d(p, pl, d_in, d_out, d_ws, steps, s, &dr);
+    if (e != cudaSuccess) return cuda_fail(e);
+    h->dist.xbase += (unsigned long long)steps + 1;  // prologue exchange + one per step
+    return PERKS_OK;
+  }
   switch (v) {
     case PERKS_HOSTLOOP:
     case PERKS_PERSISTENT:
@@ -321,6 +482,75 @@ perks_status perks_stencil_run_host(perks_stencil_t h, perks_variant v, const vo
   return PERKS_OK;
 }
 
+perks_status perks_stencil_run_group(const perks_stencil_t *hs, int n, perks_variant v,
+                                     const void *const *d_in, void *const *d_out,
+                                     void *const *d_ws, const size_t *ws_bytes, int64_t steps,
+                                     void *stream) {
+  if (!hs || n < 1 || !d_in || !d_out || !d_ws || !ws_bytes || !valid_variant(v) || steps < 0)
+    return PERKS_ERR_INVALID_ARGUMENT;
+  for (int i = 0; i < n; i++) {
+    if (!hs[i] || !d_in[i] || !d_out[i]) return PERKS_ERR_INVALID_ARGUMENT;
+    if (!hs[i]->dist.on || hs[i]->p.device != hs[0]->p.device || hs[i]->p.dtype != hs[0]->p.dtype ||
+        hs[i]->p.shape != hs[0]->p.shape)
+      return PERKS_ERR_INVALID_ARGUMENT;
+    if (!hs[i]->dist.connected) return PERKS_ERR_COMM;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  DeviceGuard g(hs[0]->p.device);
+  if (steps == 0) {
+    for (int i = 0; i < n; i++) {
+      perks_status st = perks_stencil_run(hs[i], v, d_in[i], d_out[i], d_ws[i], ws_bytes[i], 0, stream);
+      if (st != PERKS_OK) return st;
+    }
+    return PERKS_OK;
+  }
+  std::vector<const Problem *> ps(n);
+  std::vector<const Plan *> pls(n);
+  std::vector<DistRun> drs(n);
+  const perks_variant rv = resolve(hs[0], v);
+  for (int i = 0; i < n; i++) {
+    const Plan &pl = get_plan(hs[i], rv);
+    if (!pl.ok) return PERKS_ERR_UNSUPPORTED;
+    if (pl.ws_bytes > 0 && (!d_ws[i] || ws_bytes[i] < pl.ws_bytes || ((uintptr_t)d_ws[i] & 255) != 0))
+      return PERKS_ERR_WORKSPACE;
+    ps[i] = &hs[i]->p;
+    pls[i] = &pl;
+    drs[i] = dist_run(hs[i]);
+    drs[i].noncoop = 1;
+  }
+  cudaError_t e = cudaSuccess;
+  if (rv == PERKS_HOSTLOOP) {
+    e = run_stream3d_hostloop_group(ps.data(), pls.data(), d_in, d_out, d_ws, drs.data(), n, steps, s);
+  } else {
+    // one persistent kernel per slab, each on its own stream, all resident together
+    cudaEvent_t fork;
+    if ((e = cudaEventCreateWithFlags(&fork, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e);
+    cudaEventRecord(fork, s);
+    std::vector<cudaEvent_t> joins(n);
+    for (int i = 0; i < n && e == cudaSuccess; i++) {
+      perks_stencil_s *h = hs[i];
+      if (h->g_streams.empty()) {
+        cudaStream_t gs;
+        if ((e = cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking)) != cudaSuccess) break;
+        h->g_streams.push_back(gs);
+      }
+      cudaStream_t gs = h->g_streams[0];
+      cudaStreamWaitEvent(gs, fork, 0);
+      e = rv == PERKS_PERKS ? run_perks3d(*ps[i], *pls[i], d_in[i], d_out[i], d_ws[i], steps, gs, &drs[i])
+                            : run_stream3d(*ps[i], *pls[i], d_in[i], d_out[i], d_ws[i], steps, gs, &drs[i]);
+      if (e != cudaSuccess) break;
+      cudaEventCreateWithFlags(&joins[i], cudaEventDisableTiming);
+      cudaEventRecord(joins[i], gs);
+      cudaStreamWaitEvent(s, joins[i], 0);
+      cudaEventDestroy(joins[i]);
+    }
+    cudaEventDestroy(fork);
+  }
+  if (e != cudaSuccess) return cuda_fail(e);
+  for (int i = 0; i < n; i++) hs[i]->dist.xbase += (unsigned long long)steps + 1;
+  return PERKS_OK;
+}
+
 perks_status perks_stencil_destroy(perks_stencil_t h) {
   if (!h) return PERKS_ERR_INVALID_ARGUMENT;
   {
@@ -330,6 +560,10 @@ perks_status perks_stencil_destroy(perks_stencil_t h) {
     if (h->h_out) cudaFree(h->h_out);
     if (h->h_ws) cudaFree(h->h_ws);
     if (h->h_stream) cudaStreamDestroy(h->h_stream);
+    for (cudaStream_t gs : h->g_streams) cudaStreamDestroy(gs);
+    if (h->dist.lo_ipc && h->dist.lo_base) cudaIpcCloseMemHandle(h->dist.lo_base);
+    if (h->dist.hi_ipc && h->dist.hi_base) cudaIpcCloseMemHandle(h->dist.hi_base);
+    if (h->dist.alloc) cudaFree(h->dist.alloc);
   }
   delete h;
   return PERKS_OK;

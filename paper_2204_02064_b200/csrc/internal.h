@@ -19,6 +19,7 @@ struct Problem {
   double wd[27];      // weights rounded to f64 (identity)
   float wf[27];       // weights rounded once to f32 (reading R6)
   int device;
+  int rank = 0, nranks = 1;  // multi-GPU slab decomposition along z
   int num_sms;
   int max_smem_optin;
   int smem_per_sm;
@@ -46,6 +47,18 @@ struct Plan {
 
 inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
+// Host view of one rank's exchange state for one run (multi-GPU slabs; device side: dist.cuh).
+struct DistRun {
+  void *ghost = nullptr;                      // local ghost planes G[4][ny][nx]
+  unsigned long long *ctr = nullptr;          // local arrival counters [2]
+  void *lo_ghost = nullptr, *hi_ghost = nullptr;  // neighbours' G (mapped into this process)
+  unsigned long long *lo_ctr = nullptr, *hi_ctr = nullptr;  // neighbours' counters [2]
+  unsigned long long xbase = 0;               // exchange index of this run's input
+  int has_lo = 0, has_hi = 0;
+  int noncoop = 0;                            // launch persistent kernels non-cooperatively
+                                              // (several slabs resident on ONE device)
+};
+
 // ---- launchers (return cudaSuccess or the failing CUDA error) ----
 // 2D row-strip streaming kernels: host-loop (a) and persistent (b).
 Plan plan_stream2d(const Problem &p, perks_variant v);
@@ -54,7 +67,13 @@ cudaError_t run_stream2d(const Problem &p, const Plan &pl, const void *in, void 
 // 3D plane streaming kernels: host-loop (a) and persistent (b).
 Plan plan_stream3d(const Problem &p, perks_variant v);
 cudaError_t run_stream3d(const Problem &p, const Plan &pl, const void *in, void *out, void *ws,
-                         int64_t steps, cudaStream_t s);
+                         int64_t steps, cudaStream_t s, const DistRun *dr = nullptr);
+// Host loop (a) on a group of same-device slab handles: step kernels interleaved in step order.
+cudaError_t run_stream3d_hostloop_group(const Problem *const *ps, const Plan *const *pls,
+                                        const void *const *in, void *const *out, void *const *ws,
+                                        const DistRun *drs, int n, int64_t steps, cudaStream_t s);
+// Multi-GPU: the exchange of the run's input faces (exchange xbase) before the first step.
+cudaError_t launch_dist_prologue(const Problem &p, const void *in, const DistRun &dr, cudaStream_t s);
 // PERKS (c), 2D, domain resident on chip.
 Plan plan_perks2d(const Problem &p);
 cudaError_t run_perks2d(const Problem &p, const Plan &pl, const void *in, void *out, void *ws,
@@ -66,7 +85,7 @@ cudaError_t run_perks2d_cluster(const Problem &p, const Plan &pl, const void *in
 // PERKS (c), 3D, partially cached plane streaming.
 Plan plan_perks3d(const Problem &p);
 cudaError_t run_perks3d(const Problem &p, const Plan &pl, const void *in, void *out, void *ws,
-                        int64_t steps, cudaStream_t s);
+                        int64_t steps, cudaStream_t s, const DistRun *dr = nullptr);
 
 // Environment override helper (sweeps only): returns def if unset.
 int env_int(const char *name, int def);

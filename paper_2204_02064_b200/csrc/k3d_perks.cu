@@ -55,7 +55,8 @@ constexpr int KP3_THREADS = 32 * PERKS_P3D_NWARP;
 
 bool use_tma3(const Problem &p);
 bool make_maps3(const Problem &p, int P, int ROWS, const void *in, const void *out, const void *tmp,
-                Maps3 *m);
+                Maps3 *m, const void *ghost);
+Dom3 make_dom3(const Problem &p);
 
 struct P3Units {
   int tx, ty, nzc, zc;  // tiles in x/y, z-chunks, planes per chunk
@@ -260,7 +261,7 @@ __global__ void __launch_bounds__(KP3_THREADS, PERKS_P3D_MINB) perks3d_kernel(
       const int ux0 = (tt2 % u.tx) * G::TX, uy0 = (tt2 / u.tx) * G::TY;
       const int uzs = zc * u.zc, uze = min(uzs + u.zc, d.nz);
       __syncthreads();
-      stream_unit<T, S, G, TMA>(ring, src, boxmap, dst, d, ux0, uy0, uzs, uze, c, true);
+      stream_unit<T, S, G, TMA, false>(ring, src, boxmap, dst, d, ux0, uy0, uzs, uze, c, DistStep{}, true);
     }
     if (t + 1 < steps) grid_barrier(bar, (unsigned)((t + 1) * gridDim.x));
   }
@@ -372,7 +373,7 @@ static cudaError_t launch_p3(const Problem &p, const Plan &pl, const T *in, T *o
   const P3Geo g = p3geo<T>();
   Coef<T, Shape<S>::N> c;
   for (int i = 0; i < Shape<S>::N; i++) c.w[i] = sizeof(T) == 4 ? (T)p.wf[i] : (T)p.wd[i];
-  Dom3 d{(int)p.nx, (int)p.ny, (int)p.nz};
+  Dom3 d = make_dom3(p);
   P3Units u{};
   p3_units(p, g, PERKS_P3D_MINB * p.num_sms, u);
   const bool tma = (pl.cfg >> 30) & 1;
@@ -382,7 +383,7 @@ static cudaError_t launch_p3(const Problem &p, const Plan &pl, const T *in, T *o
   unsigned *bar = (unsigned *)((char *)ws + align256((size_t)p.cells() * p.elem()));
   Maps3 maps;
   std::memset(&maps, 0, sizeof(maps));
-  if (tma && !make_maps3(p, g.P, g.ROWS, in, out, tmp, &maps)) return cudaErrorInvalidValue;
+  if (tma && !make_maps3(p, g.P, g.ROWS, in, out, tmp, &maps, nullptr)) return cudaErrorInvalidValue;
   cudaError_t e = cudaMemsetAsync(bar, 0, 256, s);
   if (e != cudaSuccess) return e;
   void *k = kp3<T>(p.shape, tma);
@@ -402,7 +403,8 @@ static cudaError_t launch_p3(const Problem &p, const Plan &pl, const T *in, T *o
 }
 
 cudaError_t run_perks3d(const Problem &p, const Plan &pl, const void *in, void *out, void *ws,
-                        int64_t steps, cudaStream_t s) {
+                        int64_t steps, cudaStream_t s, const DistRun *dr) {
+  if (dr) return cudaErrorNotSupported;
   if (p.dtype == PERKS_F32) {
     if (p.shape == SHAPE_3D7) return launch_p3<float, SHAPE_3D7>(p, pl, (const float *)in, (float *)out, ws, steps, s);
     return launch_p3<float, SHAPE_3D27>(p, pl, (const float *)in, (float *)out, ws, steps, s);

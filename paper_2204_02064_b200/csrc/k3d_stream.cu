@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "internal.h"
 #include "stream3d.cuh"
@@ -45,12 +46,13 @@ template <class G> PERKS_DEVINL uint64_t *ring_bars(unsigned char *smem) {
   return reinterpret_cast<uint64_t *>(smem + (size_t)G::NS * G::SLOT_BYTES);
 }
 
-template <typename T, int S, bool TMA>
-__global__ void __launch_bounds__(K3D_THREADS) hostloop3d_kernel(const T *__restrict__ src,
+template <typename T, int S, bool TMA, bool DIST>
+__global__ void __launch_bounds__(K3D_THREADS, (TMA && !DIST) ? 4 : 2) hostloop3d_kernel(const T *__restrict__ src,
                                                                  const __grid_constant__ Maps3 maps,
                                                                  int src_idx, T *__restrict__ dst,
                                                                  Dom3 d, Units3 u,
-                                                                 Coef<T, Shape<S>::N> c) {
+                                                                 Coef<T, Shape<S>::N> c, DistK dk,
+                                                                 unsigned long long e) {
   using G = typename G3Sel<T>::G;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Ring<T, G, TMA> ring;
@@ -59,13 +61,14 @@ __global__ void __launch_bounds__(K3D_THREADS) hostloop3d_kernel(const T *__rest
   const int nunits = u.tx * u.ty * u.nzc;
   unit_coords(u, u.rev ? nunits - 1 - (int)blockIdx.x : (int)blockIdx.x, G::TX, G::TY, x0, y0, zs);
   const int ze = min(zs + u.zc, d.nz);
-  stream_unit<T, S, G, TMA>(ring, src, &maps.box[src_idx], dst, d, x0, y0, zs, ze, c);
+  const DistStep ds{dk, &maps.ghost, e, (unsigned long long)d.nx * d.ny};
+  stream_unit<T, S, G, TMA, DIST>(ring, src, &maps.box[src_idx], dst, d, x0, y0, zs, ze, c, ds);
 }
 
-template <typename T, int S, bool TMA>
+template <typename T, int S, bool TMA, bool DIST>
 __global__ void __launch_bounds__(K3D_THREADS) persistent3d_kernel(
     const T *__restrict__ in, T *out, T *tmp, const __grid_constant__ Maps3 maps, Dom3 d, Units3 u,
-    int64_t steps, unsigned *bar, Coef<T, Shape<S>::N> c) {
+    int64_t steps, unsigned *bar, Coef<T, Shape<S>::N> c, DistK dk, unsigned long long xbase) {
   using G = typename G3Sel<T>::G;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Ring<T, G, TMA> ring;
@@ -76,15 +79,40 @@ __global__ void __launch_bounds__(K3D_THREADS) persistent3d_kernel(
     const T *src = t == 0 ? in : (src_out ? out : tmp);
     const int src_idx = t == 0 ? 0 : (src_out ? 1 : 2);
     T *dst = ((steps - 1 - t) & 1) == 0 ? out : tmp;
+    const DistStep ds{dk, &maps.ghost, xbase + (unsigned long long)t, (unsigned long long)d.nx * d.ny};
     for (int id = blockIdx.x; id < nunits; id += gridDim.x) {
       int x0, y0, zs;
       unit_coords(u, (u.rev && (t & 1)) ? nunits - 1 - id : id, G::TX, G::TY, x0, y0, zs);
       const int ze = min(zs + u.zc, d.nz);
       __syncthreads();  // slots of the previous unit are free
-      stream_unit<T, S, G, TMA>(ring, src, &maps.box[src_idx], dst, d, x0, y0, zs, ze, c);
+      stream_unit<T, S, G, TMA, DIST>(ring, src, &maps.box[src_idx], dst, d, x0, y0, zs, ze, c, ds);
     }
     if (t + 1 < steps) grid_barrier(bar, (unsigned)((t + 1) * gridDim.x));
   }
+}
+
+// Multi-GPU prologue: exchange xbase = the run's INPUT face planes.  blockIdx.y = side (0: plane 0
+// to the lower neighbour's ghost side 1; 1: plane nz-1 to the upper neighbour's ghost side 0);
+// each CTA copies 8 rows.  Before overwriting the neighbour's ghost parity, wait until that
+// neighbour's last exchange of the previous run arrived (it was produced after the neighbour's
+// last ghost read, so the slot is free: no write-after-read across runs).
+template <typename T>
+__global__ void __launch_bounds__(256) dist_prologue_kernel(const T *__restrict__ in, DistK dk, int nx,
+                                                            int ny, int nz, unsigned long long xbase) {
+  const int side = blockIdx.y;
+  if (side == 0 ? !dk.has_lo : !dk.has_hi) return;
+  const unsigned long long plane = (unsigned long long)nx * ny;
+  if (threadIdx.x == 0) wait_counter_sys(dk.ctr + side, xbase * plane);
+  __syncthreads();
+  const int y0 = blockIdx.x * 8, y1 = min(y0 + 8, ny);
+  const T *srcp = in + (side == 0 ? (size_t)0 : (size_t)(nz - 1) * plane) + (size_t)y0 * nx;
+  T *dstp = reinterpret_cast<T *>(side == 0 ? dk.send_lo : dk.send_hi) +
+            (size_t)((xbase & 1) * 2 + (side == 0 ? 1 : 0)) * plane + (size_t)y0 * nx;
+  const int n16 = (int)((size_t)(y1 - y0) * nx * sizeof(T) / 16);  // nx*S % 16 == 0 (planner)
+  const uint4 *s4 = reinterpret_cast<const uint4 *>(srcp);
+  uint4 *d4 = reinterpret_cast<uint4 *>(dstp);
+  for (int i = threadIdx.x; i < n16; i += blockDim.x) d4[i] = s4[i];
+  signal_counter_sys(side == 0 ? dk.peer_ctr_lo : dk.peer_ctr_hi, (unsigned long long)(y1 - y0) * nx);
 }
 
 // ------------------------------------------------------------------ TMA descriptors (host)
@@ -124,22 +152,65 @@ bool use_tma3(const Problem &p) {
 }
 
 bool make_maps3(const Problem &p, int P, int ROWS, const void *in, const void *out, const void *tmp,
-                Maps3 *m) {
+                Maps3 *m, const void *ghost) {
   const void *b[3] = {in, out, tmp ? tmp : out};
   for (int i = 0; i < 3; i++) {
     if (!encode_map3(&m->box[i], p, b[i], P, ROWS)) return false;
     if (!encode_map3(&m->row[i], p, b[i], P, 1)) return false;
   }
+  if (ghost) {  // G[4][ny][nx]
+    Problem g = p;
+    g.nz = 4;
+    if (!encode_map3(&m->ghost, g, ghost, P, ROWS)) return false;
+  }
   return true;
+}
+
+Dom3 make_dom3(const Problem &p) {
+  Dom3 d{(int)p.nx, (int)p.ny, (int)p.nz, 1, (int)p.nz - 2};
+  if (p.rank > 0) d.zlo = 0;                  // lower face has a neighbour: interior (R12)
+  if (p.rank < p.nranks - 1) d.zhi = (int)p.nz - 1;
+  return d;
+}
+
+DistK make_distk(const DistRun *dr) {
+  DistK k{};
+  if (!dr) return k;
+  k.ctr = dr->ctr;
+  k.has_lo = dr->has_lo;
+  k.has_hi = dr->has_hi;
+  k.send_lo = dr->lo_ghost;
+  k.send_hi = dr->hi_ghost;
+  k.peer_ctr_lo = dr->lo_ctr ? dr->lo_ctr + 1 : nullptr;  // I am the lower neighbour's upper
+  k.peer_ctr_hi = dr->hi_ctr ? dr->hi_ctr + 0 : nullptr;
+  return k;
+}
+
+cudaError_t launch_dist_prologue(const Problem &p, const void *in, const DistRun &dr, cudaStream_t s) {
+  if (!dr.has_lo && !dr.has_hi) return cudaSuccess;
+  DistK k = make_distk(&dr);
+  int nx = (int)p.nx, ny = (int)p.ny, nz = (int)p.nz;
+  unsigned long long xb = dr.xbase;
+  dim3 grid((unsigned)((ny + 7) / 8), 2);
+  if (p.dtype == PERKS_F32)
+    dist_prologue_kernel<float><<<grid, 256, 0, s>>>((const float *)in, k, nx, ny, nz, xb);
+  else
+    dist_prologue_kernel<double><<<grid, 256, 0, s>>>((const double *)in, k, nx, ny, nz, xb);
+  return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ host side
 namespace {
+template <typename T> void *kptr3d(int shape, bool persistent) {  // multi-GPU slab kernels (TMA)
+  if (shape == SHAPE_3D7)
+    return persistent ? (void *)persistent3d_kernel<T, SHAPE_3D7, true, true> : (void *)hostloop3d_kernel<T, SHAPE_3D7, true, true>;
+  return persistent ? (void *)persistent3d_kernel<T, SHAPE_3D27, true, true> : (void *)hostloop3d_kernel<T, SHAPE_3D27, true, true>;
+}
 template <typename T> void *kptr3(int shape, bool persistent, bool tma) {
 #define K3(S)                                                                                   \
   if (shape == S) {                                                                             \
-    if (persistent) return tma ? (void *)persistent3d_kernel<T, S, true> : (void *)persistent3d_kernel<T, S, false>; \
-    return tma ? (void *)hostloop3d_kernel<T, S, true> : (void *)hostloop3d_kernel<T, S, false>; \
+    if (persistent) return tma ? (void *)persistent3d_kernel<T, S, true, false> : (void *)persistent3d_kernel<T, S, false, false>; \
+    return tma ? (void *)hostloop3d_kernel<T, S, true, false> : (void *)hostloop3d_kernel<T, S, false, false>; \
   }
   K3(SHAPE_3D7)
   K3(SHAPE_3D27)
@@ -148,6 +219,7 @@ template <typename T> void *kptr3(int shape, bool persistent, bool tma) {
 }
 void *pick3(const Problem &p, bool persistent) {
   const bool tma = use_tma3(p);
+  if (p.nranks > 1) return p.dtype == PERKS_F32 ? kptr3d<float>(p.shape, persistent) : kptr3d<double>(p.shape, persistent);
   return p.dtype == PERKS_F32 ? kptr3<float>(p.shape, persistent, tma) : kptr3<double>(p.shape, persistent, tma);
 }
 template <typename T> size_t smem3() {
@@ -166,6 +238,7 @@ Plan plan_stream3d(const Problem &p, perks_variant v) {
     pl.why = "stream3d: needs 3D 7pt/27pt FRAME";
     return pl;
   }
+  if (p.nranks > 1 && !use_tma3(p)) { pl.why = "stream3d: multi-GPU slabs need TMA (nx*S % 16 == 0)"; return pl; }
   const bool persistent = v == PERKS_PERSISTENT;
   void *k = pick3(p, persistent);
   const size_t smem = p.dtype == PERKS_F32 ? smem3<float>() : smem3<double>();
@@ -208,67 +281,146 @@ Plan plan_stream3d(const Problem &p, perks_variant v) {
   return pl;
 }
 
+namespace {
+// Everything one 3D streaming launch needs, prepared once per run.
 template <typename T, int S>
-static cudaError_t launch3d(const Problem &p, const Plan &pl, const T *in, T *out, T *tmp,
-                            unsigned *bar, int64_t steps, cudaStream_t s) {
+struct Launch3 {
   using G = typename G3Sel<T>::G;
   Coef<T, Shape<S>::N> c;
-  for (int i = 0; i < Shape<S>::N; i++) c.w[i] = sizeof(T) == 4 ? (T)p.wf[i] : (T)p.wd[i];
-  Dom3 d{(int)p.nx, (int)p.ny, (int)p.nz};
-  Units3 u{(int)((p.nx + G::TX - 1) / G::TX), (int)((p.ny + G::TY - 1) / G::TY), 0, pl.zchunk, 0};
-  const int zigzag = env_int("PERKS_ZIGZAG", 0);
-  u.nzc = (int)((p.nz + u.zc - 1) / u.zc);
-  const size_t smem = (size_t)pl.smem;
-  const bool tma = pl.cfg == 1;
+  Dom3 d;
+  Units3 u;
   Maps3 maps;
-  std::memset(&maps, 0, sizeof(maps));
-  if (tma && !make_maps3(p, G::P, G::ROWS, in, out, tmp, &maps)) return cudaErrorInvalidValue;
-  if (pl.variant == PERKS_HOSTLOOP) {
-    void *k = tma ? (void *)hostloop3d_kernel<T, S, true> : (void *)hostloop3d_kernel<T, S, false>;
-    for (int64_t t = 0; t < steps; t++) {
-      const bool src_out = t > 0 && ((steps - t) & 1) == 0;
-      const T *src = t == 0 ? in : (src_out ? out : tmp);
-      int src_idx = t == 0 ? 0 : (src_out ? 1 : 2);
-      u.rev = zigzag && (t & 1);
-      T *dst = (((steps - 1 - t) & 1) == 0) ? out : tmp;
-      void *args[] = {(void *)&src, (void *)&maps, (void *)&src_idx, (void *)&dst, (void *)&d,
-                      (void *)&u, (void *)&c};
-      cudaError_t e = cudaLaunchKernel(k, dim3(pl.grid), dim3(G::NT), args, smem, s);
-      if (e != cudaSuccess) return e;
-    }
+  DistK dk;
+  unsigned long long xbase = 0;
+  const T *in;
+  T *out, *tmp;
+  unsigned *bar;
+  size_t smem;
+  bool tma;
+  int grid;
+  int zigzag;
+
+  cudaError_t setup(const Problem &p, const Plan &pl, const T *in_, T *out_, T *tmp_, unsigned *bar_,
+                    const DistRun *dr) {
+    for (int i = 0; i < Shape<S>::N; i++) c.w[i] = sizeof(T) == 4 ? (T)p.wf[i] : (T)p.wd[i];
+    d = make_dom3(p);
+    u = Units3{(int)((p.nx + G::TX - 1) / G::TX), (int)((p.ny + G::TY - 1) / G::TY), 0, pl.zchunk, 0};
+    u.nzc = (int)((p.nz + u.zc - 1) / u.zc);
+    zigzag = env_int("PERKS_ZIGZAG", 0);  // experiment knob; off by default
+    smem = (size_t)pl.smem;
+    tma = pl.cfg == 1;
+    grid = pl.grid;
+    in = in_; out = out_; tmp = tmp_; bar = bar_;
+    dk = make_distk(dr);
+    xbase = dr ? dr->xbase : 0;
+    dist = p.nranks > 1;
+    if (dist && !tma) return cudaErrorNotSupported;
+    std::memset(&maps, 0, sizeof(maps));
+    if (tma && !make_maps3(p, G::P, G::ROWS, in, out, tmp, &maps, dr ? dr->ghost : nullptr))
+      return cudaErrorInvalidValue;
     return cudaSuccess;
   }
-  void *k = tma ? (void *)persistent3d_kernel<T, S, true> : (void *)persistent3d_kernel<T, S, false>;
-  u.rev = zigzag;
-  cudaError_t e = cudaMemsetAsync(bar, 0, 256, s);
-  if (e != cudaSuccess) return e;
-  void *args[] = {(void *)&in, (void *)&out, (void *)&tmp, (void *)&maps, (void *)&d, (void *)&u,
-                  (void *)&steps, (void *)&bar, (void *)&c};
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(pl.grid);
-  cfg.blockDim = dim3(G::NT);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelExC(&cfg, k, args);
-}
+  // host loop (a): the kernel of step t of `steps`
+  bool dist = false;
+  cudaError_t step(int64_t t, int64_t steps, cudaStream_t s) {
+    void *k = dist ? (void *)hostloop3d_kernel<T, S, true, true>
+                   : tma ? (void *)hostloop3d_kernel<T, S, true, false> : (void *)hostloop3d_kernel<T, S, false, false>;
+    const bool src_out = t > 0 && ((steps - t) & 1) == 0;
+    const T *src = t == 0 ? in : (src_out ? out : tmp);
+    int src_idx = t == 0 ? 0 : (src_out ? 1 : 2);
+    T *dst = (((steps - 1 - t) & 1) == 0) ? out : tmp;
+    Units3 uu = u;
+    uu.rev = zigzag && (t & 1);
+    unsigned long long e = xbase + (unsigned long long)t;
+    void *args[] = {(void *)&src, (void *)&maps, (void *)&src_idx, (void *)&dst, (void *)&d,
+                    (void *)&uu, (void *)&c, (void *)&dk, (void *)&e};
+    return cudaLaunchKernel(k, dim3(grid), dim3(G::NT), args, smem, s);
+  }
+  // persistent (b): one launch; cooperative on a single GPU (co-residency guaranteed by the driver)
+  cudaError_t persistent(int64_t steps, cudaStream_t s, bool cooperative) {
+    void *k = dist ? (void *)persistent3d_kernel<T, S, true, true>
+                   : tma ? (void *)persistent3d_kernel<T, S, true, false> : (void *)persistent3d_kernel<T, S, false, false>;
+    Units3 uu = u;
+    uu.rev = zigzag;
+    cudaError_t e = cudaMemsetAsync(bar, 0, 256, s);
+    if (e != cudaSuccess) return e;
+    void *args[] = {(void *)&in, (void *)&out, (void *)&tmp, (void *)&maps, (void *)&d, (void *)&uu,
+                    (void *)&steps, (void *)&bar, (void *)&c, (void *)&dk, (void *)&xbase};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(G::NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = cooperative ? 1 : 0;
+    return cudaLaunchKernelExC(&cfg, k, args);
+  }
+};
 
-cudaError_t run_stream3d(const Problem &p, const Plan &pl, const void *in, void *out, void *ws,
-                         int64_t steps, cudaStream_t s) {
+template <typename T, int S>
+cudaError_t run3(const Problem &p, const Plan &pl, const void *in, void *out, void *ws, int64_t steps,
+                 cudaStream_t s, const DistRun *dr) {
   char *w = (char *)ws;
   unsigned *bar = (unsigned *)(w + align256((size_t)p.cells() * p.elem()));
-  if (p.dtype == PERKS_F32) {
-    if (p.shape == SHAPE_3D7)
-      return launch3d<float, SHAPE_3D7>(p, pl, (const float *)in, (float *)out, (float *)w, bar, steps, s);
-    return launch3d<float, SHAPE_3D27>(p, pl, (const float *)in, (float *)out, (float *)w, bar, steps, s);
+  Launch3<T, S> L;
+  cudaError_t e = L.setup(p, pl, (const T *)in, (T *)out, (T *)w, bar, dr);
+  if (e != cudaSuccess) return e;
+  if (dr && (e = launch_dist_prologue(p, in, *dr, s)) != cudaSuccess) return e;
+  if (pl.variant == PERKS_HOSTLOOP) {
+    for (int64_t t = 0; t < steps; t++)
+      if ((e = L.step(t, steps, s)) != cudaSuccess) return e;
+    return cudaSuccess;
   }
-  if (p.shape == SHAPE_3D7)
-    return launch3d<double, SHAPE_3D7>(p, pl, (const double *)in, (double *)out, (double *)w, bar, steps, s);
-  return launch3d<double, SHAPE_3D27>(p, pl, (const double *)in, (double *)out, (double *)w, bar, steps, s);
+  return L.persistent(steps, s, !(dr && dr->noncoop));
+}
+}  // namespace
+
+cudaError_t run_stream3d(const Problem &p, const Plan &pl, const void *in, void *out, void *ws,
+                         int64_t steps, cudaStream_t s, const DistRun *dr) {
+  if (p.dtype == PERKS_F32)
+    return p.shape == SHAPE_3D7 ? run3<float, SHAPE_3D7>(p, pl, in, out, ws, steps, s, dr)
+                                : run3<float, SHAPE_3D27>(p, pl, in, out, ws, steps, s, dr);
+  return p.shape == SHAPE_3D7 ? run3<double, SHAPE_3D7>(p, pl, in, out, ws, steps, s, dr)
+                              : run3<double, SHAPE_3D27>(p, pl, in, out, ws, steps, s, dr);
+}
+
+namespace {
+template <typename T, int S>
+cudaError_t group3(const Problem *const *ps, const Plan *const *pls, const void *const *in,
+                   void *const *out, void *const *ws, const DistRun *drs, int n, int64_t steps,
+                   cudaStream_t s) {
+  std::vector<Launch3<T, S>> L(n);
+  for (int i = 0; i < n; i++) {
+    char *w = (char *)ws[i];
+    unsigned *bar = (unsigned *)(w + align256((size_t)ps[i]->cells() * ps[i]->elem()));
+    cudaError_t e = L[i].setup(*ps[i], *pls[i], (const T *)in[i], (T *)out[i], (T *)w, bar, &drs[i]);
+    if (e != cudaSuccess) return e;
+  }
+  for (int i = 0; i < n; i++) {
+    cudaError_t e = launch_dist_prologue(*ps[i], in[i], drs[i], s);
+    if (e != cudaSuccess) return e;
+  }
+  for (int64_t t = 0; t < steps; t++)
+    for (int i = 0; i < n; i++) {
+      cudaError_t e = L[i].step(t, steps, s);
+      if (e != cudaSuccess) return e;
+    }
+  return cudaSuccess;
+}
+}  // namespace
+
+cudaError_t run_stream3d_hostloop_group(const Problem *const *ps, const Plan *const *pls,
+                                        const void *const *in, void *const *out, void *const *ws,
+                                        const DistRun *drs, int n, int64_t steps, cudaStream_t s) {
+  const Problem &p = *ps[0];
+  if (p.dtype == PERKS_F32)
+    return p.shape == SHAPE_3D7 ? group3<float, SHAPE_3D7>(ps, pls, in, out, ws, drs, n, steps, s)
+                                : group3<float, SHAPE_3D27>(ps, pls, in, out, ws, drs, n, steps, s);
+  return p.shape == SHAPE_3D7 ? group3<double, SHAPE_3D7>(ps, pls, in, out, ws, drs, n, steps, s)
+                              : group3<double, SHAPE_3D27>(ps, pls, in, out, ws, drs, n, steps, s);
 }
 
 }  // namespace perks

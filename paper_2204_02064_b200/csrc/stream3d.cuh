@@ -19,6 +19,7 @@
 #include <cuda.h>
 
 #include "common.cuh"
+#include "dist.cuh"
 #include "shapes.cuh"
 
 namespace perks {
@@ -43,12 +44,15 @@ struct Geo3D {
 
 struct Dom3 {
   int nx, ny, nz;
+  int zlo, zhi;  // planes zlo..zhi are z-interior (single GPU: 1..nz-2; slab faces with a neighbour
+                 // are interior, reading R12)
 };
 
 // TMA descriptors of the (up to) three buffers a run reads: 0 = in, 1 = out, 2 = tmp.
 struct Maps3 {
   CUtensorMap box[3];  // box {P, ROWS, 1}: a whole tile plane with its halo ring
   CUtensorMap row[3];  // box {P, 1, 1}: one halo row (cached planes)
+  CUtensorMap ghost;   // multi-GPU ghost planes G[4][ny][nx] (dist.cuh), box {P, ROWS, 1}
 };
 
 // ---------------------------------------------------------------- mbarrier / TMA primitives
@@ -259,7 +263,7 @@ struct ThreadTile {
 template <typename T, class G>
 PERKS_DEVINL void frame_select(const Dom3 &d, const ThreadTile<G> &tt, int o, T (&val)[G::R][G::V],
                                const T (&old)[G::R][G::V]) {
-  const bool zint = o >= 1 && o <= d.nz - 2;
+  const bool zint = o >= d.zlo && o <= d.zhi;
   if (zint && tt.inner) return;
 #pragma unroll
   for (int r = 0; r < G::R; r++) {
@@ -329,6 +333,23 @@ struct Ring {
       cp_async_commit();
     }
   }
+  // Ghost plane (multi-GPU, TMA only): plane -1 / nz of this slab lives in the neighbour-written
+  // ghost buffer at z coordinate gz; wait until exchange e fully arrived (system-scope acquire),
+  // order that acquire before the async-proxy (TMA) read, then load the tile box as usual.
+  PERKS_DEVINL void issue_ghost(unsigned k, const CUtensorMap *gmap, int gz, int x0, int y0,
+                                const unsigned long long *ctr, unsigned long long target,
+                                bool col_arrive) {
+    if constexpr (TMA) {
+      if (threadIdx.x == 0) {
+        wait_counter_sys(ctr, target);
+        fence_proxy_async_global();
+        fence_proxy_async();
+        mbar_arrive_tx(bar(k), G::BOX_BYTES);
+        tma_load_3d(slot(k), gmap, x0 - G::PAD, y0 - 1, gz, bar(k));
+      }
+      if (col_arrive && threadIdx.x >= 32 && threadIdx.x < 32 + 2 * G::TY) mbar_arrive(bar(k));
+    }
+  }
   // Halo ring only of plane q into `dst_slot` (PERKS cached plane), completing on arrival k.
   // TMA path: the two halo rows (corners included) by 1D bulk copies clipped to the domain
   // (cells outside stay stale: they only feed frame cells, whose results are discarded); the
@@ -388,11 +409,53 @@ struct Ring {
 
 // Stream one unit (tile x0,y0; planes [zs, ze)) of one time step from src to dst (no caching).
 // Arrivals q = zs-1 .. ze; NS-1 planes in flight.
-template <typename T, int S, class G, bool TMA>
+// Multi-GPU face hooks shared by every 3D kernel (dist.cuh).  `e` = index of the exchange this step
+// reads; the step's output planes 0 / nz-1 are exchange e+1.
+struct DistStep {
+  DistK k;
+  const CUtensorMap *gmap;
+  unsigned long long e;
+  unsigned long long plane_cells;  // nx * ny
+};
+// Which ghost side plane q comes from (-1: an ordinary plane of the local buffers).
+PERKS_DEVINL int ghost_side(const DistStep &ds, const Dom3 &d, int q) {
+  return (q < 0 && ds.k.has_lo) ? 0 : ((q >= d.nz && ds.k.has_hi) ? 1 : -1);
+}
+// Issue plane q into ring arrival k from the local buffer or, for a slab face, the ghost planes.
+template <typename T, class G, bool TMA, bool DIST>
+PERKS_DEVINL void issue_plane_any(Ring<T, G, TMA> &ring, unsigned k, const T *src,
+                                  const CUtensorMap *map, const Dom3 &d, int q, int x0, int y0,
+                                  bool col_arrive, const DistStep &ds) {
+  if constexpr (!DIST) {
+    ring.issue_full(k, src, map, d, q, x0, y0, col_arrive);
+    return;
+  }
+  const int gs = ghost_side(ds, d, q);
+  if (gs < 0) {
+    ring.issue_full(k, src, map, d, q, x0, y0, col_arrive);
+  } else {
+    ring.issue_ghost(k, ds.gmap, (int)(ds.e & 1) * 2 + gs, x0, y0, ds.k.ctr + gs,
+                     (ds.e + 1) * ds.plane_cells, col_arrive);
+  }
+}
+// After output plane o was stored locally: a face plane also goes to the neighbour's ghost plane.
+template <typename T, class G>
+PERKS_DEVINL void send_face(const DistStep &ds, const Dom3 &d, const ThreadTile<G> &tt, int o,
+                            int x0, int y0, const T (&v)[G::R][G::V]) {
+  const bool lo = o == 0 && ds.k.has_lo, hi = o == d.nz - 1 && ds.k.has_hi;
+  if (!lo && !hi) return;
+  const int gz = (int)((ds.e + 1) & 1) * 2 + (lo ? 1 : 0);  // lower neighbour's side 1 / upper's 0
+  store_cells<T, G>(reinterpret_cast<T *>(lo ? ds.k.send_lo : ds.k.send_hi), d, tt, gz, v);
+  const unsigned long long cells =
+      (unsigned long long)min(G::TX, d.nx - x0) * (unsigned long long)min(G::TY, d.ny - y0);
+  signal_counter_sys(lo ? ds.k.peer_ctr_lo : ds.k.peer_ctr_hi, cells);  // (local nz >= 2: never both)
+}
+
+template <typename T, int S, class G, bool TMA, bool DIST>
 PERKS_DEVINL void stream_unit(Ring<T, G, TMA> &ring, const T *__restrict__ src,
                               const CUtensorMap *map, T *__restrict__ dst, const Dom3 &d, int x0,
                               int y0, int zs, int ze, const Coef<T, Shape<S>::N> &c,
-                              bool col_arrive = false) {
+                              const DistStep &ds, bool col_arrive = false) {
   constexpr int D = G::NS - 1;
   const int q0 = zs - 1;
   const int narr = ze - zs + 2;
@@ -401,7 +464,7 @@ PERKS_DEVINL void stream_unit(Ring<T, G, TMA> &ring, const T *__restrict__ src,
   tt.init(d, x0, y0);
 #pragma unroll
   for (int k = 0; k < D; k++) {
-    if (k < narr) ring.issue_full(k0 + k, src, map, d, q0 + k, x0, y0, col_arrive);
+    if (k < narr) issue_plane_any<T, G, TMA, DIST>(ring, k0 + k, src, map, d, q0 + k, x0, y0, col_arrive, ds);
     else ring.issue_none();
   }
   StreamState<T, G> st;
@@ -409,13 +472,14 @@ PERKS_DEVINL void stream_unit(Ring<T, G, TMA> &ring, const T *__restrict__ src,
   for (int k = 0; k < narr; k++) {
     const int q = q0 + k;
     ring.wait(k0 + k);
-    if (k + D < narr) ring.issue_full(k0 + k + D, src, map, d, q + D, x0, y0, col_arrive);
+    if (k + D < narr) issue_plane_any<T, G, TMA, DIST>(ring, k0 + k + D, src, map, d, q + D, x0, y0, col_arrive, ds);
     else ring.issue_none();
     T out[G::R][G::V], cq[G::R][G::V];
     arrival<T, S, G>(st, ring.slot(k0 + k), c, out, cq);
     if (q - 1 >= zs) {
       frame_select<T, G>(d, tt, q - 1, out, st.cm1);
       store_cells<T, G>(dst, d, tt, q - 1, out);
+      if constexpr (DIST) send_face<T, G>(ds, d, tt, q - 1, x0, y0, out);
     }
 #pragma unroll
     for (int r = 0; r < G::R; r++)

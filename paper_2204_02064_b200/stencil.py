@@ -12,6 +12,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import VARIANTS, check, lib
+from .dist import exchange_neighbour_blobs
 
 
 def _dtype_code(dtype) -> int:
@@ -38,7 +39,11 @@ class Stencil:
     weights: floats, rounded once to dtype by the library (reading R6).
     """
 
-    def __init__(self, shape, offsets, weights, dtype="f64", bc="frame", device=0):
+    def __init__(self, shape, offsets, weights, dtype="f64", bc="frame", device=0, rank=0,
+                 nranks=1):
+        """rank/nranks > 1: this handle is rank's z-slab of a slab-decomposed global domain
+        (perks_stencil_create_dist); ``shape`` is the LOCAL slab.  Connect it with
+        ``connect`` (or ``connect_torch_distributed``) before running."""
         shape = tuple(int(s) for s in shape)
         if len(shape) not in (2, 3):
             raise ValueError("shape must be (ny, nx) or (nz, ny, nx)")
@@ -59,8 +64,14 @@ class Stencil:
         self.dtype_code = d.dtype
         self.device = int(device)
         h = ctypes.c_void_p()
-        check(lib.perks_stencil_create(ctypes.byref(d), self.device, ctypes.byref(h)),
-              "perks_stencil_create")
+        self.rank, self.nranks = int(rank), int(nranks)
+        if self.nranks > 1:
+            check(lib.perks_stencil_create_dist(ctypes.byref(d), self.device, self.rank,
+                                                self.nranks, ctypes.byref(h)),
+                  "perks_stencil_create_dist")
+        else:
+            check(lib.perks_stencil_create(ctypes.byref(d), self.device, ctypes.byref(h)),
+                  "perks_stencil_create")
         self._h = h
         self._ws = {}
 
@@ -150,6 +161,24 @@ class Stencil:
               "perks_stencil_run_host")
         return dst
 
+    # ------------------------------------------------------------------ multi-GPU slabs
+    def export_blob(self) -> bytes:
+        """This rank's connection blob (IPC handle of the library-owned ghost planes)."""
+        buf = ctypes.create_string_buffer(_lib.DIST_BLOB_BYTES)
+        check(lib.perks_stencil_dist_export(self._h, buf), "perks_stencil_dist_export")
+        return buf.raw
+
+    def connect(self, lower_blob, upper_blob):
+        """Connect to rank-1 / rank+1 (None where there is no neighbour)."""
+        lo = ctypes.create_string_buffer(lower_blob, len(lower_blob)) if lower_blob else None
+        hi = ctypes.create_string_buffer(upper_blob, len(upper_blob)) if upper_blob else None
+        check(lib.perks_stencil_dist_connect(self._h, lo, hi), "perks_stencil_dist_connect")
+
+    def connect_torch_distributed(self, group=None):
+        """Exchange blobs with torch.distributed (plumbing only) and connect."""
+        lower, upper = exchange_neighbour_blobs(self.export_blob(), group)
+        self.connect(lower, upper)
+
     def close(self):
         if getattr(self, "_h", None):
             lib.perks_stencil_destroy(self._h)
@@ -174,3 +203,25 @@ def run(x, offsets, weights, steps, variant="auto", bc="frame"):
 
         torch.cuda.current_stream(x.device).synchronize()
         st.close()
+
+
+def run_group(stencils, xs, steps, variant="auto", outs=None, stream=None):
+    """Run the connected slab handles ``stencils`` (all on ONE device) together — the single-GPU
+    emulation of a multi-GPU slab decomposition (perks_stencil_run_group)."""
+    import torch
+
+    n = len(stencils)
+    if outs is None:
+        outs = [torch.empty_like(x) for x in xs]
+    v = _variant(variant)
+    wss = [st.workspace(v) for st in stencils]
+    VP = ctypes.c_void_p
+    hs = (VP * n)(*[st._h for st in stencils])
+    ins = (VP * n)(*[x.data_ptr() for x in xs])
+    os_ = (VP * n)(*[o.data_ptr() for o in outs])
+    ws = (VP * n)(*[w.data_ptr() for w in wss])
+    wb = (ctypes.c_size_t * n)(*[w.numel() for w in wss])
+    s = stream if stream is not None else torch.cuda.current_stream(xs[0].device)
+    check(lib.perks_stencil_run_group(hs, n, v, ins, os_, ws, wb, int(steps), VP(s.cuda_stream)),
+          "perks_stencil_run_group")
+    return outs
