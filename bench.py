@@ -217,8 +217,17 @@ def run_mine(args):
     c = _cfg(args.config)
     offs, w = si.preset(c["stencil"])
     T = args.T or c["steps"]
-    st = Stencil(c["shape"], offs, w, dtype=c["np_dtype"], device=local)
-    x = si.field_torch(c["shape"], c["np_dtype"], dev)
+    # C5 is the slab-decomposed workload: rank r owns global planes [r*nz, (r+1)*nz) of a
+    # 1024 x 1024 x (1024*N) domain and exchanges face planes with its neighbours every step
+    # (in-kernel, csrc/dist.cuh).  Every other config runs independent replicas at N > 1.
+    slab = args.config == "C5" and ws > 1
+    if slab:
+        st = Stencil(c["shape"], offs, w, dtype=c["np_dtype"], device=local, rank=rank, nranks=ws)
+        st.connect_torch_distributed()
+    else:
+        st = Stencil(c["shape"], offs, w, dtype=c["np_dtype"], device=local)
+    x = si.field_torch(c["shape"], c["np_dtype"], dev,
+                       index_offset=(rank * c["cells"]) if slab else 0)
     out = torch.empty_like(x)
     variant = args.variant
     q = st.query(variant)
@@ -336,8 +345,11 @@ def run_mine(args):
         "warmup": args.warmup, "ms_per_step": ms_per, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": c["dtype"], "data": "synthetic",
         "config": {
+            "parallelism": (f"slab{ws}" if slab else f"replicas{ws}") if ws > 1 else "single",
             "workload": f"{args.config}: {CONFIG_DESC[args.config]}"
-                        + (" per GPU (independent replicas)" if ws > 1 else ""),
+                        + ((f", global z = 1024 x {ws}, slab-decomposed, face planes exchanged "
+                            "in-kernel every step" if slab else " per GPU (independent replicas)")
+                           if ws > 1 else ""),
             "variant": q["variant"], "kernel": q["kernel"], "grid": q["grid"], "block": q["block"],
             "time_steps_per_bench_step": T, "cells": cells,
             "l2": "flushed between timed steps (256 MiB device write outside the events)",
@@ -372,7 +384,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
-    ap.add_argument("--config", default="C2", choices=sorted(si.CONFIGS))
+    ap.add_argument("--config", default="C2", choices=sorted(si.CONFIGS),
+                    help="C5 = the slab-decomposed multi-GPU workload (N>1 under torchrun)")
     ap.add_argument("--variant", default="perks",
                     choices=["perks", "persistent", "hostloop", "auto"])
     ap.add_argument("--T", type=int, default=0, help="override time steps (dev only)")

@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(K3D_THREADS, (TMA && !DIST) ? 4 : 2) hostloop3
                                                                  const __grid_constant__ Maps3 maps,
                                                                  int src_idx, T *__restrict__ dst,
                                                                  Dom3 d, Units3 u,
-                                                                 Coef<T, Shape<S>::N> c, DistK dk,
+                                                                 Coef<T, Shape<S>::N> c, const __grid_constant__ DistK dk,
                                                                  unsigned long long e) {
   using G = typename G3Sel<T>::G;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -61,14 +61,14 @@ __global__ void __launch_bounds__(K3D_THREADS, (TMA && !DIST) ? 4 : 2) hostloop3
   const int nunits = u.tx * u.ty * u.nzc;
   unit_coords(u, u.rev ? nunits - 1 - (int)blockIdx.x : (int)blockIdx.x, G::TX, G::TY, x0, y0, zs);
   const int ze = min(zs + u.zc, d.nz);
-  const DistStep ds{dk, &maps.ghost, e, (unsigned long long)d.nx * d.ny};
+  const DistStep ds{&dk, &maps.ghost, e, (unsigned long long)d.nx * d.ny};
   stream_unit<T, S, G, TMA, DIST>(ring, src, &maps.box[src_idx], dst, d, x0, y0, zs, ze, c, ds);
 }
 
 template <typename T, int S, bool TMA, bool DIST>
 __global__ void __launch_bounds__(K3D_THREADS) persistent3d_kernel(
     const T *__restrict__ in, T *out, T *tmp, const __grid_constant__ Maps3 maps, Dom3 d, Units3 u,
-    int64_t steps, unsigned *bar, Coef<T, Shape<S>::N> c, DistK dk, unsigned long long xbase) {
+    int64_t steps, unsigned *bar, Coef<T, Shape<S>::N> c, const __grid_constant__ DistK dk, unsigned long long xbase) {
   using G = typename G3Sel<T>::G;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Ring<T, G, TMA> ring;
@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(K3D_THREADS) persistent3d_kernel(
     const T *src = t == 0 ? in : (src_out ? out : tmp);
     const int src_idx = t == 0 ? 0 : (src_out ? 1 : 2);
     T *dst = ((steps - 1 - t) & 1) == 0 ? out : tmp;
-    const DistStep ds{dk, &maps.ghost, xbase + (unsigned long long)t, (unsigned long long)d.nx * d.ny};
+    const DistStep ds{&dk, &maps.ghost, xbase + (unsigned long long)t, (unsigned long long)d.nx * d.ny};
     for (int id = blockIdx.x; id < nunits; id += gridDim.x) {
       int x0, y0, zs;
       unit_coords(u, (u.rev && (t & 1)) ? nunits - 1 - id : id, G::TX, G::TY, x0, y0, zs);

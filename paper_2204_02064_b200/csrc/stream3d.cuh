@@ -412,14 +412,14 @@ struct Ring {
 // Multi-GPU face hooks shared by every 3D kernel (dist.cuh).  `e` = index of the exchange this step
 // reads; the step's output planes 0 / nz-1 are exchange e+1.
 struct DistStep {
-  DistK k;
+  const DistK *k;  // points at a __grid_constant__ kernel parameter (read from the param bank)
   const CUtensorMap *gmap;
   unsigned long long e;
   unsigned long long plane_cells;  // nx * ny
 };
 // Which ghost side plane q comes from (-1: an ordinary plane of the local buffers).
 PERKS_DEVINL int ghost_side(const DistStep &ds, const Dom3 &d, int q) {
-  return (q < 0 && ds.k.has_lo) ? 0 : ((q >= d.nz && ds.k.has_hi) ? 1 : -1);
+  return (q < 0 && ds.k->has_lo) ? 0 : ((q >= d.nz && ds.k->has_hi) ? 1 : -1);
 }
 // Issue plane q into ring arrival k from the local buffer or, for a slab face, the ghost planes.
 template <typename T, class G, bool TMA, bool DIST>
@@ -434,7 +434,7 @@ PERKS_DEVINL void issue_plane_any(Ring<T, G, TMA> &ring, unsigned k, const T *sr
   if (gs < 0) {
     ring.issue_full(k, src, map, d, q, x0, y0, col_arrive);
   } else {
-    ring.issue_ghost(k, ds.gmap, (int)(ds.e & 1) * 2 + gs, x0, y0, ds.k.ctr + gs,
+    ring.issue_ghost(k, ds.gmap, (int)(ds.e & 1) * 2 + gs, x0, y0, ds.k->ctr + gs,
                      (ds.e + 1) * ds.plane_cells, col_arrive);
   }
 }
@@ -442,29 +442,93 @@ PERKS_DEVINL void issue_plane_any(Ring<T, G, TMA> &ring, unsigned k, const T *sr
 template <typename T, class G>
 PERKS_DEVINL void send_face(const DistStep &ds, const Dom3 &d, const ThreadTile<G> &tt, int o,
                             int x0, int y0, const T (&v)[G::R][G::V]) {
-  const bool lo = o == 0 && ds.k.has_lo, hi = o == d.nz - 1 && ds.k.has_hi;
+  const bool lo = o == 0 && ds.k->has_lo, hi = o == d.nz - 1 && ds.k->has_hi;
   if (!lo && !hi) return;
   const int gz = (int)((ds.e + 1) & 1) * 2 + (lo ? 1 : 0);  // lower neighbour's side 1 / upper's 0
-  store_cells<T, G>(reinterpret_cast<T *>(lo ? ds.k.send_lo : ds.k.send_hi), d, tt, gz, v);
+  store_cells<T, G>(reinterpret_cast<T *>(lo ? ds.k->send_lo : ds.k->send_hi), d, tt, gz, v);
   const unsigned long long cells =
       (unsigned long long)min(G::TX, d.nx - x0) * (unsigned long long)min(G::TY, d.ny - y0);
-  signal_counter_sys(lo ? ds.k.peer_ctr_lo : ds.k.peer_ctr_hi, cells);  // (local nz >= 2: never both)
+  signal_counter_sys(lo ? ds.k->peer_ctr_lo : ds.k->peer_ctr_hi, cells);  // (local nz >= 2: never both)
 }
 
-template <typename T, int S, class G, bool TMA, bool DIST>
+// PERKS plane cache of one unit (k3d_perks.cu): planes q with cmap[q - czs] >= 0 stay resident in
+// shared-memory slot cache + cmap[q - czs] * G::SLOT across steps.
+template <typename T> struct CacheView {
+  T *cache;
+  const short *cmap;
+  int czs, cze;  // the cached unit's planes [czs, cze) (first/last never cached)
+};
+
+template <typename T, class G>
+PERKS_DEVINL void write_own(T *slot, const T (&v)[G::R][G::V]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int r = 0; r < G::R; r++)
+    vstore<T, G::V>(slot + (warp * G::R + r + 1) * G::P + G::PAD + lane * G::V, v[r]);
+}
+template <typename T, class G>
+PERKS_DEVINL void read_own(const T *slot, T (&v)[G::R][G::V]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int r = 0; r < G::R; r++)
+    vload<T, G::V>(v[r], slot + (warp * G::R + r + 1) * G::P + G::PAD + lane * G::V);
+}
+
+// Publish the tile-perimeter cells of cached plane o to dst (neighbours read them as halo): the
+// TB-boundary cells "continue to store and load from global memory".
+template <typename T, class G>
+PERKS_DEVINL void publish_perimeter(T *__restrict__ dst, const Dom3 &d, int o, int x0, int y0,
+                                    const T (&v)[G::R][G::V]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int x = x0 + lane * G::V;
+  T *base = dst + (size_t)o * d.nx * d.ny;
+  const int xl = min(x0 + G::TX, d.nx) - 1;  // last tile column inside the domain
+#pragma unroll
+  for (int r = 0; r < G::R; r++) {
+    const int y = y0 + warp * G::R + r;
+    if (y >= d.ny) break;
+    const bool edge_row = (warp == 0 && r == 0) || (warp == G::NWARP - 1 && r == G::R - 1) ||
+                          y == d.ny - 1;
+    if (edge_row) {
+#pragma unroll
+      for (int i = 0; i < G::V; i++)
+        if (x + i < d.nx) base[(size_t)y * d.nx + x + i] = v[r][i];
+    } else {
+      if (lane == 0 && x < d.nx) base[(size_t)y * d.nx + x] = v[r][0];
+      if (xl >= x && xl < x + G::V) {
+#pragma unroll
+        for (int i = 0; i < G::V; i++)
+          if (x + i == xl) base[(size_t)y * d.nx + x + i] = v[r][i];
+      }
+    }
+  }
+}
+
+template <typename T, int S, class G, bool TMA, bool DIST, bool CACHE = false>
 PERKS_DEVINL void stream_unit(Ring<T, G, TMA> &ring, const T *__restrict__ src,
                               const CUtensorMap *map, T *__restrict__ dst, const Dom3 &d, int x0,
                               int y0, int zs, int ze, const Coef<T, Shape<S>::N> &c,
-                              const DistStep &ds, bool col_arrive = false) {
+                              const DistStep &ds, bool col_arrive = false,
+                              const CacheView<T> &cv = CacheView<T>{}) {
   constexpr int D = G::NS - 1;
   const int q0 = zs - 1;
   const int narr = ze - zs + 2;
   const unsigned k0 = ring.gk;
   ThreadTile<G> tt;
   tt.init(d, x0, y0);
+  // cache slot of plane q (CACHE only), -1 = streamed through the ring
+  auto cs = [&](int q) -> int {
+    if constexpr (!CACHE) return -1;
+    return (q > cv.czs && q < cv.cze - 1) ? (int)cv.cmap[q - cv.czs] : -1;
+  };
+  auto issue = [&](unsigned k, int q) {
+    const int sl = cs(q);
+    if (CACHE && sl >= 0) ring.issue_halo(k, cv.cache + (size_t)sl * G::SLOT, src, d, q, x0, y0);
+    else issue_plane_any<T, G, TMA, DIST>(ring, k, src, map, d, q, x0, y0, col_arrive, ds);
+  };
 #pragma unroll
   for (int k = 0; k < D; k++) {
-    if (k < narr) issue_plane_any<T, G, TMA, DIST>(ring, k0 + k, src, map, d, q0 + k, x0, y0, col_arrive, ds);
+    if (k < narr) issue(k0 + k, q0 + k);
     else ring.issue_none();
   }
   StreamState<T, G> st;
@@ -472,14 +536,23 @@ PERKS_DEVINL void stream_unit(Ring<T, G, TMA> &ring, const T *__restrict__ src,
   for (int k = 0; k < narr; k++) {
     const int q = q0 + k;
     ring.wait(k0 + k);
-    if (k + D < narr) issue_plane_any<T, G, TMA, DIST>(ring, k0 + k + D, src, map, d, q + D, x0, y0, col_arrive, ds);
+    if (k + D < narr) issue(k0 + k + D, q + D);
     else ring.issue_none();
     T out[G::R][G::V], cq[G::R][G::V];
-    arrival<T, S, G>(st, ring.slot(k0 + k), c, out, cq);
+    const int slq = cs(q);
+    arrival<T, S, G>(st, slq >= 0 ? cv.cache + (size_t)slq * G::SLOT : ring.slot(k0 + k), c, out, cq);
     if (q - 1 >= zs) {
       frame_select<T, G>(d, tt, q - 1, out, st.cm1);
-      store_cells<T, G>(dst, d, tt, q - 1, out);
-      if constexpr (DIST) send_face<T, G>(ds, d, tt, q - 1, x0, y0, out);
+      const int slo = cs(q - 1);
+      if (CACHE && slo >= 0) {
+        // cached output: stays on chip (its slot was last read at arrival q-1, before this
+        // arrival's barrier); only the tile perimeter goes to global memory (Fig. 6 Destination)
+        publish_perimeter<T, G>(dst, d, q - 1, x0, y0, out);
+        write_own<T, G>(cv.cache + (size_t)slo * G::SLOT, out);
+      } else {
+        store_cells<T, G>(dst, d, tt, q - 1, out);
+        if constexpr (DIST) send_face<T, G>(ds, d, tt, q - 1, x0, y0, out);
+      }
     }
 #pragma unroll
     for (int r = 0; r < G::R; r++)

@@ -32,7 +32,7 @@ def _dist(tmp_path, name, shape, dtype, n, variant, Ts):
     return np.load(out)
 
 
-@pytest.mark.parametrize("variant", ["hostloop", "persistent"])
+@pytest.mark.parametrize("variant", ["hostloop", "persistent", "perks"])
 @pytest.mark.parametrize("n", [2, 3])
 @pytest.mark.parametrize("name,dtype", [("3d7pt", np.float64), ("3d27pt", np.float32)])
 def test_slabs_match_global_oracle(tmp_path, variant, n, name, dtype):
@@ -52,6 +52,7 @@ def test_many_slabs_long_run(tmp_path):
     shape, name, dtype = (24, 36, 128), "3d7pt", np.float64
     offs, w = si.preset(name)
     u0 = si.field(shape, dtype=dtype, seed=505)
-    got = _dist(tmp_path, name, shape, dtype, 4, "persistent", [1, 10, 5])
     ref = oracle.run(u0, offs, w, 16, nthreads=4)
-    assert np.array_equal(got, ref)
+    for variant in ("persistent", "perks"):
+        got = _dist(tmp_path, name, shape, dtype, 4, variant, [1, 10, 5])
+        assert np.array_equal(got, ref), variant

@@ -55,7 +55,7 @@ def _check(gpu, ref, u0, dtype, exact=True):
 
 
 CASES_2D = [(3, 3), (5, 7), (17, 33), (67, 131), (128, 128), (130, 260), (257, 300), (500, 100)]
-CASES_3D = [(3, 3, 3), (5, 6, 7), (9, 17, 33), (20, 35, 70), (34, 40, 132)]
+CASES_3D = [(3, 3, 3), (5, 6, 7), (9, 17, 33), (20, 35, 70), (34, 40, 132), (16, 40, 64), (37, 24, 128)]
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
@@ -188,3 +188,22 @@ def test_small_domain_uses_cluster_kernel(shape, dtype, name):
     u0 = si.field(shape, dtype=dtype, seed=404)
     ref = oracle.run(u0, offs, w, 100, nthreads=4)
     _check(_run_gpu(u0, name, w, 100, "perks"), ref, u0, dtype)
+
+
+@pytest.mark.parametrize("nsm", ["0", "1", "3", ""])
+@pytest.mark.parametrize("zigzag", ["0", "1"])
+@pytest.mark.parametrize("name,dtype", [("3d7pt", np.float64), ("3d27pt", np.float32)])
+def test_perks3d_cache_and_zigzag(monkeypatch, nsm, zigzag, name, dtype):
+    """PERKS-3D: cached planes (shared-memory slots spread through each CTA's segment, halo-ring
+    refresh + perimeter publish) and zig-zag traversal are bit-exact for any cache size, both
+    traversal directions and both step parities."""
+    _need_gpu()
+    if nsm:
+        monkeypatch.setenv("PERKS_P3D_NSM", nsm)
+    monkeypatch.setenv("PERKS_ZIGZAG", zigzag)
+    shape = (45, 50, 64)
+    u0 = si.field(shape, dtype=dtype, seed=606)
+    offs, w = si.preset(name)
+    for T in (5, 6):
+        ref = oracle.run(u0, offs, w, T, nthreads=4)
+        _check(_run_gpu(u0, name, w, T, "perks"), ref, u0, dtype)
