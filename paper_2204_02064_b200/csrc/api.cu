@@ -120,7 +120,7 @@ const Plan &get_plan(perks_stencil_s *h, perks_variant v) {
       if (pl.ok) pl.family = 1;
       else pl = plan_perks2d(p);
     } else if (v == PERKS_PERKS)
-      pl = plan_perks3d(p);
+      pl = plan_stream3d(p, PERKS_PERKS);
     h->plans[i] = pl;
     h->planned[i] = true;
   }
@@ -419,8 +419,7 @@ perks_status perks_stencil_run(perks_stencil_t h, perks_variant v, const void *d
   if (h->dist.on) {
     if (!h->dist.connected) return PERKS_ERR_COMM;
     DistRun dr = dist_run(h);
-    if (v == PERKS_PERKS) e = run_perks3d(p, pl, d_in, d_out, d_ws, steps, s, &dr);
-    else e = run_stream3d(p, pl, d_in, d_out, d_ws, steps, s, &dr);
+    e = run_stream3d(p, pl, d_in, d_out, d_ws, steps, s, &dr);
     if (e != cudaSuccess) return cuda_fail(e);
     h->dist.xbase += (unsigned long long)steps + 1;  // prologue exchange + one per step
     return PERKS_OK;
@@ -436,7 +435,7 @@ perks_status perks_stencil_run(perks_stencil_t h, perks_variant v, const void *d
         e = pl.family == 1 ? run_perks2d_cluster(p, pl, d_in, d_out, steps, s)
                            : run_perks2d(p, pl, d_in, d_out, d_ws, steps, s);
       else
-        e = run_perks3d(p, pl, d_in, d_out, d_ws, steps, s);
+        e = run_stream3d(p, pl, d_in, d_out, d_ws, steps, s);
       break;
     default:
       return PERKS_ERR_INVALID_ARGUMENT;
@@ -536,8 +535,7 @@ perks_status perks_stencil_run_group(const perks_stencil_t *hs, int n, perks_var
       }
       cudaStream_t gs = h->g_streams[0];
       cudaStreamWaitEvent(gs, fork, 0);
-      e = rv == PERKS_PERKS ? run_perks3d(*ps[i], *pls[i], d_in[i], d_out[i], d_ws[i], steps, gs, &drs[i])
-                            : run_stream3d(*ps[i], *pls[i], d_in[i], d_out[i], d_ws[i], steps, gs, &drs[i]);
+      e = run_stream3d(*ps[i], *pls[i], d_in[i], d_out[i], d_ws[i], steps, gs, &drs[i]);
       if (e != cudaSuccess) break;
       cudaEventCreateWithFlags(&joins[i], cudaEventDisableTiming);
       cudaEventRecord(joins[i], gs);

@@ -38,7 +38,8 @@ struct Plan {
   int64_t units = 0;          // work units per step
   int zchunk = 0;             // planes per unit (3D)
   int cfg = 0;                // index of the kernel configuration
-  int family = 0;             // kernel family within a variant (2D PERKS: 0 tiles, 1 cluster)
+  int family = 0;             // kernel family within a variant (2D PERKS: 0 tiles, 1 cluster; 3D PERKS: 2)
+  int nc = 0;                 // 3D PERKS: shared-memory plane slots per CTA
   int64_t cached_reg = 0, cached_smem = 0;
   double dram_bytes_step = 0, halo_bytes_step = 0;
   size_t ws_bytes = 0;
@@ -64,7 +65,7 @@ struct DistRun {
 Plan plan_stream2d(const Problem &p, perks_variant v);
 cudaError_t run_stream2d(const Problem &p, const Plan &pl, const void *in, void *out, void *ws,
                          int64_t steps, cudaStream_t s);
-// 3D plane streaming kernels: host-loop (a) and persistent (b).
+// 3D plane streaming kernels: host-loop (a), persistent (b) and PERKS (c).
 Plan plan_stream3d(const Problem &p, perks_variant v);
 cudaError_t run_stream3d(const Problem &p, const Plan &pl, const void *in, void *out, void *ws,
                          int64_t steps, cudaStream_t s, const DistRun *dr = nullptr);
@@ -82,10 +83,7 @@ cudaError_t run_perks2d(const Problem &p, const Plan &pl, const void *in, void *
 Plan plan_perks2d_cluster(const Problem &p);
 cudaError_t run_perks2d_cluster(const Problem &p, const Plan &pl, const void *in, void *out,
                                 int64_t steps, cudaStream_t s);
-// PERKS (c), 3D, partially cached plane streaming.
-Plan plan_perks3d(const Problem &p);
-cudaError_t run_perks3d(const Problem &p, const Plan &pl, const void *in, void *out, void *ws,
-                        int64_t steps, cudaStream_t s, const DistRun *dr = nullptr);
+// PERKS (c), 3D: the persistent kernel with a shared-memory plane cache (k3d_stream.cu).
 
 // Environment override helper (sweeps only): returns def if unset.
 int env_int(const char *name, int def);

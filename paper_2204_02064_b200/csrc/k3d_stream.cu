@@ -1,7 +1,15 @@
-// k3d_stream.cu — 3D stencil kernels without cross-step caching:
+// k3d_stream.cu — the 3D stencil kernels of all three variants:
 //   (a) host-loop: one launch per step, one (tile, z-chunk) unit per CTA  (Fig. 3 left)
 //   (b) persistent: one cooperative launch; CTAs loop over units; grid barrier per step
-// Compute body and plane loaders: stream3d.cuh (plane streaming; TMA boxes on sm_100a).
+//   (c) PERKS: the persistent kernel plus an on-chip plane cache (§3.3): each
+//       CTA keeps `nc` interior planes of its unit resident in shared memory across steps.  "Planes
+//       that already have the data cached from the previous time step do not load from global
+//       memory": a cached plane reloads only its one-cell halo ring (halo cells are never
+//       cached) and publishes only its tile perimeter (TB-boundary cells "continue to
+//       store and load from global memory").  Cached planes are spread evenly through the
+//       unit so the HBM stream never pauses, and every tile of a z-chunk caches the same planes.
+//       The first/last plane of each unit is never cached (other units read it as z-halo).
+// Compute body and plane pipelines: stream3d.cuh (plane streaming; TMA on sm_100a).
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -27,6 +35,15 @@ template <> struct G3Sel<double> { using G = Geo3D<double, 2, PERKS_S3D_R, 8, PE
 
 constexpr int K3D_THREADS = 256;
 static_assert(G3Sel<float>::G::NT == K3D_THREADS && G3Sel<double>::G::NT == K3D_THREADS, "3D block size");
+// Warp-specialised kernels: PERKS_WS_NWARP consumer warps + 1 producer warp = 256 threads, so two
+// CTAs per SM keep a 128-register budget.
+#ifndef PERKS_WS_NWARP
+#define PERKS_WS_NWARP 7
+#endif
+template <typename T, bool WS> struct GS { using G = typename G3Sel<T>::G; };
+template <typename T> struct GS<T, true> {
+  using G = Geo3D<T, 16 / (int)sizeof(T), PERKS_S3D_R, PERKS_WS_NWARP, PERKS_S3D_NS>;
+};
 
 struct Units3 {
   int tx, ty, nzc, zc;
@@ -46,48 +63,133 @@ template <class G> PERKS_DEVINL uint64_t *ring_bars(unsigned char *smem) {
   return reinterpret_cast<uint64_t *>(smem + (size_t)G::NS * G::SLOT_BYTES);
 }
 
+// Threads per CTA: warp-specialised kernels add one producer warp (stream3d.cuh WsPipe).  The
+// host loop (a) keeps the single-role ring (TMA issued by thread 0, CTA barrier per plane) at 4-5
+// CTAs per SM, measured faster for one-unit-per-launch CTAs (profiles/r01_ws_pipeline_sweep.txt);
+// the persistent kernel (b) uses the warp-specialised pipeline, measured faster when a CTA
+// streams long units back to back.
+#ifndef PERKS_S3D_HWS
+#define PERKS_S3D_HWS 0
+#endif
+#ifndef PERKS_S3D_MINB
+#define PERKS_S3D_MINB 4
+#endif
+template <bool TMA> constexpr bool host_ws() { return TMA && PERKS_S3D_HWS; }
+template <bool WS> constexpr int k3d_threads() { return WS ? 32 * PERKS_WS_NWARP + 32 : K3D_THREADS; }
+
 template <typename T, int S, bool TMA, bool DIST>
-__global__ void __launch_bounds__(K3D_THREADS, (TMA && !DIST) ? 4 : 2) hostloop3d_kernel(const T *__restrict__ src,
+__global__ void __launch_bounds__(k3d_threads<host_ws<TMA>()>(), (TMA && !DIST) ? PERKS_S3D_MINB : 2) hostloop3d_kernel(const T *__restrict__ src,
                                                                  const __grid_constant__ Maps3 maps,
                                                                  int src_idx, T *__restrict__ dst,
                                                                  Dom3 d, Units3 u,
                                                                  Coef<T, Shape<S>::N> c, const __grid_constant__ DistK dk,
                                                                  unsigned long long e) {
-  using G = typename G3Sel<T>::G;
+  using G = typename GS<T, host_ws<TMA>()>::G;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  Ring<T, G, TMA> ring;
-  ring.init(reinterpret_cast<T *>(smem_raw), ring_bars<G>(smem_raw), 0);
   int x0, y0, zs;
   const int nunits = u.tx * u.ty * u.nzc;
   unit_coords(u, u.rev ? nunits - 1 - (int)blockIdx.x : (int)blockIdx.x, G::TX, G::TY, x0, y0, zs);
   const int ze = min(zs + u.zc, d.nz);
   const DistStep ds{&dk, &maps.ghost, e, (unsigned long long)d.nx * d.ny};
-  stream_unit<T, S, G, TMA, DIST>(ring, src, &maps.box[src_idx], dst, d, x0, y0, zs, ze, c, ds);
+  if constexpr (host_ws<TMA>()) {
+    WsPipe<T, G> pp;
+    pp.init(reinterpret_cast<T *>(smem_raw), ring_bars<G>(smem_raw));
+    stream_unit_ws<T, S, G, DIST>(pp, src, &maps.box[src_idx], dst, d, x0, y0, zs, ze, c, ds);
+  } else {
+    Ring<T, G, TMA> ring;
+    ring.init(reinterpret_cast<T *>(smem_raw), ring_bars<G>(smem_raw), 0);
+    stream_unit<T, S, G, TMA, DIST>(ring, src, &maps.box[src_idx], dst, d, x0, y0, zs, ze, c, ds);
+  }
 }
 
-template <typename T, int S, bool TMA, bool DIST>
-__global__ void __launch_bounds__(K3D_THREADS) persistent3d_kernel(
+// Cache geometry of a PERKS launch (CACHE kernels only).
+struct Cache3 {
+  int nc;  // shared-memory plane slots per CTA
+};
+
+// Slot map of a unit [zs, ze): cmap[j] = cache slot of plane zs + j, or -1.  nc slots spread
+// evenly over the interior planes zs+1 .. ze-2 (the unit's first/last plane is never cached).
+PERKS_DEVINL int cache_slot_of(int j, int len, int nc) {
+  const int elig = len - 2, jj = j - 1;
+  if (nc <= 0 || jj < 0 || jj >= elig) return -1;
+  const int a = (jj * nc) / elig, b = ((jj + 1) * nc) / elig;
+  return b != a ? a : -1;
+}
+
+template <typename T, int S, bool TMA, bool DIST, bool CACHE>
+__global__ void __launch_bounds__(k3d_threads<TMA>(), (CACHE && DIST) ? 1 : 2) persistent3d_kernel(
     const T *__restrict__ in, T *out, T *tmp, const __grid_constant__ Maps3 maps, Dom3 d, Units3 u,
-    int64_t steps, unsigned *bar, Coef<T, Shape<S>::N> c, const __grid_constant__ DistK dk, unsigned long long xbase) {
-  using G = typename G3Sel<T>::G;
+    int64_t steps, unsigned *bar, Coef<T, Shape<S>::N> c, const __grid_constant__ DistK dk,
+    unsigned long long xbase, Cache3 ch) {
+  using G = typename GS<T, TMA>::G;
+  static_assert(!CACHE || TMA, "the PERKS cache runs on the warp-specialised TMA pipeline");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Ring<T, G, TMA> ring;
-  ring.init(reinterpret_cast<T *>(smem_raw), ring_bars<G>(smem_raw), 0);
+  WsPipe<T, G> pp;
+  if constexpr (TMA) pp.init(reinterpret_cast<T *>(smem_raw), ring_bars<G>(smem_raw));
+  else ring.init(reinterpret_cast<T *>(smem_raw), ring_bars<G>(smem_raw), 0);
   const int nunits = u.tx * u.ty * u.nzc;
+
+  // ---- PERKS: the CTA's first unit hosts the cache
+  T *cache = reinterpret_cast<T *>(smem_raw + (size_t)G::NS * G::SLOT_BYTES + 128);
+  short *cmap = reinterpret_cast<short *>(cache + (size_t)ch.nc * G::SLOT);
+  int cx0 = 0, cy0 = 0, czs = 0, cze = 0;
+  const bool consumer = (int)(threadIdx.x >> 5) < G::NWARP;
+  if constexpr (CACHE) {
+    if (blockIdx.x < nunits) {
+      unit_coords(u, blockIdx.x, G::TX, G::TY, cx0, cy0, czs);
+      cze = min(czs + u.zc, d.nz);
+    }
+    const int nc = min(ch.nc, max(0, cze - czs - 2));
+    for (int j = threadIdx.x; j < cze - czs; j += blockDim.x) cmap[j] = (short)cache_slot_of(j, cze - czs, nc);
+    __syncthreads();
+    // prologue: cached planes from `in` (the one-time load half of 2·D_cache)
+    for (int q = czs + 1; q < cze - 1 && consumer; q++) {
+      const int sl = cmap[q - czs];
+      if (sl >= 0) issue_plane<T, G>(cache + (size_t)sl * G::SLOT, in, d, q, cx0, cy0, false);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+  const CacheView<T> cv{cache, cmap, czs, cze};
+
   for (int64_t t = 0; t < steps; t++) {
     const bool src_out = t > 0 && ((steps - t) & 1) == 0;
     const T *src = t == 0 ? in : (src_out ? out : tmp);
     const int src_idx = t == 0 ? 0 : (src_out ? 1 : 2);
     T *dst = ((steps - 1 - t) & 1) == 0 ? out : tmp;
     const DistStep ds{&dk, &maps.ghost, xbase + (unsigned long long)t, (unsigned long long)d.nx * d.ny};
+    if (TMA && threadIdx.x == 0) fence_proxy_async_global();  // last step's stores -> TMA reads
     for (int id = blockIdx.x; id < nunits; id += gridDim.x) {
       int x0, y0, zs;
-      unit_coords(u, (u.rev && (t & 1)) ? nunits - 1 - id : id, G::TX, G::TY, x0, y0, zs);
+      // (the zig-zag unit-order experiment never applies to PERKS: the cache belongs to a unit)
+      unit_coords(u, (!CACHE && u.rev && (t & 1)) ? nunits - 1 - id : id, G::TX, G::TY, x0, y0, zs);
       const int ze = min(zs + u.zc, d.nz);
-      __syncthreads();  // slots of the previous unit are free
-      stream_unit<T, S, G, TMA, DIST>(ring, src, &maps.box[src_idx], dst, d, x0, y0, zs, ze, c, ds);
+      if constexpr (TMA) {
+        if (CACHE && id == (int)blockIdx.x)
+          stream_unit_ws<T, S, G, DIST, CACHE>(pp, src, &maps.box[src_idx], dst, d, x0, y0, zs, ze, c, ds, cv);
+        else
+          stream_unit_ws<T, S, G, DIST, false>(pp, src, &maps.box[src_idx], dst, d, x0, y0, zs, ze, c, ds);
+      } else {
+        __syncthreads();  // slots of the previous unit are free
+        stream_unit<T, S, G, TMA, DIST>(ring, src, &maps.box[src_idx], dst, d, x0, y0, zs, ze, c, ds);
+      }
     }
     if (t + 1 < steps) grid_barrier(bar, (unsigned)((t + 1) * gridDim.x));
+  }
+
+  if constexpr (CACHE) {  // epilogue: cached planes to `out` (store half of 2·D_cache)
+    __syncthreads();
+    ThreadTile<G> ct;
+    ct.init(d, cx0, cy0);
+    for (int q = czs + 1; q < cze - 1 && consumer; q++) {
+      const int sl = cmap[q - czs];
+      if (sl < 0) continue;
+      T v[G::R][G::V];
+      read_own<T, G>(cache + (size_t)sl * G::SLOT, v);
+      store_cells<T, G>(out, d, ct, q, v);
+    }
   }
 }
 
@@ -203,13 +305,13 @@ cudaError_t launch_dist_prologue(const Problem &p, const void *in, const DistRun
 namespace {
 template <typename T> void *kptr3d(int shape, bool persistent) {  // multi-GPU slab kernels (TMA)
   if (shape == SHAPE_3D7)
-    return persistent ? (void *)persistent3d_kernel<T, SHAPE_3D7, true, true> : (void *)hostloop3d_kernel<T, SHAPE_3D7, true, true>;
-  return persistent ? (void *)persistent3d_kernel<T, SHAPE_3D27, true, true> : (void *)hostloop3d_kernel<T, SHAPE_3D27, true, true>;
+    return persistent ? (void *)persistent3d_kernel<T, SHAPE_3D7, true, true, false> : (void *)hostloop3d_kernel<T, SHAPE_3D7, true, true>;
+  return persistent ? (void *)persistent3d_kernel<T, SHAPE_3D27, true, true, false> : (void *)hostloop3d_kernel<T, SHAPE_3D27, true, true>;
 }
 template <typename T> void *kptr3(int shape, bool persistent, bool tma) {
 #define K3(S)                                                                                   \
   if (shape == S) {                                                                             \
-    if (persistent) return tma ? (void *)persistent3d_kernel<T, S, true, false> : (void *)persistent3d_kernel<T, S, false, false>; \
+    if (persistent) return tma ? (void *)persistent3d_kernel<T, S, true, false, false> : (void *)persistent3d_kernel<T, S, false, false, false>; \
     return tma ? (void *)hostloop3d_kernel<T, S, true, false> : (void *)hostloop3d_kernel<T, S, false, false>; \
   }
   K3(SHAPE_3D7)
@@ -222,15 +324,27 @@ void *pick3(const Problem &p, bool persistent) {
   if (p.nranks > 1) return p.dtype == PERKS_F32 ? kptr3d<float>(p.shape, persistent) : kptr3d<double>(p.shape, persistent);
   return p.dtype == PERKS_F32 ? kptr3<float>(p.shape, persistent, tma) : kptr3<double>(p.shape, persistent, tma);
 }
-template <typename T> size_t smem3() {
-  using G = typename G3Sel<T>::G;
-  return (size_t)G::NS * G::SLOT_BYTES + (size_t)G::NS * sizeof(uint64_t);
+template <typename T, bool WS> size_t smem3_t() {
+  using G = typename GS<T, WS>::G;
+  return (size_t)G::NS * G::SLOT_BYTES + 2 * (size_t)G::NS * sizeof(uint64_t);
 }
-template <typename T> void geo3(int &tx, int &ty, int &nt) {
-  tx = G3Sel<T>::G::TX; ty = G3Sel<T>::G::TY; nt = G3Sel<T>::G::NT;
+template <typename T> size_t smem3(bool ws) { return ws ? smem3_t<T, true>() : smem3_t<T, false>(); }
+template <typename T, bool WS> void geo3_t(int &tx, int &ty, int &nt, size_t &slot) {
+  using G = typename GS<T, WS>::G;
+  tx = G::TX; ty = G::TY; nt = G::NT + (WS ? 32 : 0); slot = G::SLOT_BYTES;
+}
+template <typename T> void geo3(bool ws, int &tx, int &ty, int &nt, size_t &slot) {
+  if (ws) geo3_t<T, true>(tx, ty, nt, slot); else geo3_t<T, false>(tx, ty, nt, slot);
 }
 }  // namespace
 
+template <typename T> void *kptr_perks(int shape, bool dist) {
+  if (shape == SHAPE_3D7)
+    return dist ? (void *)persistent3d_kernel<T, SHAPE_3D7, true, true, true> : (void *)persistent3d_kernel<T, SHAPE_3D7, true, false, true>;
+  return dist ? (void *)persistent3d_kernel<T, SHAPE_3D27, true, true, true> : (void *)persistent3d_kernel<T, SHAPE_3D27, true, false, true>;
+}
+
+// Plan (a) host loop, (b) persistent or (c) PERKS for a 3D problem.
 Plan plan_stream3d(const Problem &p, perks_variant v) {
   Plan pl;
   pl.variant = v;
@@ -238,26 +352,56 @@ Plan plan_stream3d(const Problem &p, perks_variant v) {
     pl.why = "stream3d: needs 3D 7pt/27pt FRAME";
     return pl;
   }
-  if (p.nranks > 1 && !use_tma3(p)) { pl.why = "stream3d: multi-GPU slabs need TMA (nx*S % 16 == 0)"; return pl; }
-  const bool persistent = v == PERKS_PERSISTENT;
-  void *k = pick3(p, persistent);
-  const size_t smem = p.dtype == PERKS_F32 ? smem3<float>() : smem3<double>();
+  const bool tma = use_tma3(p);
+  if (p.nranks > 1 && !tma) { pl.why = "stream3d: multi-GPU slabs need TMA (nx*S % 16 == 0)"; return pl; }
+  const bool cache = v == PERKS_PERKS;
+  if (cache && !tma) { pl.why = "perks3d: needs TMA (nx*S % 16 == 0)"; return pl; }
+  const bool persistent = v != PERKS_HOSTLOOP;
+  void *k = cache ? (p.dtype == PERKS_F32 ? kptr_perks<float>(p.shape, p.nranks > 1) : kptr_perks<double>(p.shape, p.nranks > 1))
+                  : pick3(p, persistent);
+  const bool ws = tma && (persistent || PERKS_S3D_HWS);  // warp-specialised pipeline
+  const size_t ring = p.dtype == PERKS_F32 ? smem3<float>(ws) : smem3<double>(ws);
   int TX, TY, NT;
-  if (p.dtype == PERKS_F32) geo3<float>(TX, TY, NT); else geo3<double>(TX, TY, NT);
-  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
-    pl.why = "cudaFuncSetAttribute"; return pl;
-  }
+  size_t slot;
+  if (p.dtype == PERKS_F32) geo3<float>(ws, TX, TY, NT, slot); else geo3<double>(ws, TX, TY, NT, slot);
+  const int tx = (int)((p.nx + TX - 1) / TX), ty = (int)((p.ny + TY - 1) / TY);
+  const int tiles = tx * ty;
   cudaFuncAttributes fa;
   if (cudaFuncGetAttributes(&fa, k) != cudaSuccess) { pl.why = "cudaFuncGetAttributes"; return pl; }
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NT, smem);
-  const int tx = (int)((p.nx + TX - 1) / TX), ty = (int)((p.ny + TY - 1) / TY);
-  const int resident = std::max(1, occ * p.num_sms);
+  size_t smem = ring;
+  int occ = 0, nc = 0;
+  if (!cache) {
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+      cudaGetLastError();
+      pl.why = "cudaFuncSetAttribute"; return pl;
+    }
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NT, smem);
+  } else {
+    // PERKS: the shared memory the ring leaves at `cps` CTAs per SM caches planes (
+    // minimal occupancy that keeps the HBM stream saturated: 2 CTAs/SM measured best)
+    const int force_cps = env_int("PERKS_P3D_CPS", 0);
+    for (int cps = force_cps > 0 ? force_cps : 2; cps >= 1; cps--) {
+      const size_t budget = std::min<size_t>((size_t)p.max_smem_optin, (size_t)p.smem_per_sm / cps - 1024);
+      const size_t fixed = ring + 128 + align256((size_t)p.nz * sizeof(short));
+      nc = budget > fixed ? (int)((budget - fixed) / slot) : 0;
+      const int forced = env_int("PERKS_P3D_NSM", -1);
+      if (forced >= 0) nc = std::min(nc, forced);
+      smem = fixed + (size_t)nc * slot;
+      if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        cudaGetLastError();
+        continue;
+      }
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NT, smem);
+      if (occ >= cps) { occ = cps; break; }
+    }
+  }
+  if (occ < 1) { pl.why = "stream3d: not co-resident"; return pl; }
+  const int resident = occ * p.num_sms;
   // z chunks: about two waves of units for the host loop; exactly one wave for the persistent
-  // kernel (one unit per CTA per step, so no CTA idles at the tail)
-  const int tiles = tx * ty;
+  // kernels (one unit per CTA per step, so no CTA idles at the tail)
   int nzc = persistent ? std::max(1, resident / tiles) : std::max(1, (2 * resident + tiles - 1) / tiles);
   nzc = std::min<int>(nzc, (int)std::max<int64_t>(1, p.nz / 8));
+  if (persistent && env_int("PERKS_S3D_NZC", 0) > 0) nzc = std::min<int>(env_int("PERKS_S3D_NZC", 0), (int)p.nz);  // sweeps
   const int zc = (int)((p.nz + nzc - 1) / nzc);
   nzc = (int)((p.nz + zc - 1) / zc);
   pl.units = (int64_t)tiles * nzc;
@@ -268,15 +412,34 @@ Plan plan_stream3d(const Problem &p, perks_variant v) {
   pl.smem = (int)smem;
   pl.ctas_per_sm = occ;
   pl.grid = persistent ? (int)std::min<int64_t>(pl.units, resident) : (int)pl.units;
-  pl.cfg = use_tma3(p) ? 1 : 0;
+  pl.cfg = tma ? 1 : 0;
+  pl.family = cache ? 2 : 0;  // (2: PERKS 3D, supports multi-GPU slabs)
+  pl.nc = cache ? std::min(nc, std::max(0, zc - 2)) : 0;
   const double S = (double)p.elem();
-  pl.dram_bytes_step = 2.0 * S * (double)p.cells();
+  // cached cells: every CTA's first unit caches nc planes of its tile (last z-chunk may be shorter)
+  int64_t cached = 0;
+  if (cache) {
+    for (int cz = 0; cz < nzc; cz++) {
+      const int len = (int)std::min<int64_t>(zc, p.nz - (int64_t)cz * zc);
+      cached += (int64_t)tiles * std::min(pl.nc, std::max(0, len - 2));
+    }
+    if (pl.units > pl.grid) cached = cached * pl.grid / pl.units;
+    cached *= (int64_t)TX * TY;
+    cached = std::min<int64_t>(cached, p.cells());
+  }
+  pl.cached_smem = cached;
+  pl.dram_bytes_step = 2.0 * S * ((double)p.cells() - (double)cached);
   pl.halo_bytes_step = S * (double)p.nz * (2.0 * TX * ty * tx + 2.0 * TY * ty * tx) +
                        S * 2.0 * nzc * (double)p.nx * p.ny;
   pl.ws_bytes = align256((size_t)p.cells() * p.elem()) + (persistent ? 256 : 0);
-  snprintf(pl.name, sizeof(pl.name), "%s3d_%s_%s_t%dx%d_z%d%s", persistent ? "persistent" : "hostloop",
+  snprintf(pl.name, sizeof(pl.name), "%s3d_%s_%s_t%dx%d_z%d%s", cache ? "perks" : persistent ? "persistent" : "hostloop",
            p.shape == SHAPE_3D7 ? "7pt" : "27pt", p.dtype == PERKS_F32 ? "f32" : "f64", TX, TY, zc,
-           pl.cfg ? "_tma" : "_cpasync");
+           cache ? "_c" : (pl.cfg ? "_tma" : "_cpasync"));
+  if (cache) {
+    char extra[24];
+    snprintf(extra, sizeof(extra), "%d_%dcta", pl.nc, occ);
+    strncat(pl.name, extra, sizeof(pl.name) - strlen(pl.name) - 1);
+  }
   pl.ok = true;
   return pl;
 }
@@ -285,7 +448,6 @@ namespace {
 // Everything one 3D streaming launch needs, prepared once per run.
 template <typename T, int S>
 struct Launch3 {
-  using G = typename G3Sel<T>::G;
   Coef<T, Shape<S>::N> c;
   Dom3 d;
   Units3 u;
@@ -299,12 +461,17 @@ struct Launch3 {
   bool tma;
   int grid;
   int zigzag;
+  bool cache = false;
+  Cache3 ch{0};
+  int block = 0;
 
   cudaError_t setup(const Problem &p, const Plan &pl, const T *in_, T *out_, T *tmp_, unsigned *bar_,
                     const DistRun *dr) {
     for (int i = 0; i < Shape<S>::N; i++) c.w[i] = sizeof(T) == 4 ? (T)p.wf[i] : (T)p.wd[i];
     d = make_dom3(p);
-    u = Units3{(int)((p.nx + G::TX - 1) / G::TX), (int)((p.ny + G::TY - 1) / G::TY), 0, pl.zchunk, 0};
+    u = Units3{(int)((p.nx + pl.tile[0] - 1) / pl.tile[0]), (int)((p.ny + pl.tile[1] - 1) / pl.tile[1]), 0,
+               pl.zchunk, 0};
+    block = pl.block;
     u.nzc = (int)((p.nz + u.zc - 1) / u.zc);
     zigzag = env_int("PERKS_ZIGZAG", 0);  // experiment knob; off by default
     smem = (size_t)pl.smem;
@@ -314,9 +481,14 @@ struct Launch3 {
     dk = make_distk(dr);
     xbase = dr ? dr->xbase : 0;
     dist = p.nranks > 1;
+    cache = pl.family == 2;
+    ch.nc = pl.nc;
     if (dist && !tma) return cudaErrorNotSupported;
     std::memset(&maps, 0, sizeof(maps));
-    if (tma && !make_maps3(p, G::P, G::ROWS, in, out, tmp, &maps, dr ? dr->ghost : nullptr))
+    const bool ws = pl.variant != PERKS_HOSTLOOP || PERKS_S3D_HWS;
+    const int P = ws ? GS<T, true>::G::P : GS<T, false>::G::P;
+    const int ROWS = ws ? GS<T, true>::G::ROWS : GS<T, false>::G::ROWS;
+    if (tma && !make_maps3(p, P, ROWS, in, out, tmp, &maps, dr ? dr->ghost : nullptr))
       return cudaErrorInvalidValue;
     return cudaSuccess;
   }
@@ -334,21 +506,22 @@ struct Launch3 {
     unsigned long long e = xbase + (unsigned long long)t;
     void *args[] = {(void *)&src, (void *)&maps, (void *)&src_idx, (void *)&dst, (void *)&d,
                     (void *)&uu, (void *)&c, (void *)&dk, (void *)&e};
-    return cudaLaunchKernel(k, dim3(grid), dim3(G::NT), args, smem, s);
+    return cudaLaunchKernel(k, dim3(grid), dim3(block), args, smem, s);
   }
   // persistent (b): one launch; cooperative on a single GPU (co-residency guaranteed by the driver)
   cudaError_t persistent(int64_t steps, cudaStream_t s, bool cooperative) {
-    void *k = dist ? (void *)persistent3d_kernel<T, S, true, true>
-                   : tma ? (void *)persistent3d_kernel<T, S, true, false> : (void *)persistent3d_kernel<T, S, false, false>;
+    void *k = cache ? (dist ? (void *)persistent3d_kernel<T, S, true, true, true> : (void *)persistent3d_kernel<T, S, true, false, true>)
+            : dist ? (void *)persistent3d_kernel<T, S, true, true, false>
+                   : tma ? (void *)persistent3d_kernel<T, S, true, false, false> : (void *)persistent3d_kernel<T, S, false, false, false>;
     Units3 uu = u;
     uu.rev = zigzag;
     cudaError_t e = cudaMemsetAsync(bar, 0, 256, s);
     if (e != cudaSuccess) return e;
     void *args[] = {(void *)&in, (void *)&out, (void *)&tmp, (void *)&maps, (void *)&d, (void *)&uu,
-                    (void *)&steps, (void *)&bar, (void *)&c, (void *)&dk, (void *)&xbase};
+                    (void *)&steps, (void *)&bar, (void *)&c, (void *)&dk, (void *)&xbase, (void *)&ch};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(G::NT);
+    cfg.blockDim = dim3(block);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute at[1];

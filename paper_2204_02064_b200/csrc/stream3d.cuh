@@ -24,6 +24,13 @@
 
 namespace perks {
 
+// Unroll factor of the per-plane loops (3 turns the stage-accumulator rotation into register
+// renaming; sweeps only, the default keeps register pressure low).
+#ifndef PERKS_WS_UNROLL
+#define PERKS_WS_UNROLL 1
+#endif
+constexpr int kWsUnroll = PERKS_WS_UNROLL;
+
 template <typename T, int V_, int R_, int NWARP_, int NS_>
 struct Geo3D {
   static constexpr int V = V_, R = R_, NWARP = NWARP_, NS = NS_;
@@ -70,6 +77,9 @@ PERKS_DEVINL void mbar_arrive(uint64_t *b) {
 // arrive when all of this thread's prior cp.async copies have landed
 PERKS_DEVINL void mbar_arrive_cpasync(uint64_t *b) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+PERKS_DEVINL void mbar_arrive_release(uint64_t *b) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
 }
 PERKS_DEVINL void mbar_wait(uint64_t *b, unsigned parity) {
   asm volatile(
@@ -249,6 +259,9 @@ struct ThreadTile {
   bool xin;          // x < nx (vector start inside the domain)
   bool inner;        // all owned cells interior in x and y (no frame select needed)
   bool vec;          // rows 16-byte aligned: vector stores
+  bool full;         // xin && vec && all R rows inside: the branch-free store path
+  size_t off;        // y * nx + x (offset inside a plane)
+  size_t plane;      // nx * ny
   PERKS_DEVINL void init(const Dom3 &d, int x0, int y0) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     x = x0 + lane * G::V;
@@ -256,6 +269,9 @@ struct ThreadTile {
     xin = x < d.nx;
     inner = x >= 1 && x + G::V - 1 <= d.nx - 2 && y >= 1 && y + G::R - 1 <= d.ny - 2;
     vec = (d.nx % G::V) == 0;
+    full = xin && vec && y + G::R <= d.ny;
+    off = (size_t)y * d.nx + x;
+    plane = (size_t)d.nx * d.ny;
   }
 };
 
@@ -279,6 +295,12 @@ PERKS_DEVINL void frame_select(const Dom3 &d, const ThreadTile<G> &tt, int o, T 
 template <typename T, class G>
 PERKS_DEVINL void store_cells(T *__restrict__ dst, const Dom3 &d, const ThreadTile<G> &tt, int o,
                               const T (&v)[G::R][G::V]) {
+  if (tt.full) {  // the common case: R aligned vector stores, no per-row tests
+    T *p = dst + (size_t)o * tt.plane + tt.off;
+#pragma unroll
+    for (int r = 0; r < G::R; r++) vstore<T, G::V>(p + (size_t)r * d.nx, v[r]);
+    return;
+  }
   if (!tt.xin) return;
   T *base = dst + (size_t)o * d.nx * d.ny;
 #pragma unroll
@@ -533,6 +555,7 @@ PERKS_DEVINL void stream_unit(Ring<T, G, TMA> &ring, const T *__restrict__ src,
   }
   StreamState<T, G> st;
   st.zero();
+#pragma unroll kWsUnroll
   for (int k = 0; k < narr; k++) {
     const int q = q0 + k;
     ring.wait(k0 + k);
@@ -561,6 +584,193 @@ PERKS_DEVINL void stream_unit(Ring<T, G, TMA> &ring, const T *__restrict__ src,
   }
   ring.gk = k0 + narr;
   ring.drain();
+}
+
+
+// ================================================================ warp-specialised pipeline (TMA)
+
+// Warps 0..NWARP-1 compute ("consumers"); warp NWARP is the producer.  Slot i of the NS-slot ring
+// has two mbarriers: full[i] (1 expect_tx arrival + 32 producer-lane arrivals, TMA/bulk
+// transaction bytes) and empty[i] (one arrival per consumer warp).  Consumer warps never
+// synchronise with each other per plane — each waits only for the plane it needs and releases it
+// when done — so warps drift within the ring depth and latency is hidden with few CTAs per SM
+// (the occupancy-vs-concurrency trade-off of P:719-738 without a CTA barrier per plane).
+// Arrival index k runs across units and steps; slot = k % NS, phase = (k / NS) & 1.
+template <typename T, class G>
+struct WsPipe {
+  static constexpr unsigned FULL_COUNT = 33;
+  T *slots;
+  uint64_t *full, *empty;
+  unsigned gk;
+
+  PERKS_DEVINL T *slot(unsigned k) const { return slots + (size_t)(k % G::NS) * G::SLOT; }
+  PERKS_DEVINL uint64_t *fb(unsigned k) const { return full + (k % G::NS); }
+  PERKS_DEVINL uint64_t *eb(unsigned k) const { return empty + (k % G::NS); }
+
+  // all threads: thread 0 initialises the barriers
+  PERKS_DEVINL void init(T *s, uint64_t *bars) {
+    slots = s;
+    full = bars;
+    empty = bars + G::NS;
+    gk = 0;
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < G::NS; i++) {
+        mbar_init(full + i, FULL_COUNT);
+        mbar_init(empty + i, G::NWARP);
+      }
+      mbar_fence_init();
+    }
+    __syncthreads();
+  }
+  // ---- producer (warp NWARP, all lanes) ----
+  // slot of arrival k free again (all consumer warps released arrival k - NS)
+  PERKS_DEVINL void acquire(unsigned k) {
+    if (k >= G::NS) mbar_wait(eb(k), ((k / G::NS) + 1) & 1u);
+    if ((threadIdx.x & 31) == 0) fence_proxy_async();  // consumers' generic reads -> TMA writes
+    __syncwarp();
+  }
+  PERKS_DEVINL void load_box(unsigned k, T *dst, const CUtensorMap *map, int x0, int y0, int z) {
+    if ((threadIdx.x & 31) == 0) {
+      mbar_arrive_tx(fb(k), G::BOX_BYTES);
+      tma_load_3d(dst, map, x0 - G::PAD, y0 - 1, z, fb(k));
+    }
+    mbar_arrive(fb(k));
+  }
+  PERKS_DEVINL void load_full(unsigned k, const CUtensorMap *map, int x0, int y0, int q) {
+    load_box(k, slot(k), map, x0, y0, q);
+  }
+  PERKS_DEVINL void load_ghost(unsigned k, const CUtensorMap *gmap, int gz, int x0, int y0,
+                               const unsigned long long *ctr, unsigned long long target) {
+    if ((threadIdx.x & 31) == 0) {
+      wait_counter_sys(ctr, target);
+      fence_proxy_async_global();
+    }
+    __syncwarp();
+    load_box(k, slot(k), gmap, x0, y0, gz);
+  }
+  // halo ring only (PERKS cached plane q) into `dst`: rows by bulk copies (lane 0), the two
+  // columns by per-lane cp.async completing on the same barrier
+  PERKS_DEVINL void load_halo(unsigned k, T *dst, const T *src, const Dom3 &d, int q, int x0, int y0) {
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) {
+      const int xa = max(x0 - G::PAD, 0), xb = min(x0 + G::TX + G::PAD, d.nx);
+      const unsigned rb = (unsigned)((xb - xa) * (int)sizeof(T));
+      const bool top = y0 >= 1, bot = y0 + G::TY < d.ny;
+      mbar_arrive_tx(fb(k), (top ? rb : 0u) + (bot ? rb : 0u));
+      const size_t pl = (size_t)d.nx * d.ny;
+      if (top) bulk_load(dst + (xa - (x0 - G::PAD)), src + (size_t)q * pl + (size_t)(y0 - 1) * d.nx + xa, rb, fb(k));
+      if (bot)
+        bulk_load(dst + (G::ROWS - 1) * G::P + (xa - (x0 - G::PAD)),
+                  src + (size_t)q * pl + (size_t)(y0 + G::TY) * d.nx + xa, rb, fb(k));
+    }
+    for (int t = lane; t < 2 * G::TY; t += 32) {
+      const int j = 1 + (t >> 1);
+      const bool right = t & 1;
+      const int y = y0 - 1 + j;
+      const int xx = right ? x0 + G::TX : x0 - 1;
+      const bool ok = y < d.ny && xx >= 0 && xx < d.nx;
+      const T *g = ok ? src + ((size_t)q * d.ny + y) * d.nx + xx : src;
+      cp_async<(int)sizeof(T)>(dst + j * G::P + (right ? G::PAD + G::TX : G::PAD - 1), g, ok);
+    }
+    mbar_arrive_cpasync(fb(k));
+  }
+  // ---- consumers (warps 0..NWARP-1) ----
+  PERKS_DEVINL void wait_full(unsigned k) { mbar_wait(fb(k), (k / G::NS) & 1u); }
+  PERKS_DEVINL void release(unsigned k) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive_release(eb(k));
+  }
+  // every consumer warp has released arrival k (its slot's reads are complete)
+  PERKS_DEVINL void wait_released(unsigned k) { mbar_wait(eb(k), (k / G::NS) & 1u); }
+};
+
+// Named barrier over the consumer warps only (the producer keeps streaming).
+template <class G> PERKS_DEVINL void consumers_sync() {
+  asm volatile("bar.sync 1, %0;\n" ::"n"(32 * G::NWARP) : "memory");
+}
+
+// Face plane o to the neighbour's ghost plane (multi-GPU), consumer warps only.
+template <typename T, class G>
+PERKS_DEVINL void send_face_ws(const DistStep &ds, const Dom3 &d, const ThreadTile<G> &tt, int o,
+                               int x0, int y0, const T (&v)[G::R][G::V]) {
+  const bool lo = o == 0 && ds.k->has_lo, hi = o == d.nz - 1 && ds.k->has_hi;
+  if (!lo && !hi) return;
+  const int gz = (int)((ds.e + 1) & 1) * 2 + (lo ? 1 : 0);
+  store_cells<T, G>(reinterpret_cast<T *>(lo ? ds.k->send_lo : ds.k->send_hi), d, tt, gz, v);
+  __threadfence_system();
+  consumers_sync<G>();
+  if (threadIdx.x == 0) {
+    const unsigned long long cells =
+        (unsigned long long)min(G::TX, d.nx - x0) * (unsigned long long)min(G::TY, d.ny - y0);
+    red_release_sys_add_u64(lo ? ds.k->peer_ctr_lo : ds.k->peer_ctr_hi, cells);
+  }
+}
+
+// One unit (tile x0,y0; planes [zs, ze)) of one step through the warp-specialised pipeline.
+// Called by ALL warps of the CTA; the producer issues arrivals zs-1 .. ze, the consumers run the
+// staged plane body (arrival(), stages A/B/C) and store / cache the outputs.
+template <typename T, int S, class G, bool DIST, bool CACHE = false>
+PERKS_DEVINL void stream_unit_ws(WsPipe<T, G> &pp, const T *__restrict__ src, const CUtensorMap *map,
+                                 T *__restrict__ dst, const Dom3 &d, int x0, int y0, int zs, int ze,
+                                 const Coef<T, Shape<S>::N> &c, const DistStep &ds,
+                                 const CacheView<T> &cv = CacheView<T>{}) {
+  const int q0 = zs - 1;
+  const int narr = ze - zs + 2;
+  const unsigned k0 = pp.gk;
+  auto cs = [&](int q) -> int {
+    if constexpr (!CACHE) return -1;
+    return (q > cv.czs && q < cv.cze - 1) ? (int)cv.cmap[q - cv.czs] : -1;
+  };
+  pp.gk = k0 + narr;
+  if ((int)(threadIdx.x >> 5) == G::NWARP) {  // ---- producer
+    for (int k = 0; k < narr; k++) {
+      const unsigned kk = k0 + k;
+      const int q = q0 + k;
+      pp.acquire(kk);
+      const int sl = cs(q);
+      if (CACHE && sl >= 0) {
+        pp.load_halo(kk, cv.cache + (size_t)sl * G::SLOT, src, d, q, x0, y0);
+      } else {
+        const int gs = DIST ? ghost_side(ds, d, q) : -1;
+        if (gs < 0) pp.load_full(kk, map, x0, y0, q);
+        else pp.load_ghost(kk, ds.gmap, (int)(ds.e & 1) * 2 + gs, x0, y0, ds.k->ctr + gs,
+                           (ds.e + 1) * ds.plane_cells);
+      }
+    }
+    return;
+  }
+  // ---- consumers
+  ThreadTile<G> tt;
+  tt.init(d, x0, y0);
+  StreamState<T, G> st;
+  st.zero();
+#pragma unroll kWsUnroll  // (3: the accumulator rotation of arrival() becomes renaming)
+  for (int k = 0; k < narr; k++) {
+    const unsigned kk = k0 + k;
+    const int q = q0 + k;
+    const int slq = cs(q);
+    pp.wait_full(kk);
+    T out[G::R][G::V], cq[G::R][G::V];
+    arrival<T, S, G>(st, (CACHE && slq >= 0) ? cv.cache + (size_t)slq * G::SLOT : pp.slot(kk), c, out, cq);
+    pp.release(kk);
+    if (q - 1 >= zs) {
+      frame_select<T, G>(d, tt, q - 1, out, st.cm1);
+      const int slo = cs(q - 1);
+      if (CACHE && slo >= 0) {
+        // cached output: stays on chip once every warp has finished reading the old plane
+        publish_perimeter<T, G>(dst, d, q - 1, x0, y0, out);
+        pp.wait_released(kk - 1);
+        write_own<T, G>(cv.cache + (size_t)slo * G::SLOT, out);
+      } else {
+        store_cells<T, G>(dst, d, tt, q - 1, out);
+        if constexpr (DIST) send_face_ws<T, G>(ds, d, tt, q - 1, x0, y0, out);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < G::R; r++)
+#pragma unroll
+      for (int i = 0; i < G::V; i++) st.cm1[r][i] = cq[r][i];
+  }
 }
 
 }  // namespace perks

@@ -1,10 +1,11 @@
 cd /root/repo
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q -k "3d or dist" > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "perks3d_cache" > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
 (
-for k in 1 2 3; do echo "== K $k"; PERKS_P3D_K=$k timeout 300 python tools/quick_bench.py C3,C4 perks 2>&1 | grep -v speedup; done
-echo "== nozz"; PERKS_ZIGZAG=0 timeout 300 python tools/quick_bench.py C3,C4 perks 2>&1 | grep -v speedup
-echo "== nsm0"; PERKS_P3D_NSM=0 timeout 300 python tools/quick_bench.py C3,C4 perks 2>&1 | grep -v speedup
-for n in p3cps3 p3ns6 p3r1; do echo "== $n"; PERKS_LIB_PATH=build/var_$n/libperks_stencil.so timeout 300 python tools/quick_bench.py C3,C4 perks 2>&1 | grep -v speedup; done
-timeout 300 python tools/quick_bench.py C3,C4 hostloop
-) > gpurun_out/perks3d_sweep.log 2>&1
+for lib in default ws8 ws8ns6 ws7ns6 ws8ns8; do
+  if [ $lib = default ]; then L=""; else L=build/var_$lib/libperks_stencil.so; fi
+  for nzc in 0 1 2 4; do
+    echo "== $lib nzc=$nzc"; PERKS_LIB_PATH=$L PERKS_S3D_NZC=$nzc timeout 300 python tools/quick_bench.py C3,C4 persistent,perks 2>&1 | grep -v speedup
+  done
+done
+) > gpurun_out/persist_sweep.log 2>&1
