@@ -38,7 +38,7 @@ static_assert(G3Sel<float>::G::NT == K3D_THREADS && G3Sel<double>::G::NT == K3D_
 // Warp-specialised kernels: PERKS_WS_NWARP consumer warps + 1 producer warp = 256 threads, so two
 // CTAs per SM keep a 128-register budget.
 #ifndef PERKS_WS_NWARP
-#define PERKS_WS_NWARP 7
+#define PERKS_WS_NWARP 8
 #endif
 template <typename T, bool WS> struct GS { using G = typename G3Sel<T>::G; };
 template <typename T> struct GS<T, true> {
@@ -117,7 +117,7 @@ PERKS_DEVINL int cache_slot_of(int j, int len, int nc) {
 }
 
 template <typename T, int S, bool TMA, bool DIST, bool CACHE>
-__global__ void __launch_bounds__(k3d_threads<TMA>(), (CACHE && DIST) ? 1 : 2) persistent3d_kernel(
+__global__ void __launch_bounds__(k3d_threads<TMA>(), DIST ? 1 : 2) persistent3d_kernel(
     const T *__restrict__ in, T *out, T *tmp, const __grid_constant__ Maps3 maps, Dom3 d, Units3 u,
     int64_t steps, unsigned *bar, Coef<T, Shape<S>::N> c, const __grid_constant__ DistK dk,
     unsigned long long xbase, Cache3 ch) {
