@@ -362,7 +362,16 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
 
 namespace {
 // Configurations (index = Plan::cfg).  f32 V=4, f64 V=2 (16-byte vectors per thread-row).
-using P2F_A = Geo2P<float, 4, 2, 4, 16, 48>;   // 256 x 256 tile, 256 thr, 64 KiB regs + 192 KiB smem
+#ifndef PERKS_P2F_WY
+#define PERKS_P2F_WY 4
+#endif
+#ifndef PERKS_P2F_RR
+#define PERKS_P2F_RR 16
+#endif
+#ifndef PERKS_P2F_RS
+#define PERKS_P2F_RS 48
+#endif
+using P2F_A = Geo2P<float, 4, 2, PERKS_P2F_WY, PERKS_P2F_RR, PERKS_P2F_RS>;   // default 256 x 256 tile, 256 thr, 64 KiB regs + 192 KiB smem
 using P2F_B = Geo2P<float, 4, 1, 8, 8, 8>;     // 128 x 128 tile, 256 thr
 using P2F_C = Geo2P<float, 4, 1, 4, 8, 0>;     // 128 x  32 tile, 128 thr
 using P2D_A = Geo2P<double, 2, 2, 4, 16, 16>;  // 128 x 128 tile, 256 thr, 64 KiB regs + 64 KiB smem

@@ -399,8 +399,21 @@ Plan plan_stream3d(const Problem &p, perks_variant v) {
   const int resident = occ * p.num_sms;
   // z chunks: about two waves of units for the host loop; exactly one wave for the persistent
   // kernels (one unit per CTA per step, so no CTA idles at the tail)
-  int nzc = persistent ? std::max(1, resident / tiles) : std::max(1, (2 * resident + tiles - 1) / tiles);
+  int nzc = std::max(1, (2 * resident + tiles - 1) / tiles);
   nzc = std::min<int>(nzc, (int)std::max<int64_t>(1, p.nz / 8));
+  if (persistent) {
+    // persistent kernels: pick the z-chunking that minimises the busiest CTA's planes per step,
+    // ceil(units / grid) * (chunk + 2 halo planes), with grid <= resident CTAs (load balance over
+    // 148 SMs: e.g. C3 64 tiles x 4 chunks on 256 CTAs; C5 1024 tiles x 2 chunks)
+    int64_t best = -1;
+    for (int n = 1; n <= std::max<int64_t>(1, p.nz / 4); n++) {
+      const int64_t zcn = (p.nz + n - 1) / n, nn = (p.nz + zcn - 1) / zcn;
+      if (nn != n) continue;
+      const int64_t un = (int64_t)tiles * n, g = std::min<int64_t>(un, resident);
+      const int64_t cost = ((un + g - 1) / g) * (zcn + 2);
+      if (best < 0 || cost < best) { best = cost; nzc = n; }
+    }
+  }
   if (persistent && env_int("PERKS_S3D_NZC", 0) > 0) nzc = std::min<int>(env_int("PERKS_S3D_NZC", 0), (int)p.nz);  // sweeps
   const int zc = (int)((p.nz + nzc - 1) / nzc);
   nzc = (int)((p.nz + zc - 1) / zc);
