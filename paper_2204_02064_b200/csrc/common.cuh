@@ -43,20 +43,42 @@ template <> struct VecT<double, 2> { using type = double2; };
 
 template <typename T, int V>
 PERKS_DEVINL void vload(T (&v)[V], const T *p) {
-  using VT = typename VecT<T, V>::type;
-  VT t = *reinterpret_cast<const VT *>(p);
-  const T *s = reinterpret_cast<const T *>(&t);
+  if constexpr (V * sizeof(T) > 16) {  // several 16-byte vectors
+    constexpr int C = 16 / (int)sizeof(T);
 #pragma unroll
-  for (int i = 0; i < V; i++) v[i] = s[i];
+    for (int j = 0; j < V / C; j++) {
+      T w[C];
+      vload<T, C>(w, p + j * C);
+#pragma unroll
+      for (int i = 0; i < C; i++) v[j * C + i] = w[i];
+    }
+  } else {
+    using VT = typename VecT<T, V>::type;
+    VT t = *reinterpret_cast<const VT *>(p);
+    const T *s = reinterpret_cast<const T *>(&t);
+#pragma unroll
+    for (int i = 0; i < V; i++) v[i] = s[i];
+  }
 }
 template <typename T, int V>
 PERKS_DEVINL void vstore(T *p, const T (&v)[V]) {
-  using VT = typename VecT<T, V>::type;
-  VT t;
-  T *d = reinterpret_cast<T *>(&t);
+  if constexpr (V * sizeof(T) > 16) {
+    constexpr int C = 16 / (int)sizeof(T);
 #pragma unroll
-  for (int i = 0; i < V; i++) d[i] = v[i];
-  *reinterpret_cast<VT *>(p) = t;
+    for (int j = 0; j < V / C; j++) {
+      T w[C];
+#pragma unroll
+      for (int i = 0; i < C; i++) w[i] = v[j * C + i];
+      vstore<T, C>(p + j * C, w);
+    }
+  } else {
+    using VT = typename VecT<T, V>::type;
+    VT t;
+    T *d = reinterpret_cast<T *>(&t);
+#pragma unroll
+    for (int i = 0; i < V; i++) d[i] = v[i];
+    *reinterpret_cast<VT *>(p) = t;
+  }
 }
 // L2-only (bypass L1) loads for data produced by other CTAs during the same launch.
 template <typename T> PERKS_DEVINL T ld_cg(const T *p) { return __ldcg(p); }

@@ -371,7 +371,10 @@ namespace {
 #ifndef PERKS_P2F_RS
 #define PERKS_P2F_RS 48
 #endif
-using P2F_A = Geo2P<float, 4, 2, PERKS_P2F_WY, PERKS_P2F_RR, PERKS_P2F_RS>;   // default 256 x 256 tile, 256 thr, 64 KiB regs + 192 KiB smem
+#ifndef PERKS_P2F_V
+#define PERKS_P2F_V 4
+#endif
+using P2F_A = Geo2P<float, PERKS_P2F_V, 8 / PERKS_P2F_V, PERKS_P2F_WY, PERKS_P2F_RR, PERKS_P2F_RS>;   // default 256 x 256 tile, 256 thr, 64 KiB regs + 192 KiB smem
 using P2F_B = Geo2P<float, 4, 1, 8, 8, 8>;     // 128 x 128 tile, 256 thr
 using P2F_C = Geo2P<float, 4, 1, 4, 8, 0>;     // 128 x  32 tile, 128 thr
 using P2D_A = Geo2P<double, 2, 2, 4, 16, 16>;  // 128 x 128 tile, 256 thr, 64 KiB regs + 64 KiB smem

@@ -40,6 +40,9 @@ static_assert(G3Sel<float>::G::NT == K3D_THREADS && G3Sel<double>::G::NT == K3D_
 #ifndef PERKS_WS_NWARP
 #define PERKS_WS_NWARP 8
 #endif
+#ifndef PERKS_WS_MINB
+#define PERKS_WS_MINB 2
+#endif
 template <typename T, bool WS> struct GS { using G = typename G3Sel<T>::G; };
 template <typename T> struct GS<T, true> {
   using G = Geo3D<T, 16 / (int)sizeof(T), PERKS_S3D_R, PERKS_WS_NWARP, PERKS_S3D_NS>;
@@ -117,7 +120,7 @@ PERKS_DEVINL int cache_slot_of(int j, int len, int nc) {
 }
 
 template <typename T, int S, bool TMA, bool DIST, bool CACHE>
-__global__ void __launch_bounds__(k3d_threads<TMA>(), DIST ? 1 : 2) persistent3d_kernel(
+__global__ void __launch_bounds__(k3d_threads<TMA>(), DIST ? 1 : PERKS_WS_MINB) persistent3d_kernel(
     const T *__restrict__ in, T *out, T *tmp, const __grid_constant__ Maps3 maps, Dom3 d, Units3 u,
     int64_t steps, unsigned *bar, Coef<T, Shape<S>::N> c, const __grid_constant__ DistK dk,
     unsigned long long xbase, Cache3 ch) {
@@ -380,7 +383,7 @@ Plan plan_stream3d(const Problem &p, perks_variant v) {
     // PERKS: the shared memory the ring leaves at `cps` CTAs per SM caches planes (
     // minimal occupancy that keeps the HBM stream saturated: 2 CTAs/SM measured best)
     const int force_cps = env_int("PERKS_P3D_CPS", 0);
-    for (int cps = force_cps > 0 ? force_cps : 2; cps >= 1; cps--) {
+    for (int cps = force_cps > 0 ? force_cps : PERKS_WS_MINB; cps >= 1; cps--) {
       const size_t budget = std::min<size_t>((size_t)p.max_smem_optin, (size_t)p.smem_per_sm / cps - 1024);
       const size_t fixed = ring + 128 + align256((size_t)p.nz * sizeof(short));
       nc = budget > fixed ? (int)((budget - fixed) / slot) : 0;
