@@ -117,8 +117,15 @@ const Plan &get_plan(perks_stencil_s *h, perks_variant v) {
       pl = p.ndim == 2 ? plan_stream2d(p, v) : plan_stream3d(p, v);
     else if (v == PERKS_PERKS && p.ndim == 2) {
       pl = plan_perks2d_cluster(p);  // small domains: one cluster, registers only
-      if (pl.ok) pl.family = 1;
-      else pl = plan_perks2d(p);
+      if (pl.ok) {
+        pl.family = 1;
+      } else {
+        // full-width strips (fp32, 1025..3072 wide) are opt-in: measured slower than square tiles
+        // on C2 (profiles/r01_c2_strip_first.txt), kept as a tested alternative
+        if (env_int("PERKS_STRIP", 0)) pl = plan_perks2d_strip(p);
+        if (pl.ok && env_int("PERKS_STRIP", 0)) pl.family = 3;
+        else pl = plan_perks2d(p);   // square tiles
+      }
     } else if (v == PERKS_PERKS)
       pl = plan_stream3d(p, PERKS_PERKS);
     h->plans[i] = pl;
@@ -238,6 +245,9 @@ static perks_status create_impl(const perks_stencil_desc *d, int device, int ran
       e = cudaDeviceGetAttribute(&p.max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     if (e == cudaSuccess)
       e = cudaDeviceGetAttribute(&p.smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+    int l2 = 0;
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device);
+    p.l2_bytes = l2;
     if (e != cudaSuccess) { delete h; return cuda_fail(e); }
     const int force_sms = env_int("PERKS_NUM_SMS", 0);  // sweeps only
     if (force_sms > 0 && force_sms < p.num_sms) p.num_sms = force_sms;
@@ -433,7 +443,8 @@ perks_status perks_stencil_run(perks_stencil_t h, perks_variant v, const void *d
     case PERKS_PERKS:
       if (p.ndim == 2)
         e = pl.family == 1 ? run_perks2d_cluster(p, pl, d_in, d_out, steps, s)
-                           : run_perks2d(p, pl, d_in, d_out, d_ws, steps, s);
+            : pl.family == 3 ? run_perks2d_strip(p, pl, d_in, d_out, d_ws, steps, s)
+                             : run_perks2d(p, pl, d_in, d_out, d_ws, steps, s);
       else
         e = run_stream3d(p, pl, d_in, d_out, d_ws, steps, s);
       break;

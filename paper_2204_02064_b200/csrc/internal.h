@@ -23,6 +23,7 @@ struct Problem {
   int num_sms;
   int max_smem_optin;
   int smem_per_sm;
+  int64_t l2_bytes = 0;
   size_t elem() const { return dtype == PERKS_F64 ? 8 : 4; }
   int64_t cells() const { return nx * ny * nz; }
 };
@@ -38,8 +39,9 @@ struct Plan {
   int64_t units = 0;          // work units per step
   int zchunk = 0;             // planes per unit (3D)
   int cfg = 0;                // index of the kernel configuration
-  int family = 0;             // kernel family within a variant (2D PERKS: 0 tiles, 1 cluster; 3D PERKS: 2)
+  int family = 0;             // kernel family within a variant (2D PERKS: 0 tiles, 1 cluster, 3 strips; 3D PERKS: 2)
   int nc = 0;                 // 3D PERKS: shared-memory plane slots per CTA
+  int wsg = 0;                // 3D persistent: warp-specialised geometry (k3d_stream.cu)
   int64_t cached_reg = 0, cached_smem = 0;
   double dram_bytes_step = 0, halo_bytes_step = 0;
   size_t ws_bytes = 0;
@@ -83,6 +85,10 @@ cudaError_t run_perks2d(const Problem &p, const Plan &pl, const void *in, void *
 Plan plan_perks2d_cluster(const Problem &p);
 cudaError_t run_perks2d_cluster(const Problem &p, const Plan &pl, const void *in, void *out,
                                 int64_t steps, cudaStream_t s);
+// PERKS (c), 2D fp32 domains 1025..3072 wide: full-width strips, edge rows first.
+Plan plan_perks2d_strip(const Problem &p);
+cudaError_t run_perks2d_strip(const Problem &p, const Plan &pl, const void *in, void *out, void *ws,
+                              int64_t steps, cudaStream_t s);
 // PERKS (c), 3D: the persistent kernel with a shared-memory plane cache (k3d_stream.cu).
 
 // Environment override helper (sweeps only): returns def if unset.

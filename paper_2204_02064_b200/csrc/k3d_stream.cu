@@ -35,17 +35,15 @@ template <> struct G3Sel<double> { using G = Geo3D<double, 2, PERKS_S3D_R, 8, PE
 
 constexpr int K3D_THREADS = 256;
 static_assert(G3Sel<float>::G::NT == K3D_THREADS && G3Sel<double>::G::NT == K3D_THREADS, "3D block size");
-// Warp-specialised kernels: PERKS_WS_NWARP consumer warps + 1 producer warp = 256 threads, so two
-// CTAs per SM keep a 128-register budget.
-#ifndef PERKS_WS_NWARP
-#define PERKS_WS_NWARP 8
-#endif
-#ifndef PERKS_WS_MINB
-#define PERKS_WS_MINB 2
-#endif
-template <typename T, bool WS> struct GS { using G = typename G3Sel<T>::G; };
-template <typename T> struct GS<T, true> {
-  using G = Geo3D<T, 16 / (int)sizeof(T), PERKS_S3D_R, PERKS_WS_NWARP, PERKS_S3D_NS>;
+// Warp-specialised geometries (consumer warps + 1 producer warp, CTAs per SM), chosen per problem
+// by the planner (profiles/r01_ws_geometry_sweep.txt): WSG 0 = 8 warps x 2 CTAs/SM (best while the
+// domain is within a few L2 sizes, C3/C4); WSG 1 = 4 warps x 3 CTAs/SM (more independent plane
+// streams in flight: best for domains far larger than L2, C5).
+constexpr int wsg_nwarp(int g) { return g == 0 ? 8 : 4; }
+constexpr int wsg_minb(int g) { return g == 0 ? 2 : 3; }
+template <typename T, bool WS, int WSG = 0> struct GS { using G = typename G3Sel<T>::G; };
+template <typename T, int WSG> struct GS<T, true, WSG> {
+  using G = Geo3D<T, 16 / (int)sizeof(T), PERKS_S3D_R, wsg_nwarp(WSG), PERKS_S3D_NS>;
 };
 
 struct Units3 {
@@ -78,7 +76,7 @@ template <class G> PERKS_DEVINL uint64_t *ring_bars(unsigned char *smem) {
 #define PERKS_S3D_MINB 4
 #endif
 template <bool TMA> constexpr bool host_ws() { return TMA && PERKS_S3D_HWS; }
-template <bool WS> constexpr int k3d_threads() { return WS ? 32 * PERKS_WS_NWARP + 32 : K3D_THREADS; }
+template <bool WS, int WSG = 0> constexpr int k3d_threads() { return WS ? 32 * wsg_nwarp(WSG) + 32 : K3D_THREADS; }
 
 template <typename T, int S, bool TMA, bool DIST>
 __global__ void __launch_bounds__(k3d_threads<host_ws<TMA>()>(), (TMA && !DIST) ? PERKS_S3D_MINB : 2) hostloop3d_kernel(const T *__restrict__ src,
@@ -119,12 +117,12 @@ PERKS_DEVINL int cache_slot_of(int j, int len, int nc) {
   return b != a ? a : -1;
 }
 
-template <typename T, int S, bool TMA, bool DIST, bool CACHE>
-__global__ void __launch_bounds__(k3d_threads<TMA>(), DIST ? 1 : PERKS_WS_MINB) persistent3d_kernel(
+template <typename T, int S, bool TMA, bool DIST, bool CACHE, int WSG>
+__global__ void __launch_bounds__(k3d_threads<TMA, WSG>(), DIST ? 1 : wsg_minb(WSG)) persistent3d_kernel(
     const T *__restrict__ in, T *out, T *tmp, const __grid_constant__ Maps3 maps, Dom3 d, Units3 u,
     int64_t steps, unsigned *bar, Coef<T, Shape<S>::N> c, const __grid_constant__ DistK dk,
     unsigned long long xbase, Cache3 ch) {
-  using G = typename GS<T, TMA>::G;
+  using G = typename GS<T, TMA, WSG>::G;
   static_assert(!CACHE || TMA, "the PERKS cache runs on the warp-specialised TMA pipeline");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Ring<T, G, TMA> ring;
@@ -306,15 +304,32 @@ cudaError_t launch_dist_prologue(const Problem &p, const void *in, const DistRun
 
 // ------------------------------------------------------------------ host side
 namespace {
-template <typename T> void *kptr3d(int shape, bool persistent) {  // multi-GPU slab kernels (TMA)
-  if (shape == SHAPE_3D7)
-    return persistent ? (void *)persistent3d_kernel<T, SHAPE_3D7, true, true, false> : (void *)hostloop3d_kernel<T, SHAPE_3D7, true, true>;
-  return persistent ? (void *)persistent3d_kernel<T, SHAPE_3D27, true, true, false> : (void *)hostloop3d_kernel<T, SHAPE_3D27, true, true>;
+// persistent kernel pointer for (shape, TMA, DIST, CACHE, WSG)
+template <typename T, int S, bool DIST, bool CACHE> void *pk_w(int wsg) {
+  return wsg == 1 ? (void *)persistent3d_kernel<T, S, true, DIST, CACHE, 1>
+                  : (void *)persistent3d_kernel<T, S, true, DIST, CACHE, 0>;
+}
+template <typename T, int S> void *pk_s(bool tma, bool dist, bool cache, int wsg) {
+  if (!tma) return (void *)persistent3d_kernel<T, S, false, false, false, 0>;
+  if (dist) return cache ? pk_w<T, S, true, true>(wsg) : pk_w<T, S, true, false>(wsg);
+  return cache ? pk_w<T, S, false, true>(wsg) : pk_w<T, S, false, false>(wsg);
+}
+template <typename T> void *pk(int shape, bool tma, bool dist, bool cache, int wsg) {
+  return shape == SHAPE_3D7 ? pk_s<T, SHAPE_3D7>(tma, dist, cache, wsg) : pk_s<T, SHAPE_3D27>(tma, dist, cache, wsg);
+}
+void *persist_ptr(const Problem &p, bool tma, bool cache, int wsg) {
+  const bool dist = p.nranks > 1;
+  return p.dtype == PERKS_F32 ? pk<float>(p.shape, tma, dist, cache, wsg) : pk<double>(p.shape, tma, dist, cache, wsg);
+}
+template <typename T> void *kptr3d(int shape, bool persistent) {  // multi-GPU host-loop kernels (TMA)
+  (void)persistent;
+  return shape == SHAPE_3D7 ? (void *)hostloop3d_kernel<T, SHAPE_3D7, true, true>
+                            : (void *)hostloop3d_kernel<T, SHAPE_3D27, true, true>;
 }
 template <typename T> void *kptr3(int shape, bool persistent, bool tma) {
 #define K3(S)                                                                                   \
   if (shape == S) {                                                                             \
-    if (persistent) return tma ? (void *)persistent3d_kernel<T, S, true, false, false> : (void *)persistent3d_kernel<T, S, false, false, false>; \
+    (void)persistent; \
     return tma ? (void *)hostloop3d_kernel<T, S, true, false> : (void *)hostloop3d_kernel<T, S, false, false>; \
   }
   K3(SHAPE_3D7)
@@ -322,30 +337,29 @@ template <typename T> void *kptr3(int shape, bool persistent, bool tma) {
 #undef K3
   return nullptr;
 }
+// host-loop kernel pointer
 void *pick3(const Problem &p, bool persistent) {
   const bool tma = use_tma3(p);
   if (p.nranks > 1) return p.dtype == PERKS_F32 ? kptr3d<float>(p.shape, persistent) : kptr3d<double>(p.shape, persistent);
   return p.dtype == PERKS_F32 ? kptr3<float>(p.shape, persistent, tma) : kptr3<double>(p.shape, persistent, tma);
 }
-template <typename T, bool WS> size_t smem3_t() {
-  using G = typename GS<T, WS>::G;
-  return (size_t)G::NS * G::SLOT_BYTES + 2 * (size_t)G::NS * sizeof(uint64_t);
-}
-template <typename T> size_t smem3(bool ws) { return ws ? smem3_t<T, true>() : smem3_t<T, false>(); }
-template <typename T, bool WS> void geo3_t(int &tx, int &ty, int &nt, size_t &slot) {
-  using G = typename GS<T, WS>::G;
+template <typename T, bool WS, int WSG> void geo3_t(int &tx, int &ty, int &nt, size_t &slot, size_t &ring,
+                                                  int &P, int &ROWS) {
+  using G = typename GS<T, WS, WSG>::G;
   tx = G::TX; ty = G::TY; nt = G::NT + (WS ? 32 : 0); slot = G::SLOT_BYTES;
+  ring = (size_t)G::NS * G::SLOT_BYTES + 2 * (size_t)G::NS * sizeof(uint64_t);
+  P = G::P; ROWS = G::ROWS;
 }
-template <typename T> void geo3(bool ws, int &tx, int &ty, int &nt, size_t &slot) {
-  if (ws) geo3_t<T, true>(tx, ty, nt, slot); else geo3_t<T, false>(tx, ty, nt, slot);
+struct Geo3Info { int TX, TY, NT, P, ROWS; size_t slot, ring; };
+template <typename T> Geo3Info geo3(bool ws, int wsg) {
+  Geo3Info g;
+  if (!ws) geo3_t<T, false, 0>(g.TX, g.TY, g.NT, g.slot, g.ring, g.P, g.ROWS);
+  else if (wsg == 1) geo3_t<T, true, 1>(g.TX, g.TY, g.NT, g.slot, g.ring, g.P, g.ROWS);
+  else geo3_t<T, true, 0>(g.TX, g.TY, g.NT, g.slot, g.ring, g.P, g.ROWS);
+  return g;
 }
 }  // namespace
 
-template <typename T> void *kptr_perks(int shape, bool dist) {
-  if (shape == SHAPE_3D7)
-    return dist ? (void *)persistent3d_kernel<T, SHAPE_3D7, true, true, true> : (void *)persistent3d_kernel<T, SHAPE_3D7, true, false, true>;
-  return dist ? (void *)persistent3d_kernel<T, SHAPE_3D27, true, true, true> : (void *)persistent3d_kernel<T, SHAPE_3D27, true, false, true>;
-}
 
 // Plan (a) host loop, (b) persistent or (c) PERKS for a 3D problem.
 Plan plan_stream3d(const Problem &p, perks_variant v) {
@@ -360,13 +374,16 @@ Plan plan_stream3d(const Problem &p, perks_variant v) {
   const bool cache = v == PERKS_PERKS;
   if (cache && !tma) { pl.why = "perks3d: needs TMA (nx*S % 16 == 0)"; return pl; }
   const bool persistent = v != PERKS_HOSTLOOP;
-  void *k = cache ? (p.dtype == PERKS_F32 ? kptr_perks<float>(p.shape, p.nranks > 1) : kptr_perks<double>(p.shape, p.nranks > 1))
-                  : pick3(p, persistent);
-  const bool ws = tma && (persistent || PERKS_S3D_HWS);  // warp-specialised pipeline
-  const size_t ring = p.dtype == PERKS_F32 ? smem3<float>(ws) : smem3<double>(ws);
-  int TX, TY, NT;
-  size_t slot;
-  if (p.dtype == PERKS_F32) geo3<float>(ws, TX, TY, NT, slot); else geo3<double>(ws, TX, TY, NT, slot);
+  const bool ws = tma && persistent;  // warp-specialised pipeline (persistent kernels)
+  // WS geometry: 4 warps x 3 CTAs/SM once one buffer is >= 16 L2 sizes (more plane streams in
+  // flight for DRAM-latency-bound streaming), else 8 warps x 2 CTAs/SM
+  int wsg = ((double)p.cells() * p.elem() >= 16.0 * (double)p.l2_bytes) ? 1 : 0;
+  if (env_int("PERKS_WSG", -1) >= 0) wsg = env_int("PERKS_WSG", 0) ? 1 : 0;
+  if (!ws) wsg = 0;
+  void *k = persistent ? persist_ptr(p, tma, cache, wsg) : pick3(p, false);
+  const Geo3Info gi = p.dtype == PERKS_F32 ? geo3<float>(ws, wsg) : geo3<double>(ws, wsg);
+  const size_t ring = gi.ring, slot = gi.slot;
+  const int TX = gi.TX, TY = gi.TY, NT = gi.NT;
   const int tx = (int)((p.nx + TX - 1) / TX), ty = (int)((p.ny + TY - 1) / TY);
   const int tiles = tx * ty;
   cudaFuncAttributes fa;
@@ -383,7 +400,7 @@ Plan plan_stream3d(const Problem &p, perks_variant v) {
     // PERKS: the shared memory the ring leaves at `cps` CTAs per SM caches planes (
     // minimal occupancy that keeps the HBM stream saturated: 2 CTAs/SM measured best)
     const int force_cps = env_int("PERKS_P3D_CPS", 0);
-    for (int cps = force_cps > 0 ? force_cps : PERKS_WS_MINB; cps >= 1; cps--) {
+    for (int cps = force_cps > 0 ? force_cps : wsg_minb(wsg); cps >= 1; cps--) {
       const size_t budget = std::min<size_t>((size_t)p.max_smem_optin, (size_t)p.smem_per_sm / cps - 1024);
       const size_t fixed = ring + 128 + align256((size_t)p.nz * sizeof(short));
       nc = budget > fixed ? (int)((budget - fixed) / slot) : 0;
@@ -430,6 +447,7 @@ Plan plan_stream3d(const Problem &p, perks_variant v) {
   pl.grid = persistent ? (int)std::min<int64_t>(pl.units, resident) : (int)pl.units;
   pl.cfg = tma ? 1 : 0;
   pl.family = cache ? 2 : 0;  // (2: PERKS 3D, supports multi-GPU slabs)
+  pl.wsg = wsg;
   pl.nc = cache ? std::min(nc, std::max(0, zc - 2)) : 0;
   const double S = (double)p.elem();
   // cached cells: every CTA's first unit caches nc planes of its tile (last z-chunk may be shorter)
@@ -480,6 +498,7 @@ struct Launch3 {
   bool cache = false;
   Cache3 ch{0};
   int block = 0;
+  int wsg = 0;
 
   cudaError_t setup(const Problem &p, const Plan &pl, const T *in_, T *out_, T *tmp_, unsigned *bar_,
                     const DistRun *dr) {
@@ -501,9 +520,10 @@ struct Launch3 {
     ch.nc = pl.nc;
     if (dist && !tma) return cudaErrorNotSupported;
     std::memset(&maps, 0, sizeof(maps));
-    const bool ws = pl.variant != PERKS_HOSTLOOP || PERKS_S3D_HWS;
-    const int P = ws ? GS<T, true>::G::P : GS<T, false>::G::P;
-    const int ROWS = ws ? GS<T, true>::G::ROWS : GS<T, false>::G::ROWS;
+    const bool ws = pl.variant != PERKS_HOSTLOOP && pl.cfg == 1;
+    wsg = pl.wsg;
+    const Geo3Info gi = geo3<T>(ws, wsg);
+    const int P = gi.P, ROWS = gi.ROWS;
     if (tma && !make_maps3(p, P, ROWS, in, out, tmp, &maps, dr ? dr->ghost : nullptr))
       return cudaErrorInvalidValue;
     return cudaSuccess;
@@ -526,9 +546,7 @@ struct Launch3 {
   }
   // persistent (b): one launch; cooperative on a single GPU (co-residency guaranteed by the driver)
   cudaError_t persistent(int64_t steps, cudaStream_t s, bool cooperative) {
-    void *k = cache ? (dist ? (void *)persistent3d_kernel<T, S, true, true, true> : (void *)persistent3d_kernel<T, S, true, false, true>)
-            : dist ? (void *)persistent3d_kernel<T, S, true, true, false>
-                   : tma ? (void *)persistent3d_kernel<T, S, true, false, false> : (void *)persistent3d_kernel<T, S, false, false, false>;
+    void *k = pk_s<T, S>(tma, dist, cache, wsg);
     Units3 uu = u;
     uu.rev = zigzag;
     cudaError_t e = cudaMemsetAsync(bar, 0, 256, s);

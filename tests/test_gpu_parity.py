@@ -207,3 +207,22 @@ def test_perks3d_cache_and_zigzag(monkeypatch, nsm, zigzag, name, dtype):
     for T in (5, 6):
         ref = oracle.run(u0, offs, w, T, nthreads=4)
         _check(_run_gpu(u0, name, w, T, "perks"), ref, u0, dtype)
+
+
+@pytest.mark.parametrize("shape,name", [((1000, 1500), "2d9pt"), ((517, 3072), "2d5pt"),
+                                        ((449, 2049), "2d9pt")])
+def test_strip_kernel(monkeypatch, shape, name):
+    """Wide fp32 2D domains as full-width strips (opt-in, PERKS_STRIP=1: edge rows first, LL-tag
+    exchange with the strips above/below only); bit-exact vs the oracle, ragged last strip."""
+    _need_gpu()
+    monkeypatch.setenv("PERKS_STRIP", "1")
+    from paper_2204_02064_b200 import Stencil
+    offs, w = si.preset(name)
+    st = Stencil(shape, offs, w, dtype=np.float32)
+    q = st.query("perks")
+    st.close()
+    assert q["kernel"].startswith("perks2d_strip"), q
+    u0 = si.field(shape, dtype=np.float32, seed=707)
+    for T in (1, 2, 7, 40):
+        ref = oracle.run(u0, offs, w, T, nthreads=8)
+        _check(_run_gpu(u0, name, w, T, "perks"), ref, u0, np.float32)
