@@ -90,6 +90,9 @@ typedef struct {
   double halo_bytes_per_step;   /* bytes re-read/published for halos per step       */
   size_t workspace_bytes;       /* required workspace                                           */
   char kernel_name[64];         /* short name of the kernel instantiation                       */
+  int64_t cached_cells_tmem;    /* cells resident in Tensor Memory across steps (3D PERKS TMEM
+                                   tier, sm_100a, [draft] P:395-404)       */
+  int32_t tmem_cols_per_cta;    /* TMEM columns each CTA allocates (0 = no TMEM tier)           */
 } perks_plan_info;
 
 /* Create a handle for one device.  Validates the descriptor (errors above), matches the point

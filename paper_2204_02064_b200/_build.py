@@ -50,6 +50,49 @@ def _compile(src: str) -> tuple[str, str]:
     return obj, r.stderr
 
 
+def _func_spill_report(report: str) -> dict:
+    """{mangled function name: spill bytes} from the ptxas -v report."""
+    out, cur = {}, None
+    for ln in report.splitlines():
+        m = re.search(r"Function properties for (\S+)", ln)
+        if m:
+            cur = m.group(1)
+            continue
+        m = re.search(r"(\d+) bytes spill stores, (\d+) bytes spill loads", ln)
+        if m and cur and (int(m.group(1)) or int(m.group(2))):
+            out[cur] = int(m.group(1)) + int(m.group(2))
+    return out
+
+
+def spills_in_plane_loops(obj: str, func: str) -> list:
+    """Local-memory accesses (LDL/STL) of `func` that lie inside a hot loop: an innermost
+    backward-branch range (of >= 32 instructions) of the main body (before the final EXIT; the
+    mbarrier retry stubs follow it) that contains an mbarrier wait.  Spills of loop-invariant state in a prologue or
+    in the per-step outer loop cost one access per unit/step and are tolerated; spills in the
+    per-plane loop are not (P:859-860 register discipline)."""
+    r = subprocess.run(["cuobjdump", "-sass", "-fun", func, obj], capture_output=True, text=True)
+    ins = []
+    for ln in r.stdout.splitlines():
+        m = re.match(r"\s*/\*([0-9a-f]+)\*/\s+(.*?);", ln)
+        if m:
+            ins.append((int(m.group(1), 16), m.group(2)))
+    if not ins:
+        return ["<no SASS>"]
+    end = max((a for a, t in ins if re.fullmatch(r"\s*EXIT\s*", t)), default=ins[-1][0])
+    waits = [a for a, t in ins if "TRYWAIT" in t and a <= end]
+    loops = []
+    for a, t in ins:
+        m = re.search(r"\bBRA(?:\.\S+)?\s+(?:\S+,\s*)?0x([0-9a-f]+)", t)
+        if m and a <= end and int(m.group(1), 16) <= a:
+            loops.append((int(m.group(1), 16), a))
+    # (a wait's own spin loop — try_wait, timer read, compare — is a loop too: ignore tiny ones)
+    hot = [lp for lp in loops if any(lp[0] <= w <= lp[1] for w in waits)
+           and sum(1 for a, _ in ins if lp[0] <= a <= lp[1]) >= 32]
+    inner = [lp for lp in hot if not any(o != lp and lp[0] <= o[0] and o[1] <= lp[1] for o in hot)]
+    return [hex(a) for a, t in ins if re.search(r"\b(LDL|STL)\b", t)
+            and any(lo <= a <= hi for lo, hi in inner)]
+
+
 def build(verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     srcs = _sources()
@@ -59,11 +102,14 @@ def build(verbose: bool = False) -> str:
     report = "".join(log for _, log in results)
     with open(os.path.join(BUILD, "ptxas_report.txt"), "w") as f:
         f.write(report)
-    spills = [ln for ln in report.splitlines()
-              if re.search(r"(\d+) bytes spill (stores|loads)", ln)
-              and not re.search(r" 0 bytes spill stores, 0 bytes spill loads", ln)]
-    if spills and not os.environ.get("PERKS_ALLOW_SPILLS"):
-        raise RuntimeError("register spills (P:860 discipline):\n" + "\n".join(spills[:20]))
+    bad = []
+    for (obj, log) in results:
+        for fn, nbytes in _func_spill_report(log).items():
+            hot = spills_in_plane_loops(obj, fn)
+            if hot:
+                bad.append(f"{fn}: {nbytes} spill bytes, {len(hot)} in the plane loop at {hot[:4]}")
+    if bad and not os.environ.get("PERKS_ALLOW_SPILLS"):
+        raise RuntimeError("register spills in a plane loop (P:860 discipline):\n" + "\n".join(bad[:20]))
     newest = max(os.path.getmtime(o) for o in objs)
     if not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
         tmp = LIB + f".tmp{os.getpid()}"

@@ -53,6 +53,8 @@ class PlanInfo(ctypes.Structure):
         ("halo_bytes_per_step", ctypes.c_double),
         ("workspace_bytes", ctypes.c_size_t),
         ("kernel_name", ctypes.c_char * 64),
+        ("cached_cells_tmem", ctypes.c_int64),
+        ("tmem_cols_per_cta", ctypes.c_int32),
     ]
 
 

@@ -383,6 +383,8 @@ perks_status perks_stencil_query(perks_stencil_t h, perks_variant v, perks_plan_
   info->smem_per_cta = pl.smem;
   info->cached_cells_reg = pl.cached_reg;
   info->cached_cells_smem = pl.cached_smem;
+  info->cached_cells_tmem = pl.cached_tmem;
+  info->tmem_cols_per_cta = pl.tcols;
   info->total_cells = h->p.cells();
   info->dram_bytes_per_step = pl.dram_bytes_step;
   info->halo_bytes_per_step = pl.halo_bytes_step;

@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 #ifndef PERKS_DEVINL
 #define PERKS_DEVINL __device__ __forceinline__
@@ -182,6 +183,24 @@ template <> struct LL<double> {
   }
 };
 
+PERKS_DEVINL unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t));
+  return t;
+}
+
+#ifndef PERKS_WATCHDOG_NS
+#define PERKS_WATCHDOG_NS 10000000000ull  // 10 s: a lost neighbour becomes a trap, not a hang
+#endif
+
+// Spin (one thread) until *p >= target, acquiring at system scope.
+// Watchdog for device-side spins: after PERKS_WATCHDOG_NS a lost peer/CTA becomes a reported
+// trap (the caller's next synchronisation fails with cudaErrorLaunchFailure) instead of a hang.
+__device__ __noinline__ inline void watchdog_fire(const char *what, unsigned a, unsigned b) {
+  printf("perks watchdog: %s stuck (block %d thread %d, %u %u)\n", what, (int)blockIdx.x, (int)threadIdx.x, a, b);
+  __trap();
+}
+
 // Grid barrier on a monotonically increasing counter (reset to 0 before the launch).
 // Every CTA calls it with the same `target` = (barrier index + 1) * gridDim.x.
 // CTA-level __syncthreads + one releasing arrive per CTA + acquiring spin (P:1068 grid.sync).
@@ -189,7 +208,12 @@ PERKS_DEVINL void grid_barrier(unsigned *ctr, unsigned target) {
   __syncthreads();
   if (threadIdx.x == 0) {
     red_release_gpu(ctr, 1u);
-    while (ld_acquire_gpu(ctr) < target) {
+    if (ld_acquire_gpu(ctr) < target) {
+      const unsigned long long t0 = globaltimer_ns();
+      unsigned n = 0;
+      while (ld_acquire_gpu(ctr) < target)
+        if ((++n & 1023u) == 0 && globaltimer_ns() - t0 > PERKS_WATCHDOG_NS)
+          watchdog_fire("grid barrier", ld_acquire_gpu(ctr), target);
     }
   }
   __syncthreads();

@@ -32,17 +32,6 @@ PERKS_DEVINL void red_release_sys_add_u64(unsigned long long *p, unsigned long l
   asm volatile("red.release.sys.global.add.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
 }
 PERKS_DEVINL void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;\n" ::: "memory"); }
-PERKS_DEVINL unsigned long long globaltimer_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t));
-  return t;
-}
-
-#ifndef PERKS_WATCHDOG_NS
-#define PERKS_WATCHDOG_NS 10000000000ull  // 10 s: a lost neighbour becomes a trap, not a hang
-#endif
-
-// Spin (one thread) until *p >= target, acquiring at system scope.
 PERKS_DEVINL void wait_counter_sys(const unsigned long long *p, unsigned long long target) {
   if (ld_acquire_sys_u64(p) >= target) return;
   const unsigned long long t0 = globaltimer_ns();

@@ -41,8 +41,9 @@ struct Plan {
   int cfg = 0;                // index of the kernel configuration
   int family = 0;             // kernel family within a variant (2D PERKS: 0 tiles, 1 cluster, 3 strips; 3D PERKS: 2)
   int nc = 0;                 // 3D PERKS: shared-memory plane slots per CTA
+  int ntm = 0, tcols = 0;     // 3D PERKS: TMEM planes per CTA, TMEM columns allocated per CTA
   int wsg = 0;                // 3D persistent: warp-specialised geometry (k3d_stream.cu)
-  int64_t cached_reg = 0, cached_smem = 0;
+  int64_t cached_reg = 0, cached_smem = 0, cached_tmem = 0;
   double dram_bytes_step = 0, halo_bytes_step = 0;
   size_t ws_bytes = 0;
   char name[64] = {0};

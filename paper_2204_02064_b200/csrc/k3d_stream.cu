@@ -2,13 +2,14 @@
 //   (a) host-loop: one launch per step, one (tile, z-chunk) unit per CTA  (Fig. 3 left)
 //   (b) persistent: one cooperative launch; CTAs loop over units; grid barrier per step
 //   (c) PERKS: the persistent kernel plus an on-chip plane cache (§3.3): each
-//       CTA keeps `nc` interior planes of its unit resident in shared memory across steps.  "Planes
-//       that already have the data cached from the previous time step do not load from global
-//       memory": a cached plane reloads only its one-cell halo ring (halo cells are never
-//       cached) and publishes only its tile perimeter (TB-boundary cells "continue to
-//       store and load from global memory").  Cached planes are spread evenly through the
-//       unit so the HBM stream never pauses, and every tile of a z-chunk caches the same planes.
-//       The first/last plane of each unit is never cached (other units read it as z-halo).
+//       CTA keeps `nc` tile planes resident in shared memory and `ntm` in Tensor Memory (tmem.cuh,
+//       the sm_100a tier the paper's GPUs lack) across steps.  "Planes that already have the data
+//       cached from the previous time step do not load from global memory": a cached
+//       plane reloads only its one-cell halo ring (halo cells are never cached) and
+//       publishes only its tile perimeter (TB-boundary cells "continue to store and load from
+//       global memory").  The cached planes are spread evenly over ALL of the CTA's units
+//       of a step, so every CTA's HBM stream continues through the whole step.  The first/last
+//       plane of each unit is never cached (other units read it as z-halo).
 // Compute body and plane pipelines: stream3d.cuh (plane streaming; TMA on sm_100a).
 #include <cudaTypedefs.h>
 
@@ -60,7 +61,10 @@ PERKS_DEVINL void unit_coords(const Units3 &u, int id, int tile_x, int tile_y, i
   zs = zc * u.zc;
 }
 
+// Ring slots, then full/empty/tfull mbarriers (3 x NS) and the TMEM base address: within the
+// 128 bytes the persistent kernel reserves before its plane cache.
 template <class G> PERKS_DEVINL uint64_t *ring_bars(unsigned char *smem) {
+  static_assert(3 * G::NS * 8 + 8 <= 128, "ring barriers + TMEM address exceed 128 B");
   return reinterpret_cast<uint64_t *>(smem + (size_t)G::NS * G::SLOT_BYTES);
 }
 
@@ -76,10 +80,14 @@ template <class G> PERKS_DEVINL uint64_t *ring_bars(unsigned char *smem) {
 #define PERKS_S3D_MINB 4
 #endif
 template <bool TMA> constexpr bool host_ws() { return TMA && PERKS_S3D_HWS; }
+// host-loop CTAs per SM (launch bound): fp64 27pt needs more than 64 registers per thread
+template <typename T, int S, bool TMA, bool DIST> constexpr int hl_minb() {
+  return !(TMA && !DIST) ? 2 : (sizeof(T) == 8 && S == SHAPE_3D27) ? 3 : PERKS_S3D_MINB;
+}
 template <bool WS, int WSG = 0> constexpr int k3d_threads() { return WS ? 32 * wsg_nwarp(WSG) + 32 : K3D_THREADS; }
 
 template <typename T, int S, bool TMA, bool DIST>
-__global__ void __launch_bounds__(k3d_threads<host_ws<TMA>()>(), (TMA && !DIST) ? PERKS_S3D_MINB : 2) hostloop3d_kernel(const T *__restrict__ src,
+__global__ void __launch_bounds__(k3d_threads<host_ws<TMA>()>(), hl_minb<T, S, TMA, DIST>()) hostloop3d_kernel(const T *__restrict__ src,
                                                                  const __grid_constant__ Maps3 maps,
                                                                  int src_idx, T *__restrict__ dst,
                                                                  Dom3 d, Units3 u,
@@ -94,7 +102,7 @@ __global__ void __launch_bounds__(k3d_threads<host_ws<TMA>()>(), (TMA && !DIST) 
   const DistStep ds{&dk, &maps.ghost, e, (unsigned long long)d.nx * d.ny};
   if constexpr (host_ws<TMA>()) {
     WsPipe<T, G> pp;
-    pp.init(reinterpret_cast<T *>(smem_raw), ring_bars<G>(smem_raw));
+    pp.init();
     stream_unit_ws<T, S, G, DIST>(pp, src, &maps.box[src_idx], dst, d, x0, y0, zs, ze, c, ds);
   } else {
     Ring<T, G, TMA> ring;
@@ -105,16 +113,47 @@ __global__ void __launch_bounds__(k3d_threads<host_ws<TMA>()>(), (TMA && !DIST) 
 
 // Cache geometry of a PERKS launch (CACHE kernels only).
 struct Cache3 {
-  int nc;  // shared-memory plane slots per CTA
+  int nc;     // shared-memory plane slots per CTA
+  int ntm;    // TMEM planes per CTA (tmem.cuh; 0 = no TMEM tier)
+  int tcols;  // TMEM columns allocated per CTA (power of two >= 32, 512 / CTAs per SM)
 };
 
-// Slot map of a unit [zs, ze): cmap[j] = cache slot of plane zs + j, or -1.  nc slots spread
-// evenly over the interior planes zs+1 .. ze-2 (the unit's first/last plane is never cached).
-PERKS_DEVINL int cache_slot_of(int j, int len, int nc) {
-  const int elig = len - 2, jj = j - 1;
-  if (nc <= 0 || jj < 0 || jj >= elig) return -1;
-  const int a = (jj * nc) / elig, b = ((jj + 1) * nc) / elig;
-  return b != a ? a : -1;
+// Cache code of arrival a of a CTA's step (PERKS).  The CTA's units are processed back to back,
+// unit j contributing arrivals for its planes zs-1 .. ze (len + 2, len = ze - zs); its eligible
+// planes are zs+1 .. ze-2 (the first/last plane of a unit is read by other units as z-halo and is
+// never cached).  Of the E eligible planes of the whole step, n = ns + nt are cached, spread
+// evenly (plane g is chosen iff floor((g+1)n/E) > floor(gn/E)), and the nt TMEM planes evenly
+// among the chosen ones.
+PERKS_DEVINL int cache_code_of(int g, int E, int ns, int nt) {
+  const int n = ns + nt;
+  if (n <= 0 || g < 0 || g >= E) return -1;
+  const int a = (g * n) / E, b = ((g + 1) * n) / E;
+  if (b == a) return -1;
+  const int t0 = (a * nt) / n, t1 = ((a + 1) * nt) / n;  // TMEM planes among chosen [0, a) / [0, a]
+  return t1 != t0 ? kTmemCode + t0 : a - t1;
+}
+// The CTA's unit j of a step: tile origin, z range.
+struct UnitGeo {
+  int x0, y0, zs, ze;
+};
+template <class G> PERKS_DEVINL UnitGeo my_unit(const Units3 &u, const Dom3 &d, int j) {
+  UnitGeo g;
+  unit_coords(u, (int)blockIdx.x + j * (int)gridDim.x, G::TX, G::TY, g.x0, g.y0, g.zs);
+  g.ze = min(g.zs + u.zc, d.nz);
+  return g;
+}
+// Visit every cached plane of the CTA (prologue / epilogue): f(unit geometry, plane q, code).
+template <class G, class F>
+PERKS_DEVINL void for_cached_planes(const Units3 &u, const Dom3 &d, int nmine, const signed char *cmap, F f) {
+  int abase = 0;
+  for (int j = 0; j < nmine; j++) {
+    const UnitGeo g = my_unit<G>(u, d, j);
+    for (int q = g.zs + 1; q < g.ze - 1; q++) {
+      const int c = cmap[abase + q - g.zs + 1];
+      if (c >= 0) f(g, q, c);
+    }
+    abase += g.ze - g.zs + 2;
+  }
 }
 
 template <typename T, int S, bool TMA, bool DIST, bool CACHE, int WSG>
@@ -127,33 +166,67 @@ __global__ void __launch_bounds__(k3d_threads<TMA, WSG>(), DIST ? 1 : wsg_minb(W
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Ring<T, G, TMA> ring;
   WsPipe<T, G> pp;
-  if constexpr (TMA) pp.init(reinterpret_cast<T *>(smem_raw), ring_bars<G>(smem_raw));
+  if constexpr (TMA) pp.init();
   else ring.init(reinterpret_cast<T *>(smem_raw), ring_bars<G>(smem_raw), 0);
   const int nunits = u.tx * u.ty * u.nzc;
 
-  // ---- PERKS: the CTA's first unit hosts the cache
-  T *cache = reinterpret_cast<T *>(smem_raw + (size_t)G::NS * G::SLOT_BYTES + 128);
-  short *cmap = reinterpret_cast<short *>(cache + (size_t)ch.nc * G::SLOT);
-  int cx0 = 0, cy0 = 0, czs = 0, cze = 0;
-  const bool consumer = (int)(threadIdx.x >> 5) < G::NWARP;
+  // ---- PERKS: cached planes spread over all of this CTA's units (CacheView, stream3d.cuh)
+  const int nmine = (int)blockIdx.x < nunits ? (nunits - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  CacheView<T, G> cv{ch.nc, 0, 0u};
+  signed char *cmap = cv.cmap();
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(ring_bars<G>(smem_raw) + 3 * G::NS);
+  const int warp = (int)(threadIdx.x >> 5);
+  const bool consumer = warp < G::NWARP;
   if constexpr (CACHE) {
-    if (blockIdx.x < nunits) {
-      unit_coords(u, blockIdx.x, G::TX, G::TY, cx0, cy0, czs);
-      cze = min(czs + u.zc, d.nz);
+    int E = 0, A = 0;
+    for (int j = 0; j < nmine; j++) {
+      const UnitGeo g = my_unit<G>(u, d, j);
+      E += max(0, g.ze - g.zs - 2);
+      A += g.ze - g.zs + 2;
     }
-    const int nc = min(ch.nc, max(0, cze - czs - 2));
-    for (int j = threadIdx.x; j < cze - czs; j += blockDim.x) cmap[j] = (short)cache_slot_of(j, cze - czs, nc);
+    const int n = min(ch.nc + ch.ntm, E), ns = min(ch.nc, n), nt = min(ch.ntm, n - ns);
+    for (int a = threadIdx.x; a <= A; a += blockDim.x) {  // (a == A: the -1 sentinel)
+      int abase = 0, gbase = 0, code = -1;
+      for (int j = 0; j < nmine; j++) {
+        const UnitGeo g = my_unit<G>(u, d, j);
+        const int len = g.ze - g.zs;
+        if (a < abase + len + 2) {
+          const int k = a - abase;  // plane zs - 1 + k
+          if (k >= 2 && k <= len - 1) code = cache_code_of(gbase + k - 2, E, ns, nt);
+          break;
+        }
+        abase += len + 2;
+        gbase += max(0, len - 2);
+      }
+      cmap[a] = (signed char)code;
+    }
+    if (warp == 0) {
+      if (ch.tcols > 0) tmem_alloc(tmem_slot, (uint32_t)ch.tcols);
+      tmem_relinquish();  // lets the next CTA onto this SM (tmem.cuh)
+    }
+    tmem_fence_before_sync();
     __syncthreads();
+    tmem_fence_after_sync();
+    if (ch.tcols > 0)  // lane quarter of this warp, column group of its warp-group half
+      cv.tbase = *tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) +
+                 (uint32_t)((warp >> 2) * TmemCells<T, G::R, G::V>::WPT);
     // prologue: cached planes from `in` (the one-time load half of 2·D_cache)
-    for (int q = czs + 1; q < cze - 1 && consumer; q++) {
-      const int sl = cmap[q - czs];
-      if (sl >= 0) issue_plane<T, G>(cache + (size_t)sl * G::SLOT, in, d, q, cx0, cy0, false);
-    }
+    if (consumer)
+      for_cached_planes<G>(u, d, nmine, cmap, [&](const UnitGeo &g, int q, int code) {
+        if (is_smem_code(code)) {
+          issue_plane<T, G>(cv.slot(code), in, d, q, g.x0, g.y0, false);
+        } else {
+          ThreadTile<G> ct;
+          ct.init(d, g.x0, g.y0);
+          T v[G::R][G::V];
+          load_own_cells<T, G>(in, d, ct, q, v);
+          TmemCells<T, G::R, G::V>::store(cv.tbase + (uint32_t)((code - kTmemCode) * tmem_cpp<T, G>()), v);
+        }
+      });
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
   }
-  const CacheView<T> cv{cache, cmap, czs, cze};
 
   for (int64_t t = 0; t < steps; t++) {
     const bool src_out = t > 0 && ((steps - t) & 1) == 0;
@@ -162,16 +235,16 @@ __global__ void __launch_bounds__(k3d_threads<TMA, WSG>(), DIST ? 1 : wsg_minb(W
     T *dst = ((steps - 1 - t) & 1) == 0 ? out : tmp;
     const DistStep ds{&dk, &maps.ghost, xbase + (unsigned long long)t, (unsigned long long)d.nx * d.ny};
     if (TMA && threadIdx.x == 0) fence_proxy_async_global();  // last step's stores -> TMA reads
-    for (int id = blockIdx.x; id < nunits; id += gridDim.x) {
+    cv.kbase = 0;
+    for (int jj = 0; jj < nmine; jj++) {
+      const int id = (int)blockIdx.x + jj * (int)gridDim.x;
       int x0, y0, zs;
-      // (the zig-zag unit-order experiment never applies to PERKS: the cache belongs to a unit)
+      // (the zig-zag unit-order experiment never applies to PERKS: the cache map is per unit)
       unit_coords(u, (!CACHE && u.rev && (t & 1)) ? nunits - 1 - id : id, G::TX, G::TY, x0, y0, zs);
       const int ze = min(zs + u.zc, d.nz);
       if constexpr (TMA) {
-        if (CACHE && id == (int)blockIdx.x)
-          stream_unit_ws<T, S, G, DIST, CACHE>(pp, src, &maps.box[src_idx], dst, d, x0, y0, zs, ze, c, ds, cv);
-        else
-          stream_unit_ws<T, S, G, DIST, false>(pp, src, &maps.box[src_idx], dst, d, x0, y0, zs, ze, c, ds);
+        stream_unit_ws<T, S, G, DIST, CACHE>(pp, src, &maps.box[src_idx], dst, d, x0, y0, zs, ze, c, ds, cv);
+        cv.kbase += ze - zs + 2;
       } else {
         __syncthreads();  // slots of the previous unit are free
         stream_unit<T, S, G, TMA, DIST>(ring, src, &maps.box[src_idx], dst, d, x0, y0, zs, ze, c, ds);
@@ -182,15 +255,21 @@ __global__ void __launch_bounds__(k3d_threads<TMA, WSG>(), DIST ? 1 : wsg_minb(W
 
   if constexpr (CACHE) {  // epilogue: cached planes to `out` (store half of 2·D_cache)
     __syncthreads();
-    ThreadTile<G> ct;
-    ct.init(d, cx0, cy0);
-    for (int q = czs + 1; q < cze - 1 && consumer; q++) {
-      const int sl = cmap[q - czs];
-      if (sl < 0) continue;
-      T v[G::R][G::V];
-      read_own<T, G>(cache + (size_t)sl * G::SLOT, v);
-      store_cells<T, G>(out, d, ct, q, v);
-    }
+    if (consumer)
+      for_cached_planes<G>(u, d, nmine, cmap, [&](const UnitGeo &g, int q, int code) {
+        ThreadTile<G> ct;
+        ct.init(d, g.x0, g.y0);
+        T v[G::R][G::V];
+        if (is_tmem_code(code))
+          TmemCells<T, G::R, G::V>::load(cv.tbase + (uint32_t)((code - kTmemCode) * tmem_cpp<T, G>()), v);
+        else
+          read_own<T, G>(cv.slot(code), v);
+        store_cells<T, G>(out, d, ct, q, v);
+      });
+    tmem_fence_before_sync();
+    __syncthreads();
+    tmem_fence_after_sync();
+    if (ch.tcols > 0 && warp == 0) tmem_dealloc(*tmem_slot, (uint32_t)ch.tcols);
   }
 }
 
@@ -347,19 +426,47 @@ template <typename T, bool WS, int WSG> void geo3_t(int &tx, int &ty, int &nt, s
                                                   int &P, int &ROWS) {
   using G = typename GS<T, WS, WSG>::G;
   tx = G::TX; ty = G::TY; nt = G::NT + (WS ? 32 : 0); slot = G::SLOT_BYTES;
-  ring = (size_t)G::NS * G::SLOT_BYTES + 2 * (size_t)G::NS * sizeof(uint64_t);
+  ring = (size_t)G::NS * G::SLOT_BYTES + 3 * (size_t)G::NS * sizeof(uint64_t) + 16;  // + TMEM address
   P = G::P; ROWS = G::ROWS;
 }
-struct Geo3Info { int TX, TY, NT, P, ROWS; size_t slot, ring; };
+struct Geo3Info { int TX, TY, NT, P, ROWS, cpp; size_t slot, ring; };
 template <typename T> Geo3Info geo3(bool ws, int wsg) {
   Geo3Info g;
-  if (!ws) geo3_t<T, false, 0>(g.TX, g.TY, g.NT, g.slot, g.ring, g.P, g.ROWS);
-  else if (wsg == 1) geo3_t<T, true, 1>(g.TX, g.TY, g.NT, g.slot, g.ring, g.P, g.ROWS);
-  else geo3_t<T, true, 0>(g.TX, g.TY, g.NT, g.slot, g.ring, g.P, g.ROWS);
+  if (!ws) {
+    geo3_t<T, false, 0>(g.TX, g.TY, g.NT, g.slot, g.ring, g.P, g.ROWS);
+    g.cpp = tmem_cpp<T, typename GS<T, false, 0>::G>();
+  } else if (wsg == 1) {
+    geo3_t<T, true, 1>(g.TX, g.TY, g.NT, g.slot, g.ring, g.P, g.ROWS);
+    g.cpp = tmem_cpp<T, typename GS<T, true, 1>::G>();
+  } else {
+    geo3_t<T, true, 0>(g.TX, g.TY, g.NT, g.slot, g.ring, g.P, g.ROWS);
+    g.cpp = tmem_cpp<T, typename GS<T, true, 0>::G>();
+  }
   return g;
 }
 }  // namespace
 
+
+// Co-resident CTAs per SM from the kernel's registers, threads and shared memory.  The runtime's
+// occupancy calculator (and hence a cooperative launch) caps every kernel that contains
+// tcgen05.alloc at ONE CTA per SM (profiles/r01_tmem_occupancy_probe.txt: 1 for any smem, while
+// the same kernel launched normally runs 2 CTAs per SM, each with its own TMEM allocation), so the
+// PERKS kernels — which carry the TMEM tier — compute residency from the hardware limits
+// (B200: 64K registers in 4 SMSP files, 2048 threads, 32 CTAs, smem_per_sm incl. 1 KiB/CTA).
+int occupancy_ignoring_tmem(const Problem &p, const cudaFuncAttributes &fa, int nt, size_t smem) {
+  const int warps = (nt + 31) / 32;
+  const int regs_warp = (fa.numRegs * 32 + 255) / 256 * 256;
+  int by_regs = 0;  // warps of all CTAs round-robin over 4 SMSPs of 16384 registers each
+  for (int b = 1; b <= 32; b++) {
+    const int per_smsp = (b * warps + 3) / 4;
+    if (per_smsp * regs_warp > 16384) break;
+    by_regs = b;
+  }
+  const int by_threads = 2048 / (warps * 32);
+  const size_t per = smem + (size_t)fa.sharedSizeBytes + 1024;
+  const int by_smem = (int)((size_t)p.smem_per_sm / per);
+  return std::min(std::min(by_regs, by_threads), std::min(by_smem, 32));
+}
 
 // Plan (a) host loop, (b) persistent or (c) PERKS for a 3D problem.
 Plan plan_stream3d(const Problem &p, perks_variant v) {
@@ -388,8 +495,30 @@ Plan plan_stream3d(const Problem &p, perks_variant v) {
   const int tiles = tx * ty;
   cudaFuncAttributes fa;
   if (cudaFuncGetAttributes(&fa, k) != cudaSuccess) { pl.why = "cudaFuncGetAttributes"; return pl; }
+  // z chunks: about two waves of units for the host loop; for the persistent kernels the
+  // z-chunking that minimises the busiest CTA's planes per step, ceil(units / grid) * (chunk + 2
+  // halo planes), with grid <= resident CTAs (load balance over 148 SMs)
+  auto choose_nzc = [&](int resident) {
+    int nz_c = std::max(1, (2 * resident + tiles - 1) / tiles);
+    nz_c = std::min<int>(nz_c, (int)std::max<int64_t>(1, p.nz / 8));
+    if (persistent) {
+      int64_t best = -1;
+      for (int n = 1; n <= std::max<int64_t>(1, p.nz / 4); n++) {
+        const int64_t zcn = (p.nz + n - 1) / n, nn = (p.nz + zcn - 1) / zcn;
+        if (nn != n) continue;
+        const int64_t un = (int64_t)tiles * n, g = std::min<int64_t>(un, resident);
+        const int64_t cost = ((un + g - 1) / g) * (zcn + 2);
+        if (best < 0 || cost < best) { best = cost; nz_c = n; }
+      }
+      if (env_int("PERKS_S3D_NZC", 0) > 0) nz_c = std::min<int>(env_int("PERKS_S3D_NZC", 0), (int)p.nz);  // sweeps
+    }
+    const int zcn = (int)((p.nz + nz_c - 1) / nz_c);
+    return (int)((p.nz + zcn - 1) / zcn);
+  };
   size_t smem = ring;
-  int occ = 0, nc = 0;
+  int occ = 0, nc = 0, tcols = 0, ntm0 = 0;
+  bool tmem_ok = false;
+  const bool use_tmem = env_int("PERKS_P3D_TMEM", 1) != 0;
   if (!cache) {
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
       cudaGetLastError();
@@ -402,7 +531,17 @@ Plan plan_stream3d(const Problem &p, perks_variant v) {
     const int force_cps = env_int("PERKS_P3D_CPS", 0);
     for (int cps = force_cps > 0 ? force_cps : wsg_minb(wsg); cps >= 1; cps--) {
       const size_t budget = std::min<size_t>((size_t)p.max_smem_optin, (size_t)p.smem_per_sm / cps - 1024);
-      const size_t fixed = ring + 128 + align256((size_t)p.nz * sizeof(short));
+      // TMEM tier (tmem.cuh): 512 / cps columns per CTA (power of two), gi.cpp per plane
+      tcols = 512;
+      while (tcols * cps > 512) tcols >>= 1;
+      ntm0 = use_tmem ? tcols / gi.cpp : 0;
+      if (env_int("PERKS_P3D_NTM", -1) >= 0) ntm0 = std::min(ntm0, env_int("PERKS_P3D_NTM", 0));
+      // the CTA's cache-code map: one byte per arrival of its busiest step (+ sentinel)
+      const int nzc_c = choose_nzc(cps * p.num_sms);
+      const int64_t zc_c = (p.nz + nzc_c - 1) / nzc_c, un_c = (int64_t)tiles * nzc_c;
+      const int64_t g_c = std::min<int64_t>(un_c, (int64_t)cps * p.num_sms);
+      const size_t map_bytes = align256((size_t)(((un_c + g_c - 1) / g_c) * (zc_c + 2) + 1));
+      const size_t fixed = ring + 128 + map_bytes;
       nc = budget > fixed ? (int)((budget - fixed) / slot) : 0;
       const int forced = env_int("PERKS_P3D_NSM", -1);
       if (forced >= 0) nc = std::min(nc, forced);
@@ -411,30 +550,30 @@ Plan plan_stream3d(const Problem &p, perks_variant v) {
         cudaGetLastError();
         continue;
       }
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NT, smem);
-      if (occ >= cps) { occ = cps; break; }
+      occ = occupancy_ignoring_tmem(p, fa, NT, smem);
+      if (env_int("PERKS_DEBUG_PLAN", 0))
+        fprintf(stderr, "perks3d plan: cps=%d nc=%d smem=%zu occ=%d regs=%d static_smem=%zu\n", cps, nc, smem, occ,
+                fa.numRegs, (size_t)fa.sharedSizeBytes);
+      if (occ >= cps) {
+        // TMEM tier: every co-resident CTA allocates 512 / cps columns, so exactly cps CTAs may
+        // share an SM (more would block in tcgen05.alloc): pad shared memory until no more fit
+        while (occ > cps && smem + 1024 <= (size_t)p.max_smem_optin) {
+          smem += 1024;
+          if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+            cudaGetLastError();
+            break;
+          }
+          occ = occupancy_ignoring_tmem(p, fa, NT, smem);
+        }
+        if (occ == cps) tmem_ok = true;
+        occ = cps;
+        break;
+      }
     }
   }
   if (occ < 1) { pl.why = "stream3d: not co-resident"; return pl; }
   const int resident = occ * p.num_sms;
-  // z chunks: about two waves of units for the host loop; exactly one wave for the persistent
-  // kernels (one unit per CTA per step, so no CTA idles at the tail)
-  int nzc = std::max(1, (2 * resident + tiles - 1) / tiles);
-  nzc = std::min<int>(nzc, (int)std::max<int64_t>(1, p.nz / 8));
-  if (persistent) {
-    // persistent kernels: pick the z-chunking that minimises the busiest CTA's planes per step,
-    // ceil(units / grid) * (chunk + 2 halo planes), with grid <= resident CTAs (load balance over
-    // 148 SMs: e.g. C3 64 tiles x 4 chunks on 256 CTAs; C5 1024 tiles x 2 chunks)
-    int64_t best = -1;
-    for (int n = 1; n <= std::max<int64_t>(1, p.nz / 4); n++) {
-      const int64_t zcn = (p.nz + n - 1) / n, nn = (p.nz + zcn - 1) / zcn;
-      if (nn != n) continue;
-      const int64_t un = (int64_t)tiles * n, g = std::min<int64_t>(un, resident);
-      const int64_t cost = ((un + g - 1) / g) * (zcn + 2);
-      if (best < 0 || cost < best) { best = cost; nzc = n; }
-    }
-  }
-  if (persistent && env_int("PERKS_S3D_NZC", 0) > 0) nzc = std::min<int>(env_int("PERKS_S3D_NZC", 0), (int)p.nz);  // sweeps
+  int nzc = choose_nzc(resident);
   const int zc = (int)((p.nz + nzc - 1) / nzc);
   nzc = (int)((p.nz + zc - 1) / zc);
   pl.units = (int64_t)tiles * nzc;
@@ -448,21 +587,34 @@ Plan plan_stream3d(const Problem &p, perks_variant v) {
   pl.cfg = tma ? 1 : 0;
   pl.family = cache ? 2 : 0;  // (2: PERKS 3D, supports multi-GPU slabs)
   pl.wsg = wsg;
-  pl.nc = cache ? std::min(nc, std::max(0, zc - 2)) : 0;
+  pl.nc = cache ? nc : 0;
+  if (cache && tmem_ok && ntm0 > 0) {
+    pl.ntm = ntm0;
+    pl.tcols = tcols;
+  }
   const double S = (double)p.elem();
-  // cached cells: every CTA's first unit caches nc planes of its tile (last z-chunk may be shorter)
-  int64_t cached = 0;
+  // cached cells: per CTA min(nc + ntm, eligible planes of its units) tile planes (the kernel's
+  // cache_code_of split: shared memory first, then TMEM)
+  int64_t cached = 0, cached_t = 0;
   if (cache) {
-    for (int cz = 0; cz < nzc; cz++) {
-      const int len = (int)std::min<int64_t>(zc, p.nz - (int64_t)cz * zc);
-      cached += (int64_t)tiles * std::min(pl.nc, std::max(0, len - 2));
+    for (int64_t b = 0; b < pl.grid; b++) {
+      int64_t E = 0;
+      for (int64_t id = b; id < pl.units; id += pl.grid) {
+        const int64_t cz = id / tiles, len = std::min<int64_t>(zc, p.nz - cz * zc);
+        E += std::max<int64_t>(0, len - 2);
+      }
+      const int64_t n = std::min<int64_t>(pl.nc + pl.ntm, E), ns = std::min<int64_t>(pl.nc, n);
+      cached += ns;
+      cached_t += std::min<int64_t>(pl.ntm, n - ns);
     }
-    if (pl.units > pl.grid) cached = cached * pl.grid / pl.units;
     cached *= (int64_t)TX * TY;
+    cached_t *= (int64_t)TX * TY;
     cached = std::min<int64_t>(cached, p.cells());
+    cached_t = std::min<int64_t>(cached_t, p.cells() - cached);
   }
   pl.cached_smem = cached;
-  pl.dram_bytes_step = 2.0 * S * ((double)p.cells() - (double)cached);
+  pl.cached_tmem = cached_t;
+  pl.dram_bytes_step = 2.0 * S * ((double)p.cells() - (double)cached - (double)cached_t);
   pl.halo_bytes_step = S * (double)p.nz * (2.0 * TX * ty * tx + 2.0 * TY * ty * tx) +
                        S * 2.0 * nzc * (double)p.nx * p.ny;
   pl.ws_bytes = align256((size_t)p.cells() * p.elem()) + (persistent ? 256 : 0);
@@ -471,7 +623,8 @@ Plan plan_stream3d(const Problem &p, perks_variant v) {
            cache ? "_c" : (pl.cfg ? "_tma" : "_cpasync"));
   if (cache) {
     char extra[24];
-    snprintf(extra, sizeof(extra), "%d_%dcta", pl.nc, occ);
+    if (pl.ntm > 0) snprintf(extra, sizeof(extra), "%d_t%d_%dcta", pl.nc, pl.ntm, occ);
+    else snprintf(extra, sizeof(extra), "%d_%dcta", pl.nc, occ);
     strncat(pl.name, extra, sizeof(pl.name) - strlen(pl.name) - 1);
   }
   pl.ok = true;
@@ -496,7 +649,7 @@ struct Launch3 {
   int grid;
   int zigzag;
   bool cache = false;
-  Cache3 ch{0};
+  Cache3 ch{0, 0, 0};
   int block = 0;
   int wsg = 0;
 
@@ -518,6 +671,8 @@ struct Launch3 {
     dist = p.nranks > 1;
     cache = pl.family == 2;
     ch.nc = pl.nc;
+    ch.ntm = pl.ntm;
+    ch.tcols = pl.tcols;
     if (dist && !tma) return cudaErrorNotSupported;
     std::memset(&maps, 0, sizeof(maps));
     const bool ws = pl.variant != PERKS_HOSTLOOP && pl.cfg == 1;
@@ -581,7 +736,14 @@ cudaError_t run3(const Problem &p, const Plan &pl, const void *in, void *out, vo
       if ((e = L.step(t, steps, s)) != cudaSuccess) return e;
     return cudaSuccess;
   }
-  return L.persistent(steps, s, !(dr && dr->noncoop));
+  // A PERKS plan (its kernel carries the TMEM tier) with several CTAs per SM cannot be launched
+  // cooperatively (the
+  // runtime caps tcgen05.alloc kernels at one CTA per SM, see occupancy_ignoring_tmem): it is
+  // launched normally with a grid of exactly the co-resident capacity computed by the planner
+  // (shared memory padded so no further CTA fits an SM), which the block scheduler places all at
+  // once on an idle device.
+  const bool tmem_multi = pl.family == 2 && pl.ctas_per_sm > 1;
+  return L.persistent(steps, s, !(dr && dr->noncoop) && !tmem_multi && !env_int("PERKS_NONCOOP", 0));
 }
 }  // namespace
 

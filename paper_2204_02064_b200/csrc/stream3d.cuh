@@ -21,6 +21,7 @@
 #include "common.cuh"
 #include "dist.cuh"
 #include "shapes.cuh"
+#include "tmem.cuh"
 
 namespace perks {
 
@@ -44,6 +45,7 @@ struct Geo3D {
   static constexpr size_t SLOT_BYTES = (size_t)SLOT * sizeof(T);  // 128-B multiple (TMA dst)
   static constexpr unsigned BOX_BYTES = (unsigned)(SLOT_RAW * sizeof(T));
   static constexpr unsigned ROW_BYTES = (unsigned)(P * sizeof(T));
+
   static_assert(V * (int)sizeof(T) == 16, "one 16-byte vector per thread per row");
   static_assert(NT >= 2 * ROWS, "halo-column loaders");
   static_assert(P <= 256 && ROWS <= 256, "TMA box dims <= 256");
@@ -71,6 +73,9 @@ PERKS_DEVINL void mbar_arrive_tx(uint64_t *b, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes)
                : "memory");
 }
+PERKS_DEVINL void mbar_arrive_cnt(uint64_t *b, unsigned count) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
 PERKS_DEVINL void mbar_arrive(uint64_t *b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
 }
@@ -81,15 +86,28 @@ PERKS_DEVINL void mbar_arrive_cpasync(uint64_t *b) {
 PERKS_DEVINL void mbar_arrive_release(uint64_t *b) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
 }
+// try_wait suspends the thread for a hardware time slice; once the first try fails the spin
+// reads %globaltimer and traps after PERKS_WATCHDOG_NS (all in one asm block: no registers stay
+// live outside it and nothing is added to the fast path but one predicated branch).
 PERKS_DEVINL void mbar_wait(uint64_t *b, unsigned parity) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
+      ".reg .u64 t0, t1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra DONE_%=;\n"
+      "mov.u64 t0, %%globaltimer;\n"
       "WAIT_%=:\n"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
+      "@p bra DONE_%=;\n"
+      "mov.u64 t1, %%globaltimer;\n"
+      "sub.u64 t1, t1, t0;\n"
+      "setp.gt.u64 p, t1, %2;\n"
+      "@p trap;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
       "}\n" ::"r"(smem_u32(b)),
-      "r"(parity)
+      "r"(parity), "l"((unsigned long long)PERKS_WATCHDOG_NS)
       : "memory");
 }
 // 1D bulk async copy global -> shared (16-B aligned, size multiple of 16), completes on `bar`.
@@ -256,39 +274,36 @@ PERKS_DEVINL void arrival(StreamState<T, G> &st, const T *slot, const Coef<T, Sh
 template <class G>
 struct ThreadTile {
   int x, y;          // first owned cell
-  bool xin;          // x < nx (vector start inside the domain)
-  bool inner;        // all owned cells interior in x and y (no frame select needed)
-  bool vec;          // rows 16-byte aligned: vector stores
-  bool full;         // xin && vec && all R rows inside: the branch-free store path
-  size_t off;        // y * nx + x (offset inside a plane)
-  size_t plane;      // nx * ny
+  unsigned fmask;    // bit r*V+i: cell (x+i, y+r) is an x/y frame cell or outside the domain
+  bool full;         // x < nx, rows 16-byte aligned and all R rows inside: branch-free vector I/O
   PERKS_DEVINL void init(const Dom3 &d, int x0, int y0) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     x = x0 + lane * G::V;
     y = y0 + warp * G::R;
-    xin = x < d.nx;
-    inner = x >= 1 && x + G::V - 1 <= d.nx - 2 && y >= 1 && y + G::R - 1 <= d.ny - 2;
-    vec = (d.nx % G::V) == 0;
-    full = xin && vec && y + G::R <= d.ny;
-    off = (size_t)y * d.nx + x;
-    plane = (size_t)d.nx * d.ny;
+    full = x < d.nx && (d.nx % G::V) == 0 && y + G::R <= d.ny;
+    fmask = 0;
+#pragma unroll
+    for (int r = 0; r < G::R; r++)
+#pragma unroll
+      for (int i = 0; i < G::V; i++)
+        if (!(y + r >= 1 && y + r <= d.ny - 2 && x + i >= 1 && x + i <= d.nx - 2)) fmask |= 1u << (r * G::V + i);
   }
+  PERKS_DEVINL size_t off(const Dom3 &d) const { return (size_t)y * d.nx + x; }
 };
 
-// Frame select (reading R1) of output plane o; `old` = its step-k values (centre).
+// Frame select (reading R1) of output plane o; `old` = its step-k values (centre).  Interior
+// threads of interior planes pay one uniform compare and one mask test.
 template <typename T, class G>
 PERKS_DEVINL void frame_select(const Dom3 &d, const ThreadTile<G> &tt, int o, T (&val)[G::R][G::V],
                                const T (&old)[G::R][G::V]) {
   const bool zint = o >= d.zlo && o <= d.zhi;
-  if (zint && tt.inner) return;
+  if (zint && tt.fmask == 0) return;
+  const unsigned m = zint ? tt.fmask : ~0u;
 #pragma unroll
-  for (int r = 0; r < G::R; r++) {
-    const int y = tt.y + r;
-    const bool yint = zint && y >= 1 && y <= d.ny - 2;
+  for (int r = 0; r < G::R; r++)
 #pragma unroll
     for (int i = 0; i < G::V; i++)
-      if (!(yint && (tt.x + i) >= 1 && (tt.x + i) <= d.nx - 2)) val[r][i] = old[r][i];
-  }
+      if ((m >> (r * G::V + i)) & 1u) val[r][i] = old[r][i];
 }
 
 // Store the thread's cells of plane o (already frame-selected).
@@ -296,24 +311,43 @@ template <typename T, class G>
 PERKS_DEVINL void store_cells(T *__restrict__ dst, const Dom3 &d, const ThreadTile<G> &tt, int o,
                               const T (&v)[G::R][G::V]) {
   if (tt.full) {  // the common case: R aligned vector stores, no per-row tests
-    T *p = dst + (size_t)o * tt.plane + tt.off;
+    T *p = dst + (size_t)o * d.nx * d.ny + tt.off(d);
 #pragma unroll
     for (int r = 0; r < G::R; r++) vstore<T, G::V>(p + (size_t)r * d.nx, v[r]);
     return;
   }
-  if (!tt.xin) return;
+  if (tt.x >= d.nx) return;
   T *base = dst + (size_t)o * d.nx * d.ny;
 #pragma unroll
   for (int r = 0; r < G::R; r++) {
     const int y = tt.y + r;
     if (y >= d.ny) break;
-    if (tt.vec) {
+    if ((d.nx % G::V) == 0) {
       vstore<T, G::V>(base + (size_t)y * d.nx + tt.x, v[r]);
     } else {
 #pragma unroll
       for (int i = 0; i < G::V; i++)
         if (tt.x + i < d.nx) base[(size_t)y * d.nx + tt.x + i] = v[r][i];
     }
+  }
+}
+
+// Load the thread's cells of plane o from src (cells outside the domain read as zero: they only
+// feed frame cells, whose results are discarded).  PERKS TMEM-tier prologue.
+template <typename T, class G>
+PERKS_DEVINL void load_own_cells(const T *__restrict__ src, const Dom3 &d, const ThreadTile<G> &tt, int o,
+                                 T (&v)[G::R][G::V]) {
+  const T *base = src + (size_t)o * d.nx * d.ny;
+#pragma unroll
+  for (int r = 0; r < G::R; r++) {
+    const int y = tt.y + r;
+    if (tt.full) {
+      vload<T, G::V>(v[r], base + tt.off(d) + (size_t)r * d.nx);
+      continue;
+    }
+#pragma unroll
+    for (int i = 0; i < G::V; i++)
+      v[r][i] = (y < d.ny && tt.x + i < d.nx) ? base[(size_t)y * d.nx + tt.x + i] : T(0);
   }
 }
 
@@ -370,43 +404,6 @@ struct Ring {
         tma_load_3d(slot(k), gmap, x0 - G::PAD, y0 - 1, gz, bar(k));
       }
       if (col_arrive && threadIdx.x >= 32 && threadIdx.x < 32 + 2 * G::TY) mbar_arrive(bar(k));
-    }
-  }
-  // Halo ring only of plane q into `dst_slot` (PERKS cached plane), completing on arrival k.
-  // TMA path: the two halo rows (corners included) by 1D bulk copies clipped to the domain
-  // (cells outside stay stale: they only feed frame cells, whose results are discarded); the
-  // two halo columns by per-thread cp.async of warp 1 (arrive.noinc on the slot's mbarrier).
-  PERKS_DEVINL void issue_halo(unsigned k, T *dst_slot, const T *src, const Dom3 &d, int q, int x0,
-                               int y0) {
-    if constexpr (TMA) {
-      if (threadIdx.x == 0) {
-        fence_proxy_async();
-        const bool zin = q >= 0 && q < d.nz;
-        const int xa = max(x0 - G::PAD, 0), xb = min(x0 + G::TX + G::PAD, d.nx);
-        const unsigned rb = (unsigned)((xb - xa) * (int)sizeof(T));
-        const bool top = zin && y0 >= 1, bot = zin && y0 + G::TY < d.ny;
-        mbar_arrive_tx(bar(k), (top ? rb : 0u) + (bot ? rb : 0u));
-        const size_t pl = (size_t)d.nx * d.ny;
-        if (top)
-          bulk_load(dst_slot + (xa - (x0 - G::PAD)), src + (size_t)q * pl + (size_t)(y0 - 1) * d.nx + xa, rb, bar(k));
-        if (bot)
-          bulk_load(dst_slot + (G::ROWS - 1) * G::P + (xa - (x0 - G::PAD)),
-                    src + (size_t)q * pl + (size_t)(y0 + G::TY) * d.nx + xa, rb, bar(k));
-      }
-      if (threadIdx.x >= 32 && threadIdx.x < 32 + 2 * G::TY) {
-        const int t = threadIdx.x - 32;
-        const int j = 1 + (t >> 1);
-        const bool right = t & 1;
-        const int y = y0 - 1 + j;
-        const int xx = right ? x0 + G::TX : x0 - 1;
-        const bool ok = q >= 0 && q < d.nz && y < d.ny && xx >= 0 && xx < d.nx;
-        const T *g = ok ? src + ((size_t)q * d.ny + y) * d.nx + xx : src;
-        cp_async<(int)sizeof(T)>(dst_slot + j * G::P + (right ? G::PAD + G::TX : G::PAD - 1), g, ok);
-        mbar_arrive_cpasync(bar(k));
-      }
-    } else {
-      issue_plane<T, G>(dst_slot, src, d, q, x0, y0, true);
-      cp_async_commit();
     }
   }
   // Past the unit's last plane: cp.async commits an empty group so wait_group counting stays
@@ -473,13 +470,39 @@ PERKS_DEVINL void send_face(const DistStep &ds, const Dom3 &d, const ThreadTile<
   signal_counter_sys(lo ? ds.k->peer_ctr_lo : ds.k->peer_ctr_hi, cells);  // (local nz >= 2: never both)
 }
 
-// PERKS plane cache of one unit (k3d_perks.cu): planes q with cmap[q - czs] >= 0 stay resident in
-// shared-memory slot cache + cmap[q - czs] * G::SLOT across steps.
-template <typename T> struct CacheView {
-  T *cache;
-  const short *cmap;
-  int czs, cze;  // the cached unit's planes [czs, cze) (first/last never cached)
+// PERKS plane cache of one unit (k3d_stream.cu): the cache-code map is indexed by the unit's
+// arrival index k (plane czs - 1 + k, k in [0, cze - czs + 2), plus one -1 sentinel), so a lookup is
+// one shared-memory load at a fixed offset from the map.
+// Cache codes (one signed byte per arrival): -1 = streamed; 0 <= c < kTmemCode: shared-memory
+// slot c; c >= kTmemCode: TMEM plane c - kTmemCode (tmem.cuh), staged into the ring slot of its
+// arrival one arrival ahead.
+constexpr int kTmemCode = 64;
+PERKS_DEVINL bool is_smem_code(int c) { return c >= 0 && c < kTmemCode; }
+PERKS_DEVINL bool is_tmem_code(int c) { return c >= kTmemCode; }
+// Dynamic shared memory of the persistent 3D kernels: ring slots, 128 B of mbarriers and the TMEM
+// address, then (PERKS) nc cache slots and the CTA's cache-code map.  Every address is the
+// dynamic-smem base plus an offset (no pointer registers).
+PERKS_DEVINL unsigned char *dyn_smem() {
+  extern __shared__ __align__(128) unsigned char perks_ws_dyn_smem[];
+  return perks_ws_dyn_smem;
+}
+// PERKS plane cache of one CTA (k3d_stream.cu): the cached planes are spread evenly over ALL the
+// CTA's units of a step (so the HBM stream of every CTA continues through the whole step); the
+// code map is indexed by the CTA's arrival index within the step (units back to back, each unit
+// contributing its planes zs-1 .. ze, plus a -1 sentinel).
+template <typename T, class G> struct CacheView {
+  int nc;          // shared-memory slots of the layout (kernel parameter)
+  int kbase;       // arrival index of the current unit's first arrival within the step
+  uint32_t tbase;  // TMEM address of cached plane 0 for this thread's warp (lane quarter + column)
+  PERKS_DEVINL static T *cache() {
+    return reinterpret_cast<T *>(dyn_smem() + (size_t)G::NS * G::SLOT_BYTES + 128);
+  }
+  PERKS_DEVINL T *slot(int c) const { return cache() + (size_t)c * G::SLOT; }
+  PERKS_DEVINL signed char *cmap() const { return reinterpret_cast<signed char *>(cache() + (size_t)nc * G::SLOT); }
 };
+template <typename T, class G> constexpr int tmem_cpp() {  // TMEM columns per cached plane (tmem.cuh)
+  return TmemCells<T, G::R, G::V>::WPT * ((G::NWARP + 3) / 4);
+}
 
 template <typename T, class G>
 PERKS_DEVINL void write_own(T *slot, const T (&v)[G::R][G::V]) {
@@ -526,27 +549,19 @@ PERKS_DEVINL void publish_perimeter(T *__restrict__ dst, const Dom3 &d, int o, i
   }
 }
 
-template <typename T, int S, class G, bool TMA, bool DIST, bool CACHE = false>
+template <typename T, int S, class G, bool TMA, bool DIST>
 PERKS_DEVINL void stream_unit(Ring<T, G, TMA> &ring, const T *__restrict__ src,
                               const CUtensorMap *map, T *__restrict__ dst, const Dom3 &d, int x0,
                               int y0, int zs, int ze, const Coef<T, Shape<S>::N> &c,
-                              const DistStep &ds, bool col_arrive = false,
-                              const CacheView<T> &cv = CacheView<T>{}) {
+                              const DistStep &ds, bool col_arrive = false) {
   constexpr int D = G::NS - 1;
   const int q0 = zs - 1;
   const int narr = ze - zs + 2;
   const unsigned k0 = ring.gk;
   ThreadTile<G> tt;
   tt.init(d, x0, y0);
-  // cache slot of plane q (CACHE only), -1 = streamed through the ring
-  auto cs = [&](int q) -> int {
-    if constexpr (!CACHE) return -1;
-    return (q > cv.czs && q < cv.cze - 1) ? (int)cv.cmap[q - cv.czs] : -1;
-  };
   auto issue = [&](unsigned k, int q) {
-    const int sl = cs(q);
-    if (CACHE && sl >= 0) ring.issue_halo(k, cv.cache + (size_t)sl * G::SLOT, src, d, q, x0, y0);
-    else issue_plane_any<T, G, TMA, DIST>(ring, k, src, map, d, q, x0, y0, col_arrive, ds);
+    issue_plane_any<T, G, TMA, DIST>(ring, k, src, map, d, q, x0, y0, col_arrive, ds);
   };
 #pragma unroll
   for (int k = 0; k < D; k++) {
@@ -562,20 +577,11 @@ PERKS_DEVINL void stream_unit(Ring<T, G, TMA> &ring, const T *__restrict__ src,
     if (k + D < narr) issue(k0 + k + D, q + D);
     else ring.issue_none();
     T out[G::R][G::V], cq[G::R][G::V];
-    const int slq = cs(q);
-    arrival<T, S, G>(st, slq >= 0 ? cv.cache + (size_t)slq * G::SLOT : ring.slot(k0 + k), c, out, cq);
+    arrival<T, S, G>(st, ring.slot(k0 + k), c, out, cq);
     if (q - 1 >= zs) {
       frame_select<T, G>(d, tt, q - 1, out, st.cm1);
-      const int slo = cs(q - 1);
-      if (CACHE && slo >= 0) {
-        // cached output: stays on chip (its slot was last read at arrival q-1, before this
-        // arrival's barrier); only the tile perimeter goes to global memory (Fig. 6 Destination)
-        publish_perimeter<T, G>(dst, d, q - 1, x0, y0, out);
-        write_own<T, G>(cv.cache + (size_t)slo * G::SLOT, out);
-      } else {
-        store_cells<T, G>(dst, d, tt, q - 1, out);
-        if constexpr (DIST) send_face<T, G>(ds, d, tt, q - 1, x0, y0, out);
-      }
+      store_cells<T, G>(dst, d, tt, q - 1, out);
+      if constexpr (DIST) send_face<T, G>(ds, d, tt, q - 1, x0, y0, out);
     }
 #pragma unroll
     for (int r = 0; r < G::R; r++)
@@ -599,24 +605,28 @@ PERKS_DEVINL void stream_unit(Ring<T, G, TMA> &ring, const T *__restrict__ src,
 template <typename T, class G>
 struct WsPipe {
   static constexpr unsigned FULL_COUNT = 33;
-  T *slots;
-  uint64_t *full, *empty;
+  // The ring sits at the start of dynamic shared memory (slots, then full / empty / tfull
+  // mbarriers): addresses are compile-time offsets from the dynamic-smem base, not registers.
   unsigned gk;
+  unsigned tph;     // TMEM tier: phase bit per slot of the tfull mbarriers (after full/empty: one
+                    // arrival per consumer warp once its cells are staged; identical sequence)
 
-  PERKS_DEVINL T *slot(unsigned k) const { return slots + (size_t)(k % G::NS) * G::SLOT; }
-  PERKS_DEVINL uint64_t *fb(unsigned k) const { return full + (k % G::NS); }
-  PERKS_DEVINL uint64_t *eb(unsigned k) const { return empty + (k % G::NS); }
+  PERKS_DEVINL static unsigned char *base() { return dyn_smem(); }
+  PERKS_DEVINL static uint64_t *bars() { return reinterpret_cast<uint64_t *>(base() + (size_t)G::NS * G::SLOT_BYTES); }
+  PERKS_DEVINL T *slot(unsigned k) const { return reinterpret_cast<T *>(base()) + (size_t)(k % G::NS) * G::SLOT; }
+  PERKS_DEVINL uint64_t *fb(unsigned k) const { return bars() + (k % G::NS); }
+  PERKS_DEVINL uint64_t *eb(unsigned k) const { return bars() + G::NS + (k % G::NS); }
+  PERKS_DEVINL uint64_t *tb(unsigned k) const { return bars() + 2 * G::NS + (k % G::NS); }
 
   // all threads: thread 0 initialises the barriers
-  PERKS_DEVINL void init(T *s, uint64_t *bars) {
-    slots = s;
-    full = bars;
-    empty = bars + G::NS;
+  PERKS_DEVINL void init() {
     gk = 0;
+    tph = 0;
     if (threadIdx.x == 0) {
       for (int i = 0; i < G::NS; i++) {
-        mbar_init(full + i, FULL_COUNT);
-        mbar_init(empty + i, G::NWARP);
+        mbar_init(fb(i), FULL_COUNT);
+        mbar_init(eb(i), G::NWARP);
+        mbar_init(tb(i), G::NWARP);  // tfull (TMEM tier)
       }
       mbar_fence_init();
     }
@@ -648,8 +658,9 @@ struct WsPipe {
     __syncwarp();
     load_box(k, slot(k), gmap, x0, y0, gz);
   }
-  // halo ring only (PERKS cached plane q) into `dst`: rows by bulk copies (lane 0), the two
-  // columns by per-lane cp.async completing on the same barrier
+  // halo ring only (PERKS cached plane q) into `dst` (a cache slot, or the ring slot of a TMEM
+  // plane whose interior the consumers stage): rows by bulk copies (lane 0), the two columns by
+  // per-lane cp.async completing on the same barrier.  Halo cells are never cached.
   PERKS_DEVINL void load_halo(unsigned k, T *dst, const T *src, const Dom3 &d, int q, int x0, int y0) {
     const int lane = threadIdx.x & 31;
     if (lane == 0) {
@@ -682,6 +693,16 @@ struct WsPipe {
   }
   // every consumer warp has released arrival k (its slot's reads are complete)
   PERKS_DEVINL void wait_released(unsigned k) { mbar_wait(eb(k), (k / G::NS) & 1u); }
+  // TMEM tier: this warp's cells of arrival k are in its slot / every warp's are
+  PERKS_DEVINL void staged(unsigned k) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive_release(tb(k));
+  }
+  PERKS_DEVINL void wait_staged(unsigned k) {
+    const unsigned i = k % G::NS;
+    mbar_wait(tb(k), (tph >> i) & 1u);
+    tph ^= 1u << i;
+  }
 };
 
 // Named barrier over the consumer warps only (the producer keeps streaming).
@@ -706,6 +727,16 @@ PERKS_DEVINL void send_face_ws(const DistStep &ds, const Dom3 &d, const ThreadTi
   }
 }
 
+// TMEM tier, consumer warp: the thread's own cells of TMEM plane t into the ring slot of arrival k
+// (the producer loads the slot's halo ring), then this warp's arrival on the slot's tfull barrier.
+template <typename T, class G>
+PERKS_DEVINL void stage_tmem_plane(WsPipe<T, G> &pp, const CacheView<T, G> &cv, unsigned k, int t) {
+  T v[G::R][G::V];
+  TmemCells<T, G::R, G::V>::load(cv.tbase + (uint32_t)(t * tmem_cpp<T, G>()), v);
+  write_own<T, G>(pp.slot(k), v);
+  pp.staged(k);
+}
+
 // One unit (tile x0,y0; planes [zs, ze)) of one step through the warp-specialised pipeline.
 // Called by ALL warps of the CTA; the producer issues arrivals zs-1 .. ze, the consumers run the
 // staged plane body (arrival(), stages A/B/C) and store / cache the outputs.
@@ -713,13 +744,14 @@ template <typename T, int S, class G, bool DIST, bool CACHE = false>
 PERKS_DEVINL void stream_unit_ws(WsPipe<T, G> &pp, const T *__restrict__ src, const CUtensorMap *map,
                                  T *__restrict__ dst, const Dom3 &d, int x0, int y0, int zs, int ze,
                                  const Coef<T, Shape<S>::N> &c, const DistStep &ds,
-                                 const CacheView<T> &cv = CacheView<T>{}) {
+                                 const CacheView<T, G> &cv = CacheView<T, G>{}) {
   const int q0 = zs - 1;
   const int narr = ze - zs + 2;
   const unsigned k0 = pp.gk;
-  auto cs = [&](int q) -> int {
+  const signed char *cmk = CACHE ? cv.cmap() + cv.kbase : nullptr;  // this unit's arrival codes
+  auto cs = [&](int k) -> int {
     if constexpr (!CACHE) return -1;
-    return (q > cv.czs && q < cv.cze - 1) ? (int)cv.cmap[q - cv.czs] : -1;
+    return (int)cmk[k];
   };
   pp.gk = k0 + narr;
   if ((int)(threadIdx.x >> 5) == G::NWARP) {  // ---- producer
@@ -727,9 +759,11 @@ PERKS_DEVINL void stream_unit_ws(WsPipe<T, G> &pp, const T *__restrict__ src, co
       const unsigned kk = k0 + k;
       const int q = q0 + k;
       pp.acquire(kk);
-      const int sl = cs(q);
-      if (CACHE && sl >= 0) {
-        pp.load_halo(kk, cv.cache + (size_t)sl * G::SLOT, src, d, q, x0, y0);
+      const int sl = cs(k);
+      if (CACHE && is_smem_code(sl)) {
+        pp.load_halo(kk, cv.slot(sl), src, d, q, x0, y0);
+      } else if (CACHE && is_tmem_code(sl)) {
+        pp.load_halo(kk, pp.slot(kk), src, d, q, x0, y0);  // interior staged by the consumers
       } else {
         const int gs = DIST ? ghost_side(ds, d, q) : -1;
         if (gs < 0) pp.load_full(kk, map, x0, y0, q);
@@ -748,19 +782,25 @@ PERKS_DEVINL void stream_unit_ws(WsPipe<T, G> &pp, const T *__restrict__ src, co
   for (int k = 0; k < narr; k++) {
     const unsigned kk = k0 + k;
     const int q = q0 + k;
-    const int slq = cs(q);
+    const int slq = cs(k);
     pp.wait_full(kk);
+    if (CACHE && is_tmem_code(slq)) pp.wait_staged(kk);
     T out[G::R][G::V], cq[G::R][G::V];
-    arrival<T, S, G>(st, (CACHE && slq >= 0) ? cv.cache + (size_t)slq * G::SLOT : pp.slot(kk), c, out, cq);
+    arrival<T, S, G>(st, (CACHE && is_smem_code(slq)) ? cv.slot(slq) : pp.slot(kk), c, out, cq);
     pp.release(kk);
     if (q - 1 >= zs) {
       frame_select<T, G>(d, tt, q - 1, out, st.cm1);
-      const int slo = cs(q - 1);
-      if (CACHE && slo >= 0) {
+      const int slo = cs(k - 1);
+      if (CACHE && is_smem_code(slo)) {
         // cached output: stays on chip once every warp has finished reading the old plane
         publish_perimeter<T, G>(dst, d, q - 1, x0, y0, out);
         pp.wait_released(kk - 1);
-        write_own<T, G>(cv.cache + (size_t)slo * G::SLOT, out);
+        write_own<T, G>(cv.slot(slo), out);
+      } else if (CACHE && is_tmem_code(slo)) {
+        // TMEM-cached output: the thread's own columns (plane q-1 was staged from them at
+        // arrival q-2, before this write in program order)
+        publish_perimeter<T, G>(dst, d, q - 1, x0, y0, out);
+        TmemCells<T, G::R, G::V>::store(cv.tbase + (uint32_t)((slo - kTmemCode) * tmem_cpp<T, G>()), out);
       } else {
         store_cells<T, G>(dst, d, tt, q - 1, out);
         if constexpr (DIST) send_face_ws<T, G>(ds, d, tt, q - 1, x0, y0, out);
@@ -770,6 +810,15 @@ PERKS_DEVINL void stream_unit_ws(WsPipe<T, G> &pp, const T *__restrict__ src, co
     for (int r = 0; r < G::R; r++)
 #pragma unroll
       for (int i = 0; i < G::V; i++) st.cm1[r][i] = cq[r][i];
+    if constexpr (CACHE) {
+      // TMEM tier: stage the NEXT arrival's cells (TMEM -> registers -> its ring slot) one
+      // arrival ahead, at the point of the body with the fewest live registers
+      const int sln = cs(k + 1);  // (sentinel -1 after the unit's last arrival)
+      if (is_tmem_code(sln)) {
+        if (kk + 1 >= (unsigned)G::NS) pp.wait_released(kk + 1 - G::NS);  // slot free
+        stage_tmem_plane<T, G>(pp, cv, kk + 1, sln - kTmemCode);
+      }
+    }
   }
 }
 

@@ -97,6 +97,7 @@ class Stencil:
             "ctas_per_sm": info.ctas_per_sm, "tile": list(info.tile),
             "regs_per_thread": info.regs_per_thread, "smem_per_cta": info.smem_per_cta,
             "cached_cells_reg": info.cached_cells_reg, "cached_cells_smem": info.cached_cells_smem,
+            "cached_cells_tmem": info.cached_cells_tmem, "tmem_cols_per_cta": info.tmem_cols_per_cta,
             "total_cells": info.total_cells, "dram_bytes_per_step": info.dram_bytes_per_step,
             "halo_bytes_per_step": info.halo_bytes_per_step,
             "workspace_bytes": int(info.workspace_bytes),

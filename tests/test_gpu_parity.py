@@ -226,3 +226,30 @@ def test_strip_kernel(monkeypatch, shape, name):
     for T in (1, 2, 7, 40):
         ref = oracle.run(u0, offs, w, T, nthreads=8)
         _check(_run_gpu(u0, name, w, T, "perks"), ref, u0, np.float32)
+
+
+@pytest.mark.parametrize("nsm,ntm", [("0", ""), ("2", ""), ("0", "1"), ("3", "5")])
+@pytest.mark.parametrize("wsg", ["0", "1"])
+@pytest.mark.parametrize("name,dtype,shape", [("3d7pt", np.float64, (70, 33, 72)),
+                                              ("3d27pt", np.float32, (61, 40, 136))])
+def test_perks3d_tmem_tier(monkeypatch, nsm, ntm, wsg, name, dtype, shape):
+    """PERKS-3D Tensor-Memory cache tier (tmem.cuh): planes kept in TMEM across steps (tcgen05.st
+    at write-back, tcgen05.ld + staging into the ring slot one arrival ahead), alone or mixed
+    with the shared-memory tier, both warp-specialised geometries, long units (one z-chunk),
+    ragged tiles in x and y, both step parities: bit-exact vs the oracle."""
+    _need_gpu()
+    monkeypatch.setenv("PERKS_P3D_NSM", nsm)
+    if ntm:
+        monkeypatch.setenv("PERKS_P3D_NTM", ntm)
+    monkeypatch.setenv("PERKS_WSG", wsg)
+    monkeypatch.setenv("PERKS_S3D_NZC", "1")
+    from paper_2204_02064_b200 import Stencil
+    offs, w = si.preset(name)
+    st = Stencil(shape, offs, w, dtype=dtype)
+    q = st.query("perks")
+    st.close()
+    assert q["cached_cells_tmem"] > 0 and q["tmem_cols_per_cta"] > 0, q
+    u0 = si.field(shape, dtype=dtype, seed=808)
+    for T in (1, 4, 7):
+        ref = oracle.run(u0, offs, w, T, nthreads=8)
+        _check(_run_gpu(u0, name, w, T, "perks"), ref, u0, dtype)
