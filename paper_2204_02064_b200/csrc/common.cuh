@@ -34,6 +34,33 @@ PERKS_DEVINL double opaque_copy(double v) {
   return r;
 }
 
+// --------------------------------------------------------------------- warp shuffles
+// Neighbour-lane exchange by inline PTX: the compiler cannot prove convergence after the
+// mbarrier-wait asm blocks and would guard every __shfl_*_sync with a BRA.DIV fallback; these
+// are always called by full, converged warps.
+PERKS_DEVINL uint32_t shfl_up1_u32(uint32_t v) {
+  uint32_t r;
+  asm("shfl.sync.up.b32 %0, %1, 1, 0, -1;\n" : "=r"(r) : "r"(v));
+  return r;
+}
+PERKS_DEVINL uint32_t shfl_down1_u32(uint32_t v) {
+  uint32_t r;
+  asm("shfl.sync.down.b32 %0, %1, 1, 31, -1;\n" : "=r"(r) : "r"(v));
+  return r;
+}
+PERKS_DEVINL float shfl_up1(float v) { return __uint_as_float(shfl_up1_u32(__float_as_uint(v))); }
+PERKS_DEVINL float shfl_down1(float v) { return __uint_as_float(shfl_down1_u32(__float_as_uint(v))); }
+PERKS_DEVINL double shfl_up1(double v) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  const uint32_t lo = shfl_up1_u32((uint32_t)b), hi = shfl_up1_u32((uint32_t)(b >> 32));
+  return __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
+}
+PERKS_DEVINL double shfl_down1(double v) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  const uint32_t lo = shfl_down1_u32((uint32_t)b), hi = shfl_down1_u32((uint32_t)(b >> 32));
+  return __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
+}
+
 // --------------------------------------------------------------------- vectors
 template <typename T, int V> struct VecT;
 template <> struct VecT<float, 1> { using type = float; };

@@ -40,11 +40,16 @@ static_assert(G3Sel<float>::G::NT == K3D_THREADS && G3Sel<double>::G::NT == K3D_
 // by the planner (profiles/r01_ws_geometry_sweep.txt): WSG 0 = 8 warps x 2 CTAs/SM (best while the
 // domain is within a few L2 sizes, C3/C4); WSG 1 = 4 warps x 3 CTAs/SM (more independent plane
 // streams in flight: best for domains far larger than L2, C5).
-constexpr int wsg_nwarp(int g) { return g == 0 ? 8 : 4; }
-constexpr int wsg_minb(int g) { return g == 0 ? 2 : 3; }
+// WSG 2 = 8 warps x 4 rows x 1 CTA/SM: one CTA per SM with a large register budget per thread
+// (profiles/r01_wsg2_sweep.txt; a single CTA per SM also keeps the TMEM tier launchable
+// cooperatively).
+constexpr int wsg_nwarp(int g) { return g == 1 ? 4 : 8; }
+constexpr int wsg_minb(int g) { return g == 0 ? 2 : g == 1 ? 3 : 1; }
+constexpr int wsg_r(int g) { return g == 2 ? 2 * PERKS_S3D_R : PERKS_S3D_R; }
+constexpr int kNumWsg = 3;
 template <typename T, bool WS, int WSG = 0> struct GS { using G = typename G3Sel<T>::G; };
 template <typename T, int WSG> struct GS<T, true, WSG> {
-  using G = Geo3D<T, 16 / (int)sizeof(T), PERKS_S3D_R, wsg_nwarp(WSG), PERKS_S3D_NS>;
+  using G = Geo3D<T, 16 / (int)sizeof(T), wsg_r(WSG), wsg_nwarp(WSG), PERKS_S3D_NS>;
 };
 
 struct Units3 {
@@ -61,10 +66,9 @@ PERKS_DEVINL void unit_coords(const Units3 &u, int id, int tile_x, int tile_y, i
   zs = zc * u.zc;
 }
 
-// Ring slots, then full/empty/tfull mbarriers (3 x NS) and the TMEM base address: within the
-// 128 bytes the persistent kernel reserves before its plane cache.
+// Ring slots, then full/empty/tfull mbarriers (3 x NS) and the TMEM base address (Geo3D::BAR_BYTES,
+// before the PERKS plane cache).
 template <class G> PERKS_DEVINL uint64_t *ring_bars(unsigned char *smem) {
-  static_assert(3 * G::NS * 8 + 8 <= 128, "ring barriers + TMEM address exceed 128 B");
   return reinterpret_cast<uint64_t *>(smem + (size_t)G::NS * G::SLOT_BYTES);
 }
 
@@ -237,10 +241,11 @@ __global__ void __launch_bounds__(k3d_threads<TMA, WSG>(), DIST ? 1 : wsg_minb(W
     if (TMA && threadIdx.x == 0) fence_proxy_async_global();  // last step's stores -> TMA reads
     cv.kbase = 0;
     for (int jj = 0; jj < nmine; jj++) {
-      const int id = (int)blockIdx.x + jj * (int)gridDim.x;
+      int id = (int)blockIdx.x + jj * (int)gridDim.x;
       int x0, y0, zs;
       // (the zig-zag unit-order experiment never applies to PERKS: the cache map is per unit)
-      unit_coords(u, (!CACHE && u.rev && (t & 1)) ? nunits - 1 - id : id, G::TX, G::TY, x0, y0, zs);
+      if (!CACHE && u.rev && (t & 1)) id = nunits - 1 - id;
+      unit_coords(u, id, G::TX, G::TY, x0, y0, zs);
       const int ze = min(zs + u.zc, d.nz);
       if constexpr (TMA) {
         stream_unit_ws<T, S, G, DIST, CACHE>(pp, src, &maps.box[src_idx], dst, d, x0, y0, zs, ze, c, ds, cv);
@@ -385,8 +390,14 @@ cudaError_t launch_dist_prologue(const Problem &p, const void *in, const DistRun
 namespace {
 // persistent kernel pointer for (shape, TMA, DIST, CACHE, WSG)
 template <typename T, int S, bool DIST, bool CACHE> void *pk_w(int wsg) {
-  return wsg == 1 ? (void *)persistent3d_kernel<T, S, true, DIST, CACHE, 1>
-                  : (void *)persistent3d_kernel<T, S, true, DIST, CACHE, 0>;
+  switch (wsg) {
+    case 1: return (void *)persistent3d_kernel<T, S, true, DIST, CACHE, 1>;
+    default: break;
+  }
+  if constexpr (!DIST) {  // (multi-GPU slabs use WSG 0/1 only)
+    if (wsg == 2) return (void *)persistent3d_kernel<T, S, true, DIST, CACHE, 2>;
+  }
+  return (void *)persistent3d_kernel<T, S, true, DIST, CACHE, 0>;
 }
 template <typename T, int S> void *pk_s(bool tma, bool dist, bool cache, int wsg) {
   if (!tma) return (void *)persistent3d_kernel<T, S, false, false, false, 0>;
@@ -426,23 +437,23 @@ template <typename T, bool WS, int WSG> void geo3_t(int &tx, int &ty, int &nt, s
                                                   int &P, int &ROWS) {
   using G = typename GS<T, WS, WSG>::G;
   tx = G::TX; ty = G::TY; nt = G::NT + (WS ? 32 : 0); slot = G::SLOT_BYTES;
-  ring = (size_t)G::NS * G::SLOT_BYTES + 3 * (size_t)G::NS * sizeof(uint64_t) + 16;  // + TMEM address
+  ring = G::RING_BYTES;  // slots + mbarriers + TMEM address (Geo3D)
   P = G::P; ROWS = G::ROWS;
 }
 struct Geo3Info { int TX, TY, NT, P, ROWS, cpp; size_t slot, ring; };
-template <typename T> Geo3Info geo3(bool ws, int wsg) {
+template <typename T, bool WS, int WSG> Geo3Info geo3_g() {
   Geo3Info g;
-  if (!ws) {
-    geo3_t<T, false, 0>(g.TX, g.TY, g.NT, g.slot, g.ring, g.P, g.ROWS);
-    g.cpp = tmem_cpp<T, typename GS<T, false, 0>::G>();
-  } else if (wsg == 1) {
-    geo3_t<T, true, 1>(g.TX, g.TY, g.NT, g.slot, g.ring, g.P, g.ROWS);
-    g.cpp = tmem_cpp<T, typename GS<T, true, 1>::G>();
-  } else {
-    geo3_t<T, true, 0>(g.TX, g.TY, g.NT, g.slot, g.ring, g.P, g.ROWS);
-    g.cpp = tmem_cpp<T, typename GS<T, true, 0>::G>();
-  }
+  geo3_t<T, WS, WSG>(g.TX, g.TY, g.NT, g.slot, g.ring, g.P, g.ROWS);
+  g.cpp = tmem_cpp<T, typename GS<T, WS, WSG>::G>();
   return g;
+}
+template <typename T> Geo3Info geo3(bool ws, int wsg) {
+  if (!ws) return geo3_g<T, false, 0>();
+  switch (wsg) {
+    case 1: return geo3_g<T, true, 1>();
+    case 2: return geo3_g<T, true, 2>();
+    default: return geo3_g<T, true, 0>();
+  }
 }
 }  // namespace
 
@@ -485,8 +496,8 @@ Plan plan_stream3d(const Problem &p, perks_variant v) {
   // WS geometry: 4 warps x 3 CTAs/SM once one buffer is >= 16 L2 sizes (more plane streams in
   // flight for DRAM-latency-bound streaming), else 8 warps x 2 CTAs/SM
   int wsg = ((double)p.cells() * p.elem() >= 16.0 * (double)p.l2_bytes) ? 1 : 0;
-  if (env_int("PERKS_WSG", -1) >= 0) wsg = env_int("PERKS_WSG", 0) ? 1 : 0;
-  if (!ws) wsg = 0;
+  if (env_int("PERKS_WSG", -1) >= 0) wsg = std::min(std::max(env_int("PERKS_WSG", 0), 0), kNumWsg - 1);
+  if (!ws || (p.nranks > 1 && wsg > 1)) wsg = std::min(wsg, ws ? 1 : 0);
   void *k = persistent ? persist_ptr(p, tma, cache, wsg) : pick3(p, false);
   const Geo3Info gi = p.dtype == PERKS_F32 ? geo3<float>(ws, wsg) : geo3<double>(ws, wsg);
   const size_t ring = gi.ring, slot = gi.slot;
@@ -525,6 +536,9 @@ Plan plan_stream3d(const Problem &p, perks_variant v) {
       pl.why = "cudaFuncSetAttribute"; return pl;
     }
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NT, smem);
+    // warp-specialised persistent kernels: the geometry's designed CTAs per SM (more CTAs of the
+    // 4-warp geometry measured slower on C5: 3.63 vs 2.90 ms/step, profiles/r01_perks3d_tmem_probe.txt)
+    if (ws) occ = std::min(occ, env_int("PERKS_S3D_CPS", wsg_minb(wsg)));
   } else {
     // PERKS: the shared memory the ring leaves at `cps` CTAs per SM caches planes (
     // minimal occupancy that keeps the HBM stream saturated: 2 CTAs/SM measured best)
@@ -541,7 +555,7 @@ Plan plan_stream3d(const Problem &p, perks_variant v) {
       const int64_t zc_c = (p.nz + nzc_c - 1) / nzc_c, un_c = (int64_t)tiles * nzc_c;
       const int64_t g_c = std::min<int64_t>(un_c, (int64_t)cps * p.num_sms);
       const size_t map_bytes = align256((size_t)(((un_c + g_c - 1) / g_c) * (zc_c + 2) + 1));
-      const size_t fixed = ring + 128 + map_bytes;
+      const size_t fixed = ring + map_bytes;
       nc = budget > fixed ? (int)((budget - fixed) / slot) : 0;
       const int forced = env_int("PERKS_P3D_NSM", -1);
       if (forced >= 0) nc = std::min(nc, forced);

@@ -27,6 +27,9 @@ namespace perks {
 
 // Unroll factor of the per-plane loops (3 turns the stage-accumulator rotation into register
 // renaming; sweeps only, the default keeps register pressure low).
+#ifndef PERKS_NB_LDS
+#define PERKS_NB_LDS 1
+#endif
 #ifndef PERKS_WS_UNROLL
 #define PERKS_WS_UNROLL 1
 #endif
@@ -45,6 +48,10 @@ struct Geo3D {
   static constexpr size_t SLOT_BYTES = (size_t)SLOT * sizeof(T);  // 128-B multiple (TMA dst)
   static constexpr unsigned BOX_BYTES = (unsigned)(SLOT_RAW * sizeof(T));
   static constexpr unsigned ROW_BYTES = (unsigned)(P * sizeof(T));
+  // after the NS ring slots: full / empty / tfull mbarriers (3 x NS x 8 B) and the TMEM base
+  // address, padded to 128 B (the PERKS plane cache follows)
+  static constexpr size_t BAR_BYTES = (3 * NS * 8 + 16 + 127) / 128 * 128;
+  static constexpr size_t RING_BYTES = (size_t)NS * SLOT_BYTES + BAR_BYTES;
 
   static_assert(V * (int)sizeof(T) == 16, "one 16-byte vector per thread per row");
   static_assert(NT >= 2 * ROWS, "halo-column loaders");
@@ -193,11 +200,18 @@ PERKS_DEVINL void read_nb(const T *slot, T (&nb)[G::R + 2][G::V + 2]) {
     const T *row = slot + (warp * G::R + j) * G::P;
     T v[G::V];
     vload<T, G::V>(v, row + G::PAD + lane * G::V);
-    const T l = __shfl_up_sync(0xffffffffu, v[G::V - 1], 1);
-    const T r = __shfl_down_sync(0xffffffffu, v[0], 1);
+#if PERKS_NB_LDS
+    // x-neighbours straight from shared memory (the slot holds the halo columns): two scalar
+    // loads, no shuffle / select on the dependency chain
+    nb[j][0] = row[G::PAD + lane * G::V - 1];
+    nb[j][G::V + 1] = row[G::PAD + lane * G::V + G::V];
+#else
+    const T l = shfl_up1(v[G::V - 1]);
+    const T r = shfl_down1(v[0]);
     const T el = row[G::PAD - 1 + (lane == 31 ? G::TX + 1 : 0)];  // one broadcast-free LDS
     nb[j][0] = lane == 0 ? el : l;
     nb[j][G::V + 1] = lane == 31 ? el : r;
+#endif
 #pragma unroll
     for (int i = 0; i < G::V; i++) nb[j][i + 1] = v[i];
   }
@@ -275,18 +289,31 @@ template <class G>
 struct ThreadTile {
   int x, y;          // first owned cell
   unsigned fmask;    // bit r*V+i: cell (x+i, y+r) is an x/y frame cell or outside the domain
+  unsigned pmask;    // bit r*V+i: cell (x+i, y+r) is on the tile perimeter and inside the domain
   bool full;         // x < nx, rows 16-byte aligned and all R rows inside: branch-free vector I/O
   PERKS_DEVINL void init(const Dom3 &d, int x0, int y0) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     x = x0 + lane * G::V;
     y = y0 + warp * G::R;
     full = x < d.nx && (d.nx % G::V) == 0 && y + G::R <= d.ny;
+    const int xl = min(x0 + G::TX, d.nx) - 1, yl = min(y0 + G::TY, d.ny) - 1;  // last tile cells
+    unsigned xin = 0, xint = 0, xper = 0;  // per column i: inside / interior / tile edge
+#pragma unroll
+    for (int i = 0; i < G::V; i++) {
+      xin |= (unsigned)(x + i < d.nx) << i;
+      xint |= (unsigned)(x + i >= 1 && x + i <= d.nx - 2) << i;
+      xper |= (unsigned)(x + i == x0 || x + i == xl) << i;
+    }
     fmask = 0;
+    pmask = 0;
 #pragma unroll
-    for (int r = 0; r < G::R; r++)
-#pragma unroll
-      for (int i = 0; i < G::V; i++)
-        if (!(y + r >= 1 && y + r <= d.ny - 2 && x + i >= 1 && x + i <= d.nx - 2)) fmask |= 1u << (r * G::V + i);
+    for (int r = 0; r < G::R; r++) {
+      const int yy = y + r;
+      const unsigned row = (yy >= 1 && yy <= d.ny - 2) ? xint : 0u;
+      fmask |= (~row & ((1u << G::V) - 1)) << (r * G::V);
+      const unsigned per = (yy < d.ny) ? ((yy == y0 || yy == yl) ? xin : (xper & xin)) : 0u;
+      pmask |= per << (r * G::V);
+    }
   }
   PERKS_DEVINL size_t off(const Dom3 &d) const { return (size_t)y * d.nx + x; }
 };
@@ -478,7 +505,11 @@ PERKS_DEVINL void send_face(const DistStep &ds, const Dom3 &d, const ThreadTile<
 // arrival one arrival ahead.
 constexpr int kTmemCode = 64;
 PERKS_DEVINL bool is_smem_code(int c) { return c >= 0 && c < kTmemCode; }
+#ifdef PERKS_DBG_NO_TMEM
+PERKS_DEVINL bool is_tmem_code(int) { return false; }
+#else
 PERKS_DEVINL bool is_tmem_code(int c) { return c >= kTmemCode; }
+#endif
 // Dynamic shared memory of the persistent 3D kernels: ring slots, 128 B of mbarriers and the TMEM
 // address, then (PERKS) nc cache slots and the CTA's cache-code map.  Every address is the
 // dynamic-smem base plus an offset (no pointer registers).
@@ -495,7 +526,7 @@ template <typename T, class G> struct CacheView {
   int kbase;       // arrival index of the current unit's first arrival within the step
   uint32_t tbase;  // TMEM address of cached plane 0 for this thread's warp (lane quarter + column)
   PERKS_DEVINL static T *cache() {
-    return reinterpret_cast<T *>(dyn_smem() + (size_t)G::NS * G::SLOT_BYTES + 128);
+    return reinterpret_cast<T *>(dyn_smem() + G::RING_BYTES);
   }
   PERKS_DEVINL T *slot(int c) const { return cache() + (size_t)c * G::SLOT; }
   PERKS_DEVINL signed char *cmap() const { return reinterpret_cast<signed char *>(cache() + (size_t)nc * G::SLOT); }
@@ -520,33 +551,18 @@ PERKS_DEVINL void read_own(const T *slot, T (&v)[G::R][G::V]) {
 }
 
 // Publish the tile-perimeter cells of cached plane o to dst (neighbours read them as halo): the
-// TB-boundary cells "continue to store and load from global memory".
+// TB-boundary cells "continue to store and load from global memory".  Threads without
+// perimeter cells (pmask == 0, most of the tile) skip it in one branch.
 template <typename T, class G>
-PERKS_DEVINL void publish_perimeter(T *__restrict__ dst, const Dom3 &d, int o, int x0, int y0,
+PERKS_DEVINL void publish_perimeter(T *__restrict__ dst, const Dom3 &d, const ThreadTile<G> &tt, int o,
                                     const T (&v)[G::R][G::V]) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int x = x0 + lane * G::V;
-  T *base = dst + (size_t)o * d.nx * d.ny;
-  const int xl = min(x0 + G::TX, d.nx) - 1;  // last tile column inside the domain
+  if (tt.pmask == 0) return;
+  T *base = dst + (size_t)o * d.nx * d.ny + (size_t)tt.y * d.nx + tt.x;
 #pragma unroll
-  for (int r = 0; r < G::R; r++) {
-    const int y = y0 + warp * G::R + r;
-    if (y >= d.ny) break;
-    const bool edge_row = (warp == 0 && r == 0) || (warp == G::NWARP - 1 && r == G::R - 1) ||
-                          y == d.ny - 1;
-    if (edge_row) {
+  for (int r = 0; r < G::R; r++)
 #pragma unroll
-      for (int i = 0; i < G::V; i++)
-        if (x + i < d.nx) base[(size_t)y * d.nx + x + i] = v[r][i];
-    } else {
-      if (lane == 0 && x < d.nx) base[(size_t)y * d.nx + x] = v[r][0];
-      if (xl >= x && xl < x + G::V) {
-#pragma unroll
-        for (int i = 0; i < G::V; i++)
-          if (x + i == xl) base[(size_t)y * d.nx + x + i] = v[r][i];
-      }
-    }
-  }
+    for (int i = 0; i < G::V; i++)
+      if ((tt.pmask >> (r * G::V + i)) & 1u) base[(size_t)r * d.nx + i] = v[r][i];
 }
 
 template <typename T, int S, class G, bool TMA, bool DIST>
@@ -751,6 +767,9 @@ PERKS_DEVINL void stream_unit_ws(WsPipe<T, G> &pp, const T *__restrict__ src, co
   const signed char *cmk = CACHE ? cv.cmap() + cv.kbase : nullptr;  // this unit's arrival codes
   auto cs = [&](int k) -> int {
     if constexpr (!CACHE) return -1;
+#ifdef PERKS_DBG_CS_NONE
+    return -1;
+#endif
     return (int)cmk[k];
   };
   pp.gk = k0 + narr;
@@ -778,42 +797,56 @@ PERKS_DEVINL void stream_unit_ws(WsPipe<T, G> &pp, const T *__restrict__ src, co
   tt.init(d, x0, y0);
   StreamState<T, G> st;
   st.zero();
+  // output plane o = zs, zs+1, ... in arrival order: the fast-path store pointer just advances
+  const size_t plane = (size_t)d.nx * d.ny;
+  T *sp = dst + (size_t)zs * plane + tt.off(d);
+  int slq = cs(0), slo = -1;  // cache codes of this arrival / of the output plane (rotated)
 #pragma unroll kWsUnroll  // (3: the accumulator rotation of arrival() becomes renaming)
   for (int k = 0; k < narr; k++) {
     const unsigned kk = k0 + k;
     const int q = q0 + k;
-    const int slq = cs(k);
+    const int sln = cs(k + 1);  // next arrival's code (sentinel -1 after the unit's last)
     pp.wait_full(kk);
     if (CACHE && is_tmem_code(slq)) pp.wait_staged(kk);
     T out[G::R][G::V], cq[G::R][G::V];
-    arrival<T, S, G>(st, (CACHE && is_smem_code(slq)) ? cv.slot(slq) : pp.slot(kk), c, out, cq);
+    {  // the plane's slot: a cache slot or the ring slot, as one offset from the dynamic-smem base
+      const size_t off = (CACHE && is_smem_code(slq)) ? G::RING_BYTES + (size_t)slq * G::SLOT_BYTES
+                                                       : (size_t)(kk % G::NS) * G::SLOT_BYTES;
+      arrival<T, S, G>(st, reinterpret_cast<const T *>(dyn_smem() + off), c, out, cq);
+    }
     pp.release(kk);
     if (q - 1 >= zs) {
       frame_select<T, G>(d, tt, q - 1, out, st.cm1);
-      const int slo = cs(k - 1);
       if (CACHE && is_smem_code(slo)) {
         // cached output: stays on chip once every warp has finished reading the old plane
-        publish_perimeter<T, G>(dst, d, q - 1, x0, y0, out);
+        publish_perimeter<T, G>(dst, d, tt, q - 1, out);
         pp.wait_released(kk - 1);
         write_own<T, G>(cv.slot(slo), out);
       } else if (CACHE && is_tmem_code(slo)) {
         // TMEM-cached output: the thread's own columns (plane q-1 was staged from them at
         // arrival q-2, before this write in program order)
-        publish_perimeter<T, G>(dst, d, q - 1, x0, y0, out);
+        publish_perimeter<T, G>(dst, d, tt, q - 1, out);
         TmemCells<T, G::R, G::V>::store(cv.tbase + (uint32_t)((slo - kTmemCode) * tmem_cpp<T, G>()), out);
       } else {
-        store_cells<T, G>(dst, d, tt, q - 1, out);
+        if (tt.full) {
+#pragma unroll
+          for (int r = 0; r < G::R; r++) vstore<T, G::V>(sp + (size_t)r * d.nx, out[r]);
+        } else {
+          store_cells<T, G>(dst, d, tt, q - 1, out);
+        }
         if constexpr (DIST) send_face_ws<T, G>(ds, d, tt, q - 1, x0, y0, out);
       }
+      sp += plane;
     }
 #pragma unroll
     for (int r = 0; r < G::R; r++)
 #pragma unroll
       for (int i = 0; i < G::V; i++) st.cm1[r][i] = cq[r][i];
+    slo = slq;
+    slq = sln;
     if constexpr (CACHE) {
       // TMEM tier: stage the NEXT arrival's cells (TMEM -> registers -> its ring slot) one
       // arrival ahead, at the point of the body with the fewest live registers
-      const int sln = cs(k + 1);  // (sentinel -1 after the unit's last arrival)
       if (is_tmem_code(sln)) {
         if (kk + 1 >= (unsigned)G::NS) pp.wait_released(kk + 1 - G::NS);  // slot free
         stage_tmem_plane<T, G>(pp, cv, kk + 1, sln - kTmemCode);

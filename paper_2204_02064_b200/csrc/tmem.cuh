@@ -42,28 +42,26 @@ PERKS_DEVINL void tmem_dealloc(uint32_t taddr, uint32_t ncols) {  // whole warp 
 PERKS_DEVINL void tmem_fence_before_sync() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 PERKS_DEVINL void tmem_fence_after_sync() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 PERKS_DEVINL void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
-PERKS_DEVINL void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+PERKS_DEVINL void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n"); }
 
-// 8 consecutive columns of this thread's lane (32x32b shape: thread i <-> lane base + i).
+// 8 consecutive columns of this thread's lane (32x32b shape: thread i <-> lane base + i).  TMEM is
+// invisible to the compiler's memory model: no "memory" clobber (asm volatile keeps the order of
+// the tcgen05 statements among themselves; the loaded registers are tied to the wait).
 PERKS_DEVINL void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(taddr),
-               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
-               : "memory");
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]));
 }
 PERKS_DEVINL void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "r"(taddr)
-               : "memory");
+               : "r"(taddr));
 }
 
 // tcgen05.wait::ld with the loaded registers as in/out operands (the load's destination registers
 // are undefined until the wait completes).
 PERKS_DEVINL void tmem_wait_ld_dep(uint32_t (&r)[8]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n"
-               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7])
-               :
-               : "memory");
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]));
 }
 
 // Words of a V x R cell block (V * sizeof(T) == 16 bytes per row).
