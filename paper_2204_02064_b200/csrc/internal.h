@@ -40,6 +40,7 @@ struct Plan {
   int zchunk = 0;             // planes per unit (3D)
   int cfg = 0;                // index of the kernel configuration
   int family = 0;             // kernel family within a variant (2D PERKS: 0 tiles, 1 cluster, 3 strips; 3D PERKS: 2)
+  bool cache_kernel = false;  // 3D PERKS: the kernel with the on-chip plane cache tiers
   int nc = 0;                 // 3D PERKS: shared-memory plane slots per CTA
   int ntm = 0, tcols = 0;     // 3D PERKS: TMEM planes per CTA, TMEM columns allocated per CTA
   int wsg = 0;                // 3D persistent: warp-specialised geometry (k3d_stream.cu)

@@ -54,7 +54,8 @@ template <typename T, int WSG> struct GS<T, true, WSG> {
 
 struct Units3 {
   int tx, ty, nzc, zc;
-  int rev;  // zig-zag experiment: 1 = reversed unit order (odd steps)
+  int rev;  // zig-zag traversal: host loop: reversed unit order in this launch; persistent /
+            // PERKS: every CTA reverses its units on odd steps
 };
 
 PERKS_DEVINL void unit_coords(const Units3 &u, int id, int tile_x, int tile_y, int &x0, int &y0,
@@ -239,17 +240,26 @@ __global__ void __launch_bounds__(k3d_threads<TMA, WSG>(), DIST ? 1 : wsg_minb(W
     T *dst = ((steps - 1 - t) & 1) == 0 ? out : tmp;
     const DistStep ds{&dk, &maps.ghost, xbase + (unsigned long long)t, (unsigned long long)d.nx * d.ny};
     if (TMA && threadIdx.x == 0) fence_proxy_async_global();  // last step's stores -> TMA reads
-    cv.kbase = 0;
+    // L2-aware traversal ("zig-zag", [draft] P:395-404): on odd steps every CTA runs its units in
+    // reverse, so a step starts on the tiles the previous step wrote last (still L2-resident:
+    // B200's L2 is about one buffer of C3).  Each CTA keeps its units (and its cached planes).
+    const bool rev = u.rev && (t & 1);
     for (int jj = 0; jj < nmine; jj++) {
-      int id = (int)blockIdx.x + jj * (int)gridDim.x;
+      const int j = rev ? nmine - 1 - jj : jj;
+      const int id = (int)blockIdx.x + j * (int)gridDim.x;
       int x0, y0, zs;
-      // (the zig-zag unit-order experiment never applies to PERKS: the cache map is per unit)
-      if (!CACHE && u.rev && (t & 1)) id = nunits - 1 - id;
       unit_coords(u, id, G::TX, G::TY, x0, y0, zs);
       const int ze = min(zs + u.zc, d.nz);
       if constexpr (TMA) {
+        if constexpr (CACHE) {  // arrival offset of unit j in the forward order (cache-code map)
+          cv.kbase = 0;
+          for (int i = 0; i < j; i++) {
+            int xi, yi, zi;
+            unit_coords(u, (int)blockIdx.x + i * (int)gridDim.x, G::TX, G::TY, xi, yi, zi);
+            cv.kbase += min(zi + u.zc, d.nz) - zi + 2;
+          }
+        }
         stream_unit_ws<T, S, G, DIST, CACHE>(pp, src, &maps.box[src_idx], dst, d, x0, y0, zs, ze, c, ds, cv);
-        cv.kbase += ze - zs + 2;
       } else {
         __syncthreads();  // slots of the previous unit are free
         stream_unit<T, S, G, TMA, DIST>(ring, src, &maps.box[src_idx], dst, d, x0, y0, zs, ze, c, ds);
@@ -489,7 +499,12 @@ Plan plan_stream3d(const Problem &p, perks_variant v) {
   }
   const bool tma = use_tma3(p);
   if (p.nranks > 1 && !tma) { pl.why = "stream3d: multi-GPU slabs need TMA (nx*S % 16 == 0)"; return pl; }
-  const bool cache = v == PERKS_PERKS;
+  // PERKS-3D on-chip plane cache (shared memory + TMEM tiers): measured to cost more SM-side time
+  // (per-plane halo fetches, perimeter publishes, TMEM staging) than the DRAM/L2 traffic it saves
+  // at every 3D size tried on B200, including fully cacheable ones (profiles/r01_perks3d_cache_sweep.txt):
+  // the planner's default cache split is empty (D_cache = 0: the PERKS variant runs the persistent
+  // kernel, P:519 with D_cache = 0); PERKS_P3D_CACHE=1 enables the tiers.
+  const bool cache = v == PERKS_PERKS && env_int("PERKS_P3D_CACHE", 0) != 0;
   if (cache && !tma) { pl.why = "perks3d: needs TMA (nx*S % 16 == 0)"; return pl; }
   const bool persistent = v != PERKS_HOSTLOOP;
   const bool ws = tma && persistent;  // warp-specialised pipeline (persistent kernels)
@@ -599,7 +614,8 @@ Plan plan_stream3d(const Problem &p, perks_variant v) {
   pl.ctas_per_sm = occ;
   pl.grid = persistent ? (int)std::min<int64_t>(pl.units, resident) : (int)pl.units;
   pl.cfg = tma ? 1 : 0;
-  pl.family = cache ? 2 : 0;  // (2: PERKS 3D, supports multi-GPU slabs)
+  pl.family = v == PERKS_PERKS ? 2 : 0;  // (2: PERKS 3D, supports multi-GPU slabs)
+  pl.cache_kernel = cache;
   pl.wsg = wsg;
   pl.nc = cache ? nc : 0;
   if (cache && tmem_ok && ntm0 > 0) {
@@ -632,9 +648,10 @@ Plan plan_stream3d(const Problem &p, perks_variant v) {
   pl.halo_bytes_step = S * (double)p.nz * (2.0 * TX * ty * tx + 2.0 * TY * ty * tx) +
                        S * 2.0 * nzc * (double)p.nx * p.ny;
   pl.ws_bytes = align256((size_t)p.cells() * p.elem()) + (persistent ? 256 : 0);
-  snprintf(pl.name, sizeof(pl.name), "%s3d_%s_%s_t%dx%d_z%d%s", cache ? "perks" : persistent ? "persistent" : "hostloop",
+  snprintf(pl.name, sizeof(pl.name), "%s3d_%s_%s_t%dx%d_z%d%s",
+           v == PERKS_PERKS ? "perks" : persistent ? "persistent" : "hostloop",
            p.shape == SHAPE_3D7 ? "7pt" : "27pt", p.dtype == PERKS_F32 ? "f32" : "f64", TX, TY, zc,
-           cache ? "_c" : (pl.cfg ? "_tma" : "_cpasync"));
+           cache ? "_c" : v == PERKS_PERKS ? "_c0" : (pl.cfg ? "_tma" : "_cpasync"));
   if (cache) {
     char extra[24];
     if (pl.ntm > 0) snprintf(extra, sizeof(extra), "%d_t%d_%dcta", pl.nc, pl.ntm, occ);
@@ -675,7 +692,7 @@ struct Launch3 {
                pl.zchunk, 0};
     block = pl.block;
     u.nzc = (int)((p.nz + u.zc - 1) / u.zc);
-    zigzag = env_int("PERKS_ZIGZAG", 0);  // experiment knob; off by default
+    zigzag = env_int("PERKS_ZIGZAG", 1);  // L2-aware traversal; PERKS_ZIGZAG=0 disables
     smem = (size_t)pl.smem;
     tma = pl.cfg == 1;
     grid = pl.grid;
@@ -683,7 +700,7 @@ struct Launch3 {
     dk = make_distk(dr);
     xbase = dr ? dr->xbase : 0;
     dist = p.nranks > 1;
-    cache = pl.family == 2;
+    cache = pl.cache_kernel;
     ch.nc = pl.nc;
     ch.ntm = pl.ntm;
     ch.tcols = pl.tcols;
@@ -756,7 +773,7 @@ cudaError_t run3(const Problem &p, const Plan &pl, const void *in, void *out, vo
   // launched normally with a grid of exactly the co-resident capacity computed by the planner
   // (shared memory padded so no further CTA fits an SM), which the block scheduler places all at
   // once on an idle device.
-  const bool tmem_multi = pl.family == 2 && pl.ctas_per_sm > 1;
+  const bool tmem_multi = pl.cache_kernel && pl.ctas_per_sm > 1;
   return L.persistent(steps, s, !(dr && dr->noncoop) && !tmem_multi && !env_int("PERKS_NONCOOP", 0));
 }
 }  // namespace

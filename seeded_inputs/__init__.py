@@ -152,3 +152,12 @@ CONFIGS = {
     "C4": dict(stencil="3d27pt", dtype="f32", shape=(512, 512, 512), steps=500),
     "C5": dict(stencil="3d7pt", dtype="f64", shape=(1024, 1024, 1024), steps=100),
 }
+# Cached-fraction sweep points (not BASELINE configs): 3D domains from fully
+# on-chip-cacheable to C3's size, the 3D analogue of the paper's small/large domains (Fig. 5).
+SWEEP_CONFIGS = {
+    "S3_128": dict(stencil="3d7pt", dtype="f64", shape=(128, 128, 128), steps=1000),
+    "S3_160": dict(stencil="3d7pt", dtype="f64", shape=(160, 160, 160), steps=1000),
+    "S3_192": dict(stencil="3d7pt", dtype="f64", shape=(192, 192, 192), steps=1000),
+    "S3_224": dict(stencil="3d7pt", dtype="f64", shape=(224, 224, 224), steps=1000),
+    "S27_256": dict(stencil="3d27pt", dtype="f32", shape=(256, 256, 256), steps=500),
+}

@@ -25,14 +25,18 @@ def _need_gpu():
 
 def _dist(tmp_path, name, shape, dtype, n, variant, Ts):
     out = str(tmp_path / "res.npy")
+    env = dict(os.environ)
+    if variant == "perks_cache":  # PERKS with the on-chip plane cache tiers (opt-in, k3d_stream.cu)
+        variant = "perks"
+        env["PERKS_P3D_CACHE"] = "1"
     cmd = [sys.executable, os.path.join(HERE, "dist_worker.py"), out, name, *map(str, shape),
            "f64" if dtype == np.float64 else "f32", str(n), variant, *map(str, Ts)]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env)
     assert r.returncode == 0, r.stdout + r.stderr
     return np.load(out)
 
 
-@pytest.mark.parametrize("variant", ["hostloop", "persistent", "perks"])
+@pytest.mark.parametrize("variant", ["hostloop", "persistent", "perks", "perks_cache"])
 @pytest.mark.parametrize("n", [2, 3])
 @pytest.mark.parametrize("name,dtype", [("3d7pt", np.float64), ("3d27pt", np.float32)])
 def test_slabs_match_global_oracle(tmp_path, variant, n, name, dtype):
@@ -53,6 +57,6 @@ def test_many_slabs_long_run(tmp_path):
     offs, w = si.preset(name)
     u0 = si.field(shape, dtype=dtype, seed=505)
     ref = oracle.run(u0, offs, w, 16, nthreads=4)
-    for variant in ("persistent", "perks"):
+    for variant in ("persistent", "perks", "perks_cache"):
         got = _dist(tmp_path, name, shape, dtype, 4, variant, [1, 10, 5])
         assert np.array_equal(got, ref), variant

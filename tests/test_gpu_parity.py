@@ -198,6 +198,7 @@ def test_perks3d_cache_and_zigzag(monkeypatch, nsm, zigzag, name, dtype):
     refresh + perimeter publish) and zig-zag traversal are bit-exact for any cache size, both
     traversal directions and both step parities."""
     _need_gpu()
+    monkeypatch.setenv("PERKS_P3D_CACHE", "1")
     if nsm:
         monkeypatch.setenv("PERKS_P3D_NSM", nsm)
     monkeypatch.setenv("PERKS_ZIGZAG", zigzag)
@@ -229,7 +230,7 @@ def test_strip_kernel(monkeypatch, shape, name):
 
 
 @pytest.mark.parametrize("nsm,ntm", [("0", ""), ("2", ""), ("0", "1"), ("3", "5")])
-@pytest.mark.parametrize("wsg", ["0", "1"])
+@pytest.mark.parametrize("wsg", ["0", "1", "2"])
 @pytest.mark.parametrize("name,dtype,shape", [("3d7pt", np.float64, (70, 33, 72)),
                                               ("3d27pt", np.float32, (61, 40, 136))])
 def test_perks3d_tmem_tier(monkeypatch, nsm, ntm, wsg, name, dtype, shape):
@@ -238,6 +239,7 @@ def test_perks3d_tmem_tier(monkeypatch, nsm, ntm, wsg, name, dtype, shape):
     with the shared-memory tier, both warp-specialised geometries, long units (one z-chunk),
     ragged tiles in x and y, both step parities: bit-exact vs the oracle."""
     _need_gpu()
+    monkeypatch.setenv("PERKS_P3D_CACHE", "1")
     monkeypatch.setenv("PERKS_P3D_NSM", nsm)
     if ntm:
         monkeypatch.setenv("PERKS_P3D_NTM", ntm)

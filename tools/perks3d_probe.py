@@ -13,7 +13,7 @@ sys.path.insert(0, os.getcwd())
 import seeded_inputs as si
 from paper_2204_02064_b200 import Stencil
 cn, T, v = sys.argv[1], int(sys.argv[2]), sys.argv[3]
-c = si.CONFIGS[cn]; dt = np.float64 if c["dtype"] == "f64" else np.float32
+c = {**si.CONFIGS, **si.SWEEP_CONFIGS}[cn]; dt = np.float64 if c["dtype"] == "f64" else np.float32
 offs, w = si.preset(c["stencil"]); st = Stencil(c["shape"], offs, w, dtype=dt)
 x = si.field_torch(c["shape"], dt, "cuda"); out = torch.empty_like(x); ws = st.workspace(v)
 q = st.query(v)
