@@ -194,7 +194,8 @@ def _traffic_from_profiles(kernel_prefix, config):
     try:
         d = json.load(open(p))
         e = d.get(config, {})
-        if e.get("kernel", "").startswith(kernel_prefix):
+        if e.get("plan_kernel") == kernel_prefix or (not e.get("plan_kernel") and
+                                                      e.get("kernel", "").startswith(kernel_prefix.split("_")[0])):
             return e.get("dram_bytes_per_launch")
     except Exception:
         pass
@@ -326,18 +327,20 @@ def run_mine(args):
                 "frac": achieved / peak, "peak_source": "derived: SMs x FMA/clk x 2 x sm_max_mhz"}
     else:
         # HBM bound: algorithmic bytes = model A_gm per launch (2·S·cells·T·(1-f) + 2·S·D_cache)
-        f = (q["cached_cells_reg"] + q["cached_cells_smem"]) / cells if q["variant"] == "perks" else 0.0
+        f = ((q["cached_cells_reg"] + q["cached_cells_smem"] + q["cached_cells_tmem"]) / cells
+             if q["variant"] == "perks" else 0.0)
         alg = (2.0 * S * cells * (1 - f) * T + 2.0 * S * cells * f) / max(1, launches_per_step)
         achieved = alg / (kern_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
-    roof["traffic"] = _traffic_from_profiles(q["kernel"].split("_")[0], args.config)
+    roof["traffic"] = _traffic_from_profiles(q["kernel"], args.config)
     roof["kernel"] = q["kernel"]
 
     eff_gbs = 2.0 * S * cells * T * args.steps * ws / (tot_ms * 1e-3) / 1e9
     from paper_2204_02064_b200 import model
 
-    cached = q["cached_cells_reg"] + q["cached_cells_smem"] if q["variant"] == "perks" else 0
+    cached = (q["cached_cells_reg"] + q["cached_cells_smem"] + q["cached_cells_tmem"]
+              if q["variant"] == "perks" else 0)
     proj = model.project(cells, min(cached, cells), T, S, peaks["hbm_gbs"] * 1e9,
                          A_halo=q["halo_bytes_per_step"] / S * T)
     line = {

@@ -6,7 +6,7 @@ import seeded_inputs as si
 from paper_2204_02064_b200 import Stencil
 cn, v = sys.argv[1], sys.argv[2]
 c = si.CONFIGS[cn]
-T = int(sys.argv[3]) if len(sys.argv) > 3 else c["steps"]
+T = int(sys.argv[3]) if len(sys.argv) > 3 and int(sys.argv[3]) > 0 else c["steps"]
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 2
 dt = np.float64 if c["dtype"] == "f64" else np.float32
 offs, w = si.preset(c["stencil"])
