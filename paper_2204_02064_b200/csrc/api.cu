@@ -101,6 +101,7 @@ int find_shape(int ndim, const int32_t *off, int n) {
   } else {
     if (match_shape<SHAPE_3D7>(off, n)) return SHAPE_3D7;
     if (match_shape<SHAPE_3D27>(off, n)) return SHAPE_3D27;
+    if (match_shape<SHAPE_3D19>(off, n)) return SHAPE_3D19;
   }
   return -1;
 }

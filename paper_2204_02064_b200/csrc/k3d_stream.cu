@@ -87,7 +87,7 @@ template <class G> PERKS_DEVINL uint64_t *ring_bars(unsigned char *smem) {
 template <bool TMA> constexpr bool host_ws() { return TMA && PERKS_S3D_HWS; }
 // host-loop CTAs per SM (launch bound): fp64 27pt needs more than 64 registers per thread
 template <typename T, int S, bool TMA, bool DIST> constexpr int hl_minb() {
-  return !(TMA && !DIST) ? 2 : (sizeof(T) == 8 && S == SHAPE_3D27) ? 3 : PERKS_S3D_MINB;
+  return !(TMA && !DIST) ? 2 : (sizeof(T) == 8 && S != SHAPE_3D7) ? 3 : PERKS_S3D_MINB;
 }
 template <bool WS, int WSG = 0> constexpr int k3d_threads() { return WS ? 32 * wsg_nwarp(WSG) + 32 : K3D_THREADS; }
 
@@ -415,7 +415,9 @@ template <typename T, int S> void *pk_s(bool tma, bool dist, bool cache, int wsg
   return cache ? pk_w<T, S, false, true>(wsg) : pk_w<T, S, false, false>(wsg);
 }
 template <typename T> void *pk(int shape, bool tma, bool dist, bool cache, int wsg) {
-  return shape == SHAPE_3D7 ? pk_s<T, SHAPE_3D7>(tma, dist, cache, wsg) : pk_s<T, SHAPE_3D27>(tma, dist, cache, wsg);
+  return shape == SHAPE_3D7    ? pk_s<T, SHAPE_3D7>(tma, dist, cache, wsg)
+         : shape == SHAPE_3D19 ? pk_s<T, SHAPE_3D19>(tma, dist, cache, wsg)
+                               : pk_s<T, SHAPE_3D27>(tma, dist, cache, wsg);
 }
 void *persist_ptr(const Problem &p, bool tma, bool cache, int wsg) {
   const bool dist = p.nranks > 1;
@@ -423,8 +425,9 @@ void *persist_ptr(const Problem &p, bool tma, bool cache, int wsg) {
 }
 template <typename T> void *kptr3d(int shape, bool persistent) {  // multi-GPU host-loop kernels (TMA)
   (void)persistent;
-  return shape == SHAPE_3D7 ? (void *)hostloop3d_kernel<T, SHAPE_3D7, true, true>
-                            : (void *)hostloop3d_kernel<T, SHAPE_3D27, true, true>;
+  return shape == SHAPE_3D7    ? (void *)hostloop3d_kernel<T, SHAPE_3D7, true, true>
+         : shape == SHAPE_3D19 ? (void *)hostloop3d_kernel<T, SHAPE_3D19, true, true>
+                               : (void *)hostloop3d_kernel<T, SHAPE_3D27, true, true>;
 }
 template <typename T> void *kptr3(int shape, bool persistent, bool tma) {
 #define K3(S)                                                                                   \
@@ -434,6 +437,7 @@ template <typename T> void *kptr3(int shape, bool persistent, bool tma) {
   }
   K3(SHAPE_3D7)
   K3(SHAPE_3D27)
+  K3(SHAPE_3D19)
 #undef K3
   return nullptr;
 }
@@ -493,8 +497,9 @@ int occupancy_ignoring_tmem(const Problem &p, const cudaFuncAttributes &fa, int 
 Plan plan_stream3d(const Problem &p, perks_variant v) {
   Plan pl;
   pl.variant = v;
-  if (p.ndim != 3 || (p.shape != SHAPE_3D7 && p.shape != SHAPE_3D27) || p.bc != PERKS_BC_FRAME) {
-    pl.why = "stream3d: needs 3D 7pt/27pt FRAME";
+  if (p.ndim != 3 || (p.shape != SHAPE_3D7 && p.shape != SHAPE_3D27 && p.shape != SHAPE_3D19) ||
+      p.bc != PERKS_BC_FRAME) {
+    pl.why = "stream3d: needs 3D 7pt/19pt/27pt FRAME";
     return pl;
   }
   const bool tma = use_tma3(p);
@@ -650,7 +655,7 @@ Plan plan_stream3d(const Problem &p, perks_variant v) {
   pl.ws_bytes = align256((size_t)p.cells() * p.elem()) + (persistent ? 256 : 0);
   snprintf(pl.name, sizeof(pl.name), "%s3d_%s_%s_t%dx%d_z%d%s",
            v == PERKS_PERKS ? "perks" : persistent ? "persistent" : "hostloop",
-           p.shape == SHAPE_3D7 ? "7pt" : "27pt", p.dtype == PERKS_F32 ? "f32" : "f64", TX, TY, zc,
+           p.shape == SHAPE_3D7 ? "7pt" : p.shape == SHAPE_3D19 ? "19pt" : "27pt", p.dtype == PERKS_F32 ? "f32" : "f64", TX, TY, zc,
            cache ? "_c" : v == PERKS_PERKS ? "_c0" : (pl.cfg ? "_tma" : "_cpasync"));
   if (cache) {
     char extra[24];
@@ -781,10 +786,12 @@ cudaError_t run3(const Problem &p, const Plan &pl, const void *in, void *out, vo
 cudaError_t run_stream3d(const Problem &p, const Plan &pl, const void *in, void *out, void *ws,
                          int64_t steps, cudaStream_t s, const DistRun *dr) {
   if (p.dtype == PERKS_F32)
-    return p.shape == SHAPE_3D7 ? run3<float, SHAPE_3D7>(p, pl, in, out, ws, steps, s, dr)
-                                : run3<float, SHAPE_3D27>(p, pl, in, out, ws, steps, s, dr);
-  return p.shape == SHAPE_3D7 ? run3<double, SHAPE_3D7>(p, pl, in, out, ws, steps, s, dr)
-                              : run3<double, SHAPE_3D27>(p, pl, in, out, ws, steps, s, dr);
+    return p.shape == SHAPE_3D7    ? run3<float, SHAPE_3D7>(p, pl, in, out, ws, steps, s, dr)
+           : p.shape == SHAPE_3D19 ? run3<float, SHAPE_3D19>(p, pl, in, out, ws, steps, s, dr)
+                                   : run3<float, SHAPE_3D27>(p, pl, in, out, ws, steps, s, dr);
+  return p.shape == SHAPE_3D7    ? run3<double, SHAPE_3D7>(p, pl, in, out, ws, steps, s, dr)
+         : p.shape == SHAPE_3D19 ? run3<double, SHAPE_3D19>(p, pl, in, out, ws, steps, s, dr)
+                                 : run3<double, SHAPE_3D27>(p, pl, in, out, ws, steps, s, dr);
 }
 
 namespace {
@@ -817,10 +824,12 @@ cudaError_t run_stream3d_hostloop_group(const Problem *const *ps, const Plan *co
                                         const DistRun *drs, int n, int64_t steps, cudaStream_t s) {
   const Problem &p = *ps[0];
   if (p.dtype == PERKS_F32)
-    return p.shape == SHAPE_3D7 ? group3<float, SHAPE_3D7>(ps, pls, in, out, ws, drs, n, steps, s)
-                                : group3<float, SHAPE_3D27>(ps, pls, in, out, ws, drs, n, steps, s);
-  return p.shape == SHAPE_3D7 ? group3<double, SHAPE_3D7>(ps, pls, in, out, ws, drs, n, steps, s)
-                              : group3<double, SHAPE_3D27>(ps, pls, in, out, ws, drs, n, steps, s);
+    return p.shape == SHAPE_3D7    ? group3<float, SHAPE_3D7>(ps, pls, in, out, ws, drs, n, steps, s)
+           : p.shape == SHAPE_3D19 ? group3<float, SHAPE_3D19>(ps, pls, in, out, ws, drs, n, steps, s)
+                                   : group3<float, SHAPE_3D27>(ps, pls, in, out, ws, drs, n, steps, s);
+  return p.shape == SHAPE_3D7    ? group3<double, SHAPE_3D7>(ps, pls, in, out, ws, drs, n, steps, s)
+         : p.shape == SHAPE_3D19 ? group3<double, SHAPE_3D19>(ps, pls, in, out, ws, drs, n, steps, s)
+                                 : group3<double, SHAPE_3D27>(ps, pls, in, out, ws, drs, n, steps, s);
 }
 
 }  // namespace perks

@@ -6,6 +6,8 @@
 //   SHAPE_2D9  2d9pt  box  r=1: (dy,dx) lexicographic ascending
 //   SHAPE_3D7  3d7pt  star r=1: W,E,S,C,N,B,F
 //   SHAPE_3D27 3d27pt box  r=1: (dz,dy,dx) lexicographic ascending
+//   SHAPE_3D19 poisson 19pt r=1 (Table II "poisson(1,38)"): the 3x3x3 cube without its 8 corners,
+//              (dz,dy,dx) lexicographic ascending (reading R3b)
 //
 // The host matches a descriptor's (offset list, order) against these tables exactly; any other
 // list is PERKS_ERR_UNSUPPORTED (the kernels follow the list order, so bit-exactness holds).
@@ -14,7 +16,7 @@
 
 namespace perks {
 
-enum ShapeId : int { SHAPE_2D5 = 0, SHAPE_2D9 = 1, SHAPE_3D7 = 2, SHAPE_3D27 = 3, SHAPE_COUNT = 4 };
+enum ShapeId : int { SHAPE_2D5 = 0, SHAPE_2D9 = 1, SHAPE_3D7 = 2, SHAPE_3D27 = 3, SHAPE_3D19 = 4, SHAPE_COUNT = 5 };
 
 template <int S> struct Shape;
 
@@ -41,6 +43,19 @@ template <> struct Shape<SHAPE_3D27> {
   static constexpr __host__ __device__ int dx(int p) { return p % 3 - 1; }
   static constexpr __host__ __device__ int dy(int p) { return (p / 3) % 3 - 1; }
   static constexpr __host__ __device__ int dz(int p) { return p / 9 - 1; }
+};
+
+// 3d19pt: the p-th non-corner point of the 3x3x3 cube in (dz,dy,dx) lexicographic order, as cube
+// index c = (dz+1)*9 + (dy+1)*3 + (dx+1) (a literal table: folds at every unrolled use).
+template <> struct Shape<SHAPE_3D19> {
+  static constexpr int N = 19, NDIM = 3;
+  static constexpr __host__ __device__ int cube(int p) {
+    constexpr int c[19] = {1, 3, 4, 5, 7, 9, 10, 11, 12, 13, 14, 15, 16, 17, 19, 21, 22, 23, 25};
+    return c[p];
+  }
+  static constexpr __host__ __device__ int dx(int p) { return cube(p) % 3 - 1; }
+  static constexpr __host__ __device__ int dy(int p) { return (cube(p) / 3) % 3 - 1; }
+  static constexpr __host__ __device__ int dz(int p) { return cube(p) / 9 - 1; }
 };
 
 // Does the in-plane part of the shape touch corners (|dx| and |dy| both nonzero)?
@@ -94,5 +109,6 @@ static_assert(streamable<SHAPE_2D5>(), "2d5pt order not streamable");
 static_assert(streamable<SHAPE_2D9>(), "2d9pt order not streamable");
 static_assert(streamable<SHAPE_3D7>(), "3d7pt order not streamable");
 static_assert(streamable<SHAPE_3D27>(), "3d27pt order not streamable");
+static_assert(streamable<SHAPE_3D19>(), "3d19pt order not streamable");
 
 }  // namespace perks

@@ -126,12 +126,24 @@ def preset(name: str):
                 for dx in (-1, 0, 1):
                     offs.append((dx, dy, dz))
                     w.append((2 - abs(dx)) * (2 - abs(dy)) * (2 - abs(dz)) / 64)
+    elif name == "3d19pt":
+        # Table II "poisson(1,38)": 19 points = the 3x3x3 cube without its 8 corners (reading
+        # R3b); dyadic convex weights C=1/4, faces 1/16, edges 1/32 (sum exactly 1)
+        offs, w = [], []
+        for dz in (-1, 0, 1):
+            for dy in (-1, 0, 1):
+                for dx in (-1, 0, 1):
+                    m = abs(dx) + abs(dy) + abs(dz)
+                    if m == 3:
+                        continue
+                    offs.append((dx, dy, dz))
+                    w.append({0: 1 / 4, 1: 1 / 16, 2: 1 / 32}[m])
     else:
         raise KeyError(name)
     return offs, w
 
 
-PRESET_NDIM = {"2d5pt": 2, "2d9pt": 2, "3d7pt": 3, "3d27pt": 3}
+PRESET_NDIM = {"2d5pt": 2, "2d9pt": 2, "3d7pt": 3, "3d27pt": 3, "3d19pt": 3}
 
 
 def random_convex_weights(npts: int, dtype=np.float64, seed: int = 7) -> list[float]:

@@ -74,7 +74,7 @@ def test_parity_2d(variant, dtype, name, shape):
 
 @pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
-@pytest.mark.parametrize("name", ["3d7pt", "3d27pt"])
+@pytest.mark.parametrize("name", ["3d7pt", "3d27pt", "3d19pt"])
 @pytest.mark.parametrize("shape", CASES_3D)
 def test_parity_3d(variant, dtype, name, shape):
     _need_gpu()
@@ -93,7 +93,8 @@ def test_parity_3d(variant, dtype, name, shape):
 
 @pytest.mark.parametrize("name,shape,dtype", [
     ("2d9pt", (300, 520), np.float32), ("2d5pt", (128, 128), np.float64),
-    ("3d7pt", (24, 40, 64), np.float64), ("3d27pt", (20, 36, 128), np.float32)])
+    ("3d7pt", (24, 40, 64), np.float64), ("3d27pt", (20, 36, 128), np.float32),
+    ("3d19pt", (22, 30, 72), np.float64), ("3d19pt", (18, 33, 136), np.float32)])
 def test_random_weights_and_cross_variant(name, shape, dtype):
     """Non-symmetric random weights; all variants bit-identical to each other and the oracle."""
     _need_gpu()

@@ -75,7 +75,7 @@ def test_shift_closed_form(dtype, axis, sign):
 # ------------------------------------------------------------ constant fixed point
 
 @pytest.mark.parametrize("dtype", DT)
-@pytest.mark.parametrize("name", ["2d5pt", "2d9pt", "3d7pt", "3d27pt"])
+@pytest.mark.parametrize("name", ["2d5pt", "2d9pt", "3d7pt", "3d27pt", "3d19pt"])
 @pytest.mark.parametrize("bc", [oracle.BC_FRAME, oracle.BC_PERIODIC])
 def test_constant_preserved(dtype, name, bc):
     """Dyadic presets sum to exactly 1 -> a constant field is a fixed point."""
@@ -94,7 +94,7 @@ def _lambda_hat(offs, w, k):
                for d, wp in zip(offs, w))
 
 
-@pytest.mark.parametrize("name", ["2d5pt", "2d9pt", "3d7pt", "3d27pt", "rand2d", "rand3d"])
+@pytest.mark.parametrize("name", ["2d5pt", "2d9pt", "3d7pt", "3d27pt", "3d19pt", "rand2d", "rand3d"])
 def test_fourier_mode_decay(name):
     """PERIODIC: u0 = c0 + A·cos(k·x) -> u_T = c0·(Σw)^T + A·Re(λ̂(k)^T e^{ik·x}),
     λ̂(k) = Σ_p w_p e^{i k·d_p}.  Non-symmetric random weights make λ̂ complex, which
@@ -209,7 +209,7 @@ def test_linearity(dtype):
 
 
 @pytest.mark.parametrize("dtype", DT)
-@pytest.mark.parametrize("name", ["2d5pt", "2d9pt", "3d7pt", "3d27pt"])
+@pytest.mark.parametrize("name", ["2d5pt", "2d9pt", "3d7pt", "3d27pt", "3d19pt"])
 def test_composability(dtype, name):
     """run(T1) then run(T2) == run(T1+T2) bit-exact (the iteration is Markov)."""
     offs, w = si.preset(name)
