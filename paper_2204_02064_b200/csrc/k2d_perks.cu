@@ -50,14 +50,7 @@ PERKS_DEVINL void poll_copy(const LLWord *src, int n, unsigned tag, bool exists,
     for (int i = lane; i < n; i += 32) dst[i] = T(0);
     return;
   }
-#ifdef PERKS_DBG_NOPOLL  // timing experiment only (wrong results): no wait for the neighbours' tags
-  for (int i = lane; i < n; i += 32) {
-    T v;
-    LL<T>::get(src + i * W, tag, v);
-    dst[i] = v;
-  }
-  return;
-#endif
+
   T val[E];
   unsigned pending = 0;
 #pragma unroll
@@ -156,6 +149,8 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
         for (int i = 0; i < V; i++) LL<T>::put(g + (TX + xr + i) * W, v[i], tag);
       }
     }
+    // branch-free: lanes without a column-buffer cell store to a scratch word (predicated
+    // stores measured 30 % slower: 11.9 vs 9.1 us/step on C2)
     sm[(is_l ? pc : 0) + o_colL + o_colL_step * r] = v[0];
     sm[(is_r ? pc : 0) + o_colR + o_colR_step * r] = v[V - 1];
     if (g_l) LL<T>::put(g + (2 * TX + yr0 + r) * W, v[0], tag);
@@ -220,13 +215,9 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
           const bool cex = cx >= 0 && cx < tl.ntx && nty >= 0 && nty < tl.nty;
           const LLWord *cs = GS(cex ? nty * tl.ntx + cx : 0, par) + ((side == 0 ? TX : 0) + (lane == 0 ? TX - 1 : 0)) * W;
           T val = T(0);
-#ifdef PERKS_DBG_NOPOLL
-          if (cex) LL<T>::get(cs, tag_in, val);
-#else
           if (cex)
             while (!LL<T>::get(cs, tag_in, val)) {
             }
-#endif
           sm[dst + (lane == 0 ? 0 : TX + 1)] = val;
         }
       } else {

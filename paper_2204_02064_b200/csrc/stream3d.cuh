@@ -505,11 +505,7 @@ PERKS_DEVINL void send_face(const DistStep &ds, const Dom3 &d, const ThreadTile<
 // arrival one arrival ahead.
 constexpr int kTmemCode = 64;
 PERKS_DEVINL bool is_smem_code(int c) { return c >= 0 && c < kTmemCode; }
-#ifdef PERKS_DBG_NO_TMEM
-PERKS_DEVINL bool is_tmem_code(int) { return false; }
-#else
 PERKS_DEVINL bool is_tmem_code(int c) { return c >= kTmemCode; }
-#endif
 // Dynamic shared memory of the persistent 3D kernels: ring slots, 128 B of mbarriers and the TMEM
 // address, then (PERKS) nc cache slots and the CTA's cache-code map.  Every address is the
 // dynamic-smem base plus an offset (no pointer registers).
@@ -767,9 +763,6 @@ PERKS_DEVINL void stream_unit_ws(WsPipe<T, G> &pp, const T *__restrict__ src, co
   const signed char *cmk = CACHE ? cv.cmap() + cv.kbase : nullptr;  // this unit's arrival codes
   auto cs = [&](int k) -> int {
     if constexpr (!CACHE) return -1;
-#ifdef PERKS_DBG_CS_NONE
-    return -1;
-#endif
     return (int)cmk[k];
   };
   pp.gk = k0 + narr;
