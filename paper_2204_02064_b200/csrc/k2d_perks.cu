@@ -378,12 +378,21 @@ namespace {
 #define PERKS_P2F_V 4
 #endif
 using P2F_A = Geo2P<float, PERKS_P2F_V, 8 / PERKS_P2F_V, PERKS_P2F_WY, PERKS_P2F_RR, PERKS_P2F_RS>;   // default 256 x 256 tile, 256 thr, 64 KiB regs + 192 KiB smem
+// Tile configurations, largest first; the planner takes the SMALLEST tile whose count still fits one
+// CTA per SM, so mid-size domains use (nearly) every SM instead of a few large tiles
+// (profiles/r01_sweep2d.txt: 2048^2 on 64 tiles of 256^2 ran slower than the persistent kernel).
+using P2F_A2 = Geo2P<float, 4, 2, 4, 16, 32>;  // 256 x 192 tile, 256 thr
+using P2F_A3 = Geo2P<float, 4, 2, 4, 16, 16>;  // 256 x 128 tile, 256 thr
 using P2F_B = Geo2P<float, 4, 1, 8, 8, 8>;     // 128 x 128 tile, 256 thr
+using P2F_B2 = Geo2P<float, 4, 1, 8, 8, 0>;    // 128 x  64 tile, 256 thr
 using P2F_C = Geo2P<float, 4, 1, 4, 8, 0>;     // 128 x  32 tile, 128 thr
 using P2D_A = Geo2P<double, 2, 2, 4, 16, 16>;  // 128 x 128 tile, 256 thr, 64 KiB regs + 64 KiB smem
+using P2D_A2 = Geo2P<double, 2, 2, 4, 16, 8>;  // 128 x  96 tile, 256 thr
+using P2D_A3 = Geo2P<double, 2, 2, 4, 16, 0>;  // 128 x  64 tile, 256 thr
 using P2D_B = Geo2P<double, 2, 2, 4, 8, 0>;    // 128 x  32 tile, 256 thr
 using P2D_C = Geo2P<double, 2, 1, 2, 8, 0>;    //  64 x  16 tile,  64 thr
-constexpr int NCFG = 3;
+constexpr int NCFG_F = 6, NCFG_D = 5;
+int ncfg(const Problem &p) { return p.dtype == PERKS_F32 ? NCFG_F : NCFG_D; }
 
 struct CfgInfo {
   void *k;
@@ -397,18 +406,29 @@ template <typename T, int S, class G> CfgInfo info() {
                  (int64_t)G::RR * G::V * G::NT, (int64_t)G::RS * G::V * G::NT};
 }
 template <typename T, int S> CfgInfo info_t(int cfg);
-template <> CfgInfo info_t<float, SHAPE_2D5>(int c) {
-  return c == 0 ? info<float, SHAPE_2D5, P2F_A>() : c == 1 ? info<float, SHAPE_2D5, P2F_B>() : info<float, SHAPE_2D5, P2F_C>();
+template <int S> CfgInfo info_f(int c) {
+  switch (c) {
+    case 0: return info<float, S, P2F_A>();
+    case 1: return info<float, S, P2F_A2>();
+    case 2: return info<float, S, P2F_A3>();
+    case 3: return info<float, S, P2F_B>();
+    case 4: return info<float, S, P2F_B2>();
+    default: return info<float, S, P2F_C>();
+  }
 }
-template <> CfgInfo info_t<float, SHAPE_2D9>(int c) {
-  return c == 0 ? info<float, SHAPE_2D9, P2F_A>() : c == 1 ? info<float, SHAPE_2D9, P2F_B>() : info<float, SHAPE_2D9, P2F_C>();
+template <int S> CfgInfo info_d(int c) {
+  switch (c) {
+    case 0: return info<double, S, P2D_A>();
+    case 1: return info<double, S, P2D_A2>();
+    case 2: return info<double, S, P2D_A3>();
+    case 3: return info<double, S, P2D_B>();
+    default: return info<double, S, P2D_C>();
+  }
 }
-template <> CfgInfo info_t<double, SHAPE_2D5>(int c) {
-  return c == 0 ? info<double, SHAPE_2D5, P2D_A>() : c == 1 ? info<double, SHAPE_2D5, P2D_B>() : info<double, SHAPE_2D5, P2D_C>();
-}
-template <> CfgInfo info_t<double, SHAPE_2D9>(int c) {
-  return c == 0 ? info<double, SHAPE_2D9, P2D_A>() : c == 1 ? info<double, SHAPE_2D9, P2D_B>() : info<double, SHAPE_2D9, P2D_C>();
-}
+template <> CfgInfo info_t<float, SHAPE_2D5>(int c) { return info_f<SHAPE_2D5>(c); }
+template <> CfgInfo info_t<float, SHAPE_2D9>(int c) { return info_f<SHAPE_2D9>(c); }
+template <> CfgInfo info_t<double, SHAPE_2D5>(int c) { return info_d<SHAPE_2D5>(c); }
+template <> CfgInfo info_t<double, SHAPE_2D9>(int c) { return info_d<SHAPE_2D9>(c); }
 CfgInfo cfg_info(const Problem &p, int cfg) {
   if (p.dtype == PERKS_F32) return p.shape == SHAPE_2D5 ? info_t<float, SHAPE_2D5>(cfg) : info_t<float, SHAPE_2D9>(cfg);
   return p.shape == SHAPE_2D5 ? info_t<double, SHAPE_2D5>(cfg) : info_t<double, SHAPE_2D9>(cfg);
@@ -428,6 +448,7 @@ Plan plan_perks2d(const Problem &p) {
   // fits one CTA per SM (all CTAs co-resident; minimal occupancy).
   int forced = env_int("PERKS_P2D_CFG", -1);
   int best = -1;
+  const int NCFG = ncfg(p);
   for (int cfg = NCFG - 1; cfg >= 0 && forced < 0; cfg--) {
     CfgInfo ci = cfg_info(p, cfg);
     if (p.nx <= ci.TX && p.ny <= ci.TY && ci.smem <= (size_t)p.max_smem_optin) { best = cfg; break; }

@@ -172,4 +172,12 @@ SWEEP_CONFIGS = {
     "S3_192": dict(stencil="3d7pt", dtype="f64", shape=(192, 192, 192), steps=1000),
     "S3_224": dict(stencil="3d7pt", dtype="f64", shape=(224, 224, 224), steps=1000),
     "S27_256": dict(stencil="3d27pt", dtype="f32", shape=(256, 256, 256), steps=500),
+    # 2D domain sweep (C2's stencil): from one cluster to the full on-chip capacity
+    "S2_256": dict(stencil="2d9pt", dtype="f32", shape=(256, 256), steps=1000),
+    "S2_512": dict(stencil="2d9pt", dtype="f32", shape=(512, 512), steps=1000),
+    "S2_1024": dict(stencil="2d9pt", dtype="f32", shape=(1024, 1024), steps=1000),
+    "S2_2048": dict(stencil="2d9pt", dtype="f32", shape=(2048, 2048), steps=1000),
+    "S2_2560": dict(stencil="2d9pt", dtype="f32", shape=(2560, 2560), steps=1000),
+    "S2d_1024": dict(stencil="2d5pt", dtype="f64", shape=(1024, 1024), steps=1000),
+    "S2d_1536": dict(stencil="2d5pt", dtype="f64", shape=(1536, 1536), steps=1000),
 }

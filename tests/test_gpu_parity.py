@@ -256,3 +256,28 @@ def test_perks3d_tmem_tier(monkeypatch, nsm, ntm, wsg, name, dtype, shape):
     for T in (1, 4, 7):
         ref = oracle.run(u0, offs, w, T, nthreads=8)
         _check(_run_gpu(u0, name, w, T, "perks"), ref, u0, dtype)
+
+
+TILE_CFGS = {np.float32: [(256, 256), (256, 192), (256, 128), (128, 128), (128, 64), (128, 32)],
+             np.float64: [(128, 128), (128, 96), (128, 64), (128, 32), (64, 16)]}
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("name", ["2d5pt", "2d9pt"])
+def test_perks2d_every_tile_config(monkeypatch, dtype, name):
+    """Every PERKS-2D tile configuration (k2d_perks.cu, forced with PERKS_P2D_CFG) on a domain of
+    2.5 x 1.5 tiles (ragged in x and y, several CTAs exchanging edges), bit-exact vs the oracle."""
+    _need_gpu()
+    from paper_2204_02064_b200 import Stencil
+    offs, w = si.preset(name)
+    for cfg, (tx, ty) in enumerate(TILE_CFGS[dtype]):
+        monkeypatch.setenv("PERKS_P2D_CFG", str(cfg))
+        shape = (ty + ty // 2 + 3, 2 * tx + tx // 2 + 4)  # (ny, nx)
+        st = Stencil(shape, offs, w, dtype=dtype)
+        q = st.query("perks")
+        st.close()
+        assert q["kernel"].startswith("perks2d_") and f"_t{tx}x{ty}" in q["kernel"], (cfg, q["kernel"])
+        u0 = si.field(shape, dtype=dtype, seed=909 + cfg)
+        for T in (1, 6):
+            ref = oracle.run(u0, offs, w, T, nthreads=8)
+            _check(_run_gpu(u0, name, w, T, "perks"), ref, u0, dtype)
