@@ -24,12 +24,21 @@
 #include "common.cuh"
 #include "internal.h"
 #include "shapes.cuh"
+#include "tmem.cuh"
 
 namespace perks {
 
-template <typename T, int V_, int WX_, int WY_, int RR_, int RS_>
+// RR rows per thread in registers, RT rows in Tensor Memory (tmem.cuh: each thread's rows in its own
+// TMEM lane, 4 columns per row — a register-file extension, sm_100a), RS rows in shared memory.
+template <typename T, int V_, int WX_, int WY_, int RR_, int RS_, int RT_ = 0>
 struct Geo2P {
-  static constexpr int V = V_, WX = WX_, WY = WY_, RR = RR_, RS = RS_, R = RR_ + RS_;
+  static constexpr int V = V_, WX = WX_, WY = WY_, RR = RR_, RS = RS_, RT = RT_, R = RR_ + RT_ + RS_;
+  static constexpr int RS0 = RR + RT;  // first shared-memory row
+  // TMEM columns per CTA: warps sharing a lane quarter take consecutive column groups
+  static constexpr int TCOLS_RAW = RT * 4 * ((WX * WY + 3) / 4);
+  static constexpr int TCOLS = TCOLS_RAW == 0 ? 0 : TCOLS_RAW <= 32 ? 32 : TCOLS_RAW <= 64 ? 64
+                               : TCOLS_RAW <= 128 ? 128 : TCOLS_RAW <= 256 ? 256 : 512;
+  static_assert(TCOLS_RAW <= 512, "TMEM rows exceed 512 columns");
   static constexpr int NT = 32 * WX * WY;
   static constexpr int TX = 32 * V * WX, TY = WY * R;
   static constexpr int ROWW = TX + 2;  // x = -1 .. TX
@@ -83,7 +92,7 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
                                                            int nx, int ny,
                                                            Tiles2 tl, int64_t steps,
                                                            Coef<T, Shape<S>::N> c) {
-  constexpr int V = G::V, R = G::R, RR = G::RR, NT = G::NT, TX = G::TX, TY = G::TY;
+  constexpr int V = G::V, R = G::R, RR = G::RR, RT = G::RT, RS0 = G::RS0, NT = G::NT, TX = G::TX, TY = G::TY;
   constexpr int WX = G::WX, WY = G::WY, ROWW = G::ROWW, NWARP = NT / 32;
   constexpr bool BOX = has_corners<S>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -157,6 +166,21 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
     if (g_r) LL<T>::put(g + (2 * TX + TY + yr0 + r) * W, v[V - 1], tag);
   };
 
+  // ---- TMEM rows: one warp allocates, every CTA relinquishes its permit (tmem.cuh)
+  __shared__ uint32_t tmem_base_slot;
+  uint32_t tb = 0;  // this thread's TMEM row 0 (lane quarter of its warp + the warp's column group)
+  if constexpr (RT > 0) {
+    if (warp == 0) {
+      tmem_alloc(&tmem_base_slot, (uint32_t)G::TCOLS);
+      tmem_relinquish();
+    }
+    tmem_fence_before_sync();
+    __syncthreads();
+    tmem_fence_after_sync();
+    tb = tmem_base_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * RT * 4);
+  }
+  auto trow = [&](int r) { return tb + (uint32_t)((r - RR) * 4); };  // TMEM address of row r
+
   // ---- prologue: load the tile into the caches (P:519 the one-time 2·D_cache term, load half)
   T reg[RR > 0 ? RR : 1][V];
   auto load_row = [&](int r, T (&v)[V]) {
@@ -175,11 +199,19 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
       for (int i = 0; i < V; i++) reg[r][i] = v[i];
       publish_row(0, g0, 1u, r, v);
     }
-#pragma unroll 1
-    for (int r = RR; r < R; r++) {
+#pragma unroll
+    for (int r = RR; r < RS0; r++) {
       T v[V];
       load_row(r, v);
-      vstore<T, V>(my_smc + (size_t)(r - RR) * NT * V, v);
+      tmem_st_row<T, V>(trow(r), v);
+      publish_row(0, g0, 1u, r, v);
+    }
+    if constexpr (RT > 0) tmem_wait_st();
+#pragma unroll 1
+    for (int r = RS0; r < R; r++) {
+      T v[V];
+      load_row(r, v);
+      vstore<T, V>(my_smc + (size_t)(r - RS0) * NT * V, v);
       publish_row(0, g0, 1u, r, v);
     }
   }
@@ -290,11 +322,27 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
       if (RR > 0) {
 #pragma unroll
         for (int i = 0; i < V; i++) v[i] = opaque_copy(reg[0][i]);
+      } else if (RT > 0) {
+        tmem_ld_row<T, V>(trow(0), v);
       } else {
         vload<T, V>(v, my_smc);
       }
       widen(cur, v, 0);
     }
+    // the first row of the next tier (TMEM, then shared memory) or the halo below
+    auto next_tier_row = [&](int rn) {
+      if (RT > 0 && rn < RS0) {
+        T v[V];
+        tmem_ld_row<T, V>(trow(rn), v);
+        widen(nxt, v, rn);
+      } else if (RS0 < R) {
+        T v[V];
+        vload<T, V>(v, my_smc + (size_t)(rn - RS0) * NT * V);
+        widen(nxt, v, rn);
+      } else {
+        halo_below(nxt);
+      }
+    };
     // rows held in registers: fully unrolled so reg[][] is statically indexed
 #pragma unroll
     for (int r = 0; r < RR; r++) {
@@ -303,34 +351,40 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
 #pragma unroll
         for (int i = 0; i < V; i++) v[i] = opaque_copy(reg[r + 1 < RR ? r + 1 : 0][i]);
         widen(nxt, v, r + 1);
-      } else if (RR < R) {
-        T v[V];
-        vload<T, V>(v, my_smc);  // first shared-memory row
-        widen(nxt, v, r + 1);
       } else {
-        halo_below(nxt);
+        next_tier_row(r + 1);
       }
       T nv[V];
       finish_row(r, nv);
 #pragma unroll
       for (int i = 0; i < V; i++) reg[r][i] = nv[i];
     }
+    // rows held in TMEM: fully unrolled (compile-time column offsets); row r's old values are no
+    // longer needed once row r+1 is in the window, so its new values go straight back
+#pragma unroll
+    for (int r = RR; r < RS0; r++) {
+      next_tier_row(r + 1);
+      T nv[V];
+      finish_row(r, nv);
+      tmem_st_row<T, V>(trow(r), nv);
+    }
+    if constexpr (RT > 0) tmem_wait_st();
     // rows held in shared memory (sm_cache); unrolled by 3 = the window period; the last row
     // (which reads the row below the segment) is peeled so the loop body has no row tests
-    if (RR < R) {
+    if (RS0 < R) {
 #pragma unroll 3
-      for (int r = RR; r < R - 1; r++) {
+      for (int r = RS0; r < R - 1; r++) {
         T v[V];
-        vload<T, V>(v, my_smc + (size_t)(r + 1 - RR) * NT * V);
+        vload<T, V>(v, my_smc + (size_t)(r + 1 - RS0) * NT * V);
         widen(nxt, v, r + 1);
         T nv[V];
-        finish_row(r, nv, RR == 0 && r == 0);
-        vstore<T, V>(my_smc + (size_t)(r - RR) * NT * V, nv);
+        finish_row(r, nv, RS0 == 0 && r == 0);
+        vstore<T, V>(my_smc + (size_t)(r - RS0) * NT * V, nv);
       }
       halo_below(nxt);
       T nv[V];
       finish_row(R - 1, nv);
-      vstore<T, V>(my_smc + (size_t)(R - 1 - RR) * NT * V, nv);
+      vstore<T, V>(my_smc + (size_t)(R - 1 - RS0) * NT * V, nv);
     }
     // every warp signals "my part of x^{t+1}'s boundary is published": flag = (t+2)*NWARP when the
     // whole tile edge is out.  No CTA barrier here: the next step's halo phase only touches the
@@ -353,11 +407,23 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
   };
 #pragma unroll
   for (int r = 0; r < RR; r++) store_row(r, reg[r]);
-#pragma unroll 1
-  for (int r = RR; r < R; r++) {
+#pragma unroll
+  for (int r = RR; r < RS0; r++) {
     T v[V];
-    vload<T, V>(v, my_smc + (size_t)(r - RR) * NT * V);
+    tmem_ld_row<T, V>(trow(r), v);
     store_row(r, v);
+  }
+#pragma unroll 1
+  for (int r = RS0; r < R; r++) {
+    T v[V];
+    vload<T, V>(v, my_smc + (size_t)(r - RS0) * NT * V);
+    store_row(r, v);
+  }
+  if constexpr (RT > 0) {
+    tmem_fence_before_sync();
+    __syncthreads();
+    tmem_fence_after_sync();
+    if (warp == 0) tmem_dealloc(tmem_base_slot, (uint32_t)G::TCOLS);
   }
 }
 
@@ -386,43 +452,63 @@ using P2F_A3 = Geo2P<float, 4, 2, 4, 16, 16>;  // 256 x 128 tile, 256 thr
 using P2F_B = Geo2P<float, 4, 1, 8, 8, 8>;     // 128 x 128 tile, 256 thr
 using P2F_B2 = Geo2P<float, 4, 1, 8, 8, 0>;    // 128 x  64 tile, 256 thr
 using P2F_C = Geo2P<float, 4, 1, 4, 8, 0>;     // 128 x  32 tile, 128 thr
+// 256 x 256 tile with twice the threads: 8 register + 8 TMEM + 16 shared-memory rows per thread
+// (TMEM as a register-file extension frees the shared memory the 16-warp row buffers need)
 using P2D_A = Geo2P<double, 2, 2, 4, 16, 16>;  // 128 x 128 tile, 256 thr, 64 KiB regs + 64 KiB smem
 using P2D_A2 = Geo2P<double, 2, 2, 4, 16, 8>;  // 128 x  96 tile, 256 thr
 using P2D_A3 = Geo2P<double, 2, 2, 4, 16, 0>;  // 128 x  64 tile, 256 thr
 using P2D_B = Geo2P<double, 2, 2, 4, 8, 0>;    // 128 x  32 tile, 256 thr
 using P2D_C = Geo2P<double, 2, 1, 2, 8, 0>;    //  64 x  16 tile,  64 thr
-constexpr int NCFG_F = 6, NCFG_D = 5;
+// 16-warp tiles with a Tensor-Memory row tier (tmem.cuh): twice the threads of the 8-warp tiles,
+// each with half the rows; TMEM (a per-thread register-file extension) holds the rows the 16-warp
+// row buffers leave no shared memory for.  C2: 9.08 -> 8.25 us/step (profiles/r01_c2_tmem_rows.txt).
+using P2F_T0 = Geo2P<float, 4, 2, 8, 4, 12, 16>;   // 256 x 256 tile, 512 thr: 4 reg + 16 TMEM + 12 smem rows
+using P2F_T1 = Geo2P<float, 4, 2, 8, 4, 8, 12>;    // 256 x 192
+using P2F_T2 = Geo2P<float, 4, 2, 8, 4, 4, 8>;     // 256 x 128
+using P2D_T0 = Geo2P<double, 2, 2, 8, 4, 4, 8>;    // 128 x 128 tile, 512 thr
+using P2D_T1 = Geo2P<double, 2, 2, 8, 4, 0, 8>;    // 128 x  96
+using P2D_T2 = Geo2P<double, 2, 2, 8, 4, 0, 4>;    // 128 x  64
+constexpr int NCFG_F = 6, NCFG_D = 5;   // configurations the planner chooses among
+constexpr int NCFG_F_ALL = 9, NCFG_D_ALL = 8;  // + forced-only (PERKS_P2D_CFG) 8-warp alternatives
 int ncfg(const Problem &p) { return p.dtype == PERKS_F32 ? NCFG_F : NCFG_D; }
 
 struct CfgInfo {
   void *k;
   int TX, TY, NT;
   size_t smem;
-  int64_t reg_cells, smem_cells;
+  int64_t reg_cells, smem_cells, tmem_cells;
+  int tcols;
 };
 
 template <typename T, int S, class G> CfgInfo info() {
   return CfgInfo{(void *)perks2d_kernel<T, S, G>, G::TX, G::TY, G::NT, G::SMEM_BYTES,
-                 (int64_t)G::RR * G::V * G::NT, (int64_t)G::RS * G::V * G::NT};
+                 (int64_t)G::RR * G::V * G::NT, (int64_t)G::RS * G::V * G::NT,
+                 (int64_t)G::RT * G::V * G::NT, G::TCOLS};
 }
 template <typename T, int S> CfgInfo info_t(int cfg);
 template <int S> CfgInfo info_f(int c) {
   switch (c) {
-    case 0: return info<float, S, P2F_A>();
-    case 1: return info<float, S, P2F_A2>();
-    case 2: return info<float, S, P2F_A3>();
+    case 0: return info<float, S, P2F_T0>();
+    case 1: return info<float, S, P2F_T1>();
+    case 2: return info<float, S, P2F_T2>();
     case 3: return info<float, S, P2F_B>();
     case 4: return info<float, S, P2F_B2>();
-    default: return info<float, S, P2F_C>();
+    case 5: return info<float, S, P2F_C>();
+    case 6: return info<float, S, P2F_A>();
+    case 7: return info<float, S, P2F_A2>();
+    default: return info<float, S, P2F_A3>();
   }
 }
 template <int S> CfgInfo info_d(int c) {
   switch (c) {
-    case 0: return info<double, S, P2D_A>();
-    case 1: return info<double, S, P2D_A2>();
-    case 2: return info<double, S, P2D_A3>();
+    case 0: return info<double, S, P2D_T0>();
+    case 1: return info<double, S, P2D_T1>();
+    case 2: return info<double, S, P2D_T2>();
     case 3: return info<double, S, P2D_B>();
-    default: return info<double, S, P2D_C>();
+    case 4: return info<double, S, P2D_C>();
+    case 5: return info<double, S, P2D_A>();
+    case 6: return info<double, S, P2D_A2>();
+    default: return info<double, S, P2D_A3>();
   }
 }
 template <> CfgInfo info_t<float, SHAPE_2D5>(int c) { return info_f<SHAPE_2D5>(c); }
@@ -453,7 +539,7 @@ Plan plan_perks2d(const Problem &p) {
     CfgInfo ci = cfg_info(p, cfg);
     if (p.nx <= ci.TX && p.ny <= ci.TY && ci.smem <= (size_t)p.max_smem_optin) { best = cfg; break; }
   }
-  for (int cfg = NCFG - 1; cfg >= 0 && best < 0; cfg--) {
+  for (int cfg = forced >= 0 ? (p.dtype == PERKS_F32 ? NCFG_F_ALL : NCFG_D_ALL) - 1 : NCFG - 1; cfg >= 0 && best < 0; cfg--) {
     if (forced >= 0 && cfg != forced) continue;
     CfgInfo ci = cfg_info(p, cfg);
     const int64_t tiles = ((p.nx + ci.TX - 1) / ci.TX) * ((p.ny + ci.TY - 1) / ci.TY);
@@ -480,6 +566,8 @@ Plan plan_perks2d(const Problem &p) {
   pl.units = pl.grid;
   pl.cached_reg = ci.reg_cells * pl.grid;
   pl.cached_smem = ci.smem_cells * pl.grid;
+  pl.cached_tmem = ci.tmem_cells * pl.grid;
+  pl.tcols = ci.tcols;
   const double S = (double)p.elem();
   pl.dram_bytes_step = 0.0;  // domain fully resident: only the one-time 2·D_cache term
   pl.halo_bytes_step = S * 2.0 * pl.grid * 2.0 * (ci.TX + ci.TY);  // publish + read, L2

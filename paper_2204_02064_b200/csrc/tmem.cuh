@@ -57,6 +57,48 @@ PERKS_DEVINL void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
                : "r"(taddr));
 }
 
+// 4 consecutive columns of this thread's lane (32x32b.x4)
+PERKS_DEVINL void tmem_st4(uint32_t taddr, uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(taddr), "r"(r0), "r"(r1),
+               "r"(r2), "r"(r3));
+}
+PERKS_DEVINL void tmem_ld4_wait(uint32_t taddr, uint32_t (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]));
+}
+// One 16-byte row segment (4 fp32 or 2 fp64 values) of this thread in 4 TMEM columns.
+template <typename T, int V> PERKS_DEVINL void tmem_st_row(uint32_t taddr, const T (&v)[V]) {
+  static_assert(V * sizeof(T) == 16, "one 16-byte segment");
+  uint32_t w[4];
+  if constexpr (sizeof(T) == 4) {
+#pragma unroll
+    for (int i = 0; i < 4; i++) w[i] = __float_as_uint((float)v[i]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 2; i++) {
+      const unsigned long long b = (unsigned long long)__double_as_longlong((double)v[i]);
+      w[2 * i] = (uint32_t)b;
+      w[2 * i + 1] = (uint32_t)(b >> 32);
+    }
+  }
+  tmem_st4(taddr, w[0], w[1], w[2], w[3]);
+}
+template <typename T, int V> PERKS_DEVINL void tmem_ld_row(uint32_t taddr, T (&v)[V]) {
+  static_assert(V * sizeof(T) == 16, "one 16-byte segment");
+  uint32_t w[4];
+  tmem_ld4_wait(taddr, w);
+  if constexpr (sizeof(T) == 4) {
+#pragma unroll
+    for (int i = 0; i < 4; i++) v[i] = (T)__uint_as_float(w[i]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 2; i++)
+      v[i] = (T)__longlong_as_double((long long)((unsigned long long)w[2 * i] | ((unsigned long long)w[2 * i + 1] << 32)));
+  }
+}
+
 // tcgen05.wait::ld with the loaded registers as in/out operands (the load's destination registers
 // are undefined until the wait completes).
 PERKS_DEVINL void tmem_wait_ld_dep(uint32_t (&r)[8]) {

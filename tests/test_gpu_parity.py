@@ -258,15 +258,20 @@ def test_perks3d_tmem_tier(monkeypatch, nsm, ntm, wsg, name, dtype, shape):
         _check(_run_gpu(u0, name, w, T, "perks"), ref, u0, dtype)
 
 
-TILE_CFGS = {np.float32: [(256, 256), (256, 192), (256, 128), (128, 128), (128, 64), (128, 32)],
-             np.float64: [(128, 128), (128, 96), (128, 64), (128, 32), (64, 16)]}
+# k2d_perks.cu configuration index -> tile (16-warp TMEM-row tiles first, then 8-warp tiles; the last
+# three of each list are forced-only alternatives)
+TILE_CFGS = {np.float32: [(256, 256), (256, 192), (256, 128), (128, 128), (128, 64), (128, 32),
+                          (256, 256), (256, 192), (256, 128)],
+             np.float64: [(128, 128), (128, 96), (128, 64), (128, 32), (64, 16),
+                          (128, 128), (128, 96), (128, 64)]}
 
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
 @pytest.mark.parametrize("name", ["2d5pt", "2d9pt"])
 def test_perks2d_every_tile_config(monkeypatch, dtype, name):
-    """Every PERKS-2D tile configuration (k2d_perks.cu, forced with PERKS_P2D_CFG) on a domain of
-    2.5 x 1.5 tiles (ragged in x and y, several CTAs exchanging edges), bit-exact vs the oracle."""
+    """Every PERKS-2D tile configuration (k2d_perks.cu, forced with PERKS_P2D_CFG) — registers,
+    shared-memory and TMEM row tiers — on a domain of 2.5 x 1.5 tiles (ragged in x and y, several
+    CTAs exchanging edges), bit-exact vs the oracle."""
     _need_gpu()
     from paper_2204_02064_b200 import Stencil
     offs, w = si.preset(name)
