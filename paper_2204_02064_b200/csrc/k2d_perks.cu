@@ -232,7 +232,11 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
     //      yet t+1.  Halo cells are never cached.
     const unsigned tag_in = (unsigned)(t + 1);
 #pragma unroll 1
-    for (int side = warp; side < 4; side += NWARP) {
+    // HP warps per side (all warps take part once there are >= 8): warp w reads segment w / 4 of
+    // side w % 4, so the halo phase (and the CTA barrier after it) shortens with the warp count
+    constexpr int HP = NWARP >= 8 ? NWARP / 4 : 1;
+    for (int sw = warp; sw < 4 * HP; sw += NWARP) {
+      const int side = sw % 4, part = sw / 4;
       const int ddx = side < 2 ? 0 : (side == 2 ? -1 : 1);
       const int ddy = side < 2 ? (side == 0 ? -1 : 1) : 0;
       const int ntx = tx + ddx, nty = ty + ddy;
@@ -240,9 +244,10 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
       const int nt = nty * tl.ntx + ntx;
       if (side < 2) {
         const int dst = pr + (side == 0 ? BOT(0) : TOP(WY));
+        const int lo = part * TX / HP, hi = (part + 1) * TX / HP;
         const LLWord *src = GS(ex ? nt : 0, par) + (side == 0 ? TX : 0) * W;
-        poll_copy<T, (TX + 31) / 32>(src, TX, tag_in, ex, sm + dst + 1, lane);
-        if (BOX && lane < 2) {  // diagonal corners x = -1 (lane 0) and x = TX (lane 1)
+        poll_copy<T, (TX / HP + 31) / 32>(src + lo * W, hi - lo, tag_in, ex, sm + dst + 1 + lo, lane);
+        if (BOX && part == 0 && lane < 2) {  // diagonal corners x = -1 (lane 0) and x = TX (lane 1)
           const int cx = ntx + (lane == 0 ? -1 : 1);
           const bool cex = cx >= 0 && cx < tl.ntx && nty >= 0 && nty < tl.nty;
           const LLWord *cs = GS(cex ? nty * tl.ntx + cx : 0, par) + ((side == 0 ? TX : 0) + (lane == 0 ? TX - 1 : 0)) * W;
@@ -255,15 +260,17 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
       } else {
         const bool left = side == 2;
         const int dst = pc + (left ? RIGHT(0) : LEFT(WX));
+        const int lo = part * TY / HP, hi = (part + 1) * TY / HP;
         const LLWord *src = GS(ex ? nt : 0, par) + (2 * TX + (left ? TY : 0)) * W;
-        poll_copy<T, (TY + 31) / 32>(src, TY, tag_in, ex, sm + dst, lane);
+        poll_copy<T, (TY / HP + 31) / 32>(src + lo * W, hi - lo, tag_in, ex, sm + dst + lo, lane);
         if (BOX) {
           __syncwarp();
-          // internal corners of the row buffers at x = -1 / TX for thread-row boundaries
+          // internal corners of the row buffers at x = -1 / TX for thread-row boundaries: each
+          // value is copied by the warp that polled it
           const int xc = left ? 0 : TX + 1;
           for (int j = 1 + lane; j < WY; j += 32) {
-            sm[pr + BOT(j) + xc] = sm[dst + j * R - 1];
-            sm[pr + TOP(j) + xc] = sm[dst + j * R];
+            if (j * R - 1 >= lo && j * R - 1 < hi) sm[pr + BOT(j) + xc] = sm[dst + j * R - 1];
+            if (j * R >= lo && j * R < hi) sm[pr + TOP(j) + xc] = sm[dst + j * R];
           }
         }
       }
