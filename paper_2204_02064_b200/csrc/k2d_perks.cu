@@ -282,11 +282,16 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
     T prev[V + 2], cur[V + 2], nxt[V + 2];
     // own row (old values) + x-neighbours: shuffles inside the warp; lanes 0/31 take the
     // neighbouring warp's / tile's edge column (broadcast reads, branch free)
+    // the warp-edge column values are loaded one row ahead (rows are widened in order 0, 1, ...,
+    // R-1), so their shared-memory latency is off the row's dependency chain; the load past the
+    // last row reads the neighbouring buffer and is never used
+    T pcl = sm[pc + o_rdL], pcr = sm[pc + o_rdR];
     auto widen = [&](T (&w)[V + 2], const T (&v)[V], int r) {
       const T l = __shfl_up_sync(0xffffffffu, v[V - 1], 1);
       const T rr = __shfl_down_sync(0xffffffffu, v[0], 1);
-      const T cl = sm[pc + o_rdL + r];
-      const T cr = sm[pc + o_rdR + r];
+      const T cl = pcl, cr = pcr;
+      pcl = sm[pc + o_rdL + r + 1];
+      pcr = sm[pc + o_rdR + r + 1];
       w[0] = is_l ? cl : l;
       w[V + 1] = is_r ? cr : rr;
 #pragma unroll
