@@ -35,7 +35,8 @@ struct Geo2P {
   static constexpr int V = V_, WX = WX_, WY = WY_, RR = RR_, RS = RS_, RT = RT_, R = RR_ + RT_ + RS_;
   static constexpr int RS0 = RR + RT;  // first shared-memory row
   // TMEM columns per CTA: warps sharing a lane quarter take consecutive column groups
-  static constexpr int TCOLS_RAW = RT * 4 * ((WX * WY + 3) / 4);
+  static constexpr int WPR = V * (int)sizeof(T) / 4;  // TMEM columns per row segment
+  static constexpr int TCOLS_RAW = RT * WPR * ((WX * WY + 3) / 4);
   static constexpr int TCOLS = TCOLS_RAW == 0 ? 0 : TCOLS_RAW <= 32 ? 32 : TCOLS_RAW <= 64 ? 64
                                : TCOLS_RAW <= 128 ? 128 : TCOLS_RAW <= 256 ? 256 : 512;
   static_assert(TCOLS_RAW <= 512, "TMEM rows exceed 512 columns");
@@ -159,9 +160,12 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
       }
     }
     // branch-free: lanes without a column-buffer cell store to a scratch word (predicated
-    // stores measured 30 % slower: 11.9 vs 9.1 us/step on C2)
-    sm[(is_l ? pc : 0) + o_colL + o_colL_step * r] = v[0];
-    sm[(is_r ? pc : 0) + o_colR + o_colR_step * r] = v[V - 1];
+    // stores measured 30 % slower: 11.9 vs 9.1 us/step on C2).  One warp per tile row (WX == 1):
+    // no warp has a neighbour inside the tile, nothing to store.
+    if constexpr (WX > 1) {
+      sm[(is_l ? pc : 0) + o_colL + o_colL_step * r] = v[0];
+      sm[(is_r ? pc : 0) + o_colR + o_colR_step * r] = v[V - 1];
+    }
     if (g_l) LL<T>::put(g + (2 * TX + yr0 + r) * W, v[0], tag);
     if (g_r) LL<T>::put(g + (2 * TX + TY + yr0 + r) * W, v[V - 1], tag);
   };
@@ -177,9 +181,9 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
     tmem_fence_before_sync();
     __syncthreads();
     tmem_fence_after_sync();
-    tb = tmem_base_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * RT * 4);
+    tb = tmem_base_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * RT * G::WPR);
   }
-  auto trow = [&](int r) { return tb + (uint32_t)((r - RR) * 4); };  // TMEM address of row r
+  auto trow = [&](int r) { return tb + (uint32_t)((r - RR) * G::WPR); };  // TMEM address of row r
 
   // ---- prologue: load the tile into the caches (P:519 the one-time 2·D_cache term, load half)
   T reg[RR > 0 ? RR : 1][V];
@@ -477,11 +481,17 @@ using P2D_C = Geo2P<double, 2, 1, 2, 8, 0>;    //  64 x  16 tile,  64 thr
 using P2F_T0 = Geo2P<float, 4, 2, 8, 4, 12, 16>;   // 256 x 256 tile, 512 thr: 4 reg + 16 TMEM + 12 smem rows
 using P2F_T1 = Geo2P<float, 4, 2, 8, 4, 8, 12>;    // 256 x 192
 using P2F_T2 = Geo2P<float, 4, 2, 8, 4, 4, 8>;     // 256 x 128
+#ifndef PERKS_P2V8_RT
+#define PERKS_P2V8_RT 8
+#endif
+// 256 x 256, one warp per row band (V = 8: no intra-tile column exchange), forced-only: measured
+// 7.85 us/step on C2 vs 7.32 for P2F_T0 (profiles/r01_c2_tmem_rows.txt)
+using P2F_V8 = Geo2P<float, 8, 1, 16, 0, 16 - PERKS_P2V8_RT, PERKS_P2V8_RT>;
 using P2D_T0 = Geo2P<double, 2, 2, 8, 4, 4, 8>;    // 128 x 128 tile, 512 thr
 using P2D_T1 = Geo2P<double, 2, 2, 8, 4, 0, 8>;    // 128 x  96
 using P2D_T2 = Geo2P<double, 2, 2, 8, 4, 0, 4>;    // 128 x  64
 constexpr int NCFG_F = 6, NCFG_D = 5;   // configurations the planner chooses among
-constexpr int NCFG_F_ALL = 9, NCFG_D_ALL = 8;  // + forced-only (PERKS_P2D_CFG) 8-warp alternatives
+constexpr int NCFG_F_ALL = 10, NCFG_D_ALL = 8;  // + forced-only (PERKS_P2D_CFG) 8-warp alternatives
 int ncfg(const Problem &p) { return p.dtype == PERKS_F32 ? NCFG_F : NCFG_D; }
 
 struct CfgInfo {
@@ -508,7 +518,8 @@ template <int S> CfgInfo info_f(int c) {
     case 5: return info<float, S, P2F_C>();
     case 6: return info<float, S, P2F_A>();
     case 7: return info<float, S, P2F_A2>();
-    default: return info<float, S, P2F_A3>();
+    case 8: return info<float, S, P2F_A3>();
+    default: return info<float, S, P2F_V8>();
   }
 }
 template <int S> CfgInfo info_d(int c) {

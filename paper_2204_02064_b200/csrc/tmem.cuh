@@ -68,33 +68,43 @@ PERKS_DEVINL void tmem_ld4_wait(uint32_t taddr, uint32_t (&r)[4]) {
                : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]));
 }
-// One 16-byte row segment (4 fp32 or 2 fp64 values) of this thread in 4 TMEM columns.
+// One row segment of this thread (V values, 16 or 32 bytes) in V*sizeof(T)/4 consecutive TMEM
+// columns of its lane.
 template <typename T, int V> PERKS_DEVINL void tmem_st_row(uint32_t taddr, const T (&v)[V]) {
-  static_assert(V * sizeof(T) == 16, "one 16-byte segment");
-  uint32_t w[4];
+  constexpr int WPR = V * (int)sizeof(T) / 4;
+  static_assert(WPR == 4 || WPR == 8, "16- or 32-byte segments");
+  uint32_t w[WPR];
   if constexpr (sizeof(T) == 4) {
 #pragma unroll
-    for (int i = 0; i < 4; i++) w[i] = __float_as_uint((float)v[i]);
+    for (int i = 0; i < V; i++) w[i] = __float_as_uint((float)v[i]);
   } else {
 #pragma unroll
-    for (int i = 0; i < 2; i++) {
+    for (int i = 0; i < V; i++) {
       const unsigned long long b = (unsigned long long)__double_as_longlong((double)v[i]);
       w[2 * i] = (uint32_t)b;
       w[2 * i + 1] = (uint32_t)(b >> 32);
     }
   }
-  tmem_st4(taddr, w[0], w[1], w[2], w[3]);
+#pragma unroll
+  for (int g = 0; g < WPR / 4; g++) tmem_st4(taddr + 4 * g, w[4 * g], w[4 * g + 1], w[4 * g + 2], w[4 * g + 3]);
 }
 template <typename T, int V> PERKS_DEVINL void tmem_ld_row(uint32_t taddr, T (&v)[V]) {
-  static_assert(V * sizeof(T) == 16, "one 16-byte segment");
-  uint32_t w[4];
-  tmem_ld4_wait(taddr, w);
+  constexpr int WPR = V * (int)sizeof(T) / 4;
+  static_assert(WPR == 4 || WPR == 8, "16- or 32-byte segments");
+  uint32_t w[WPR];
+#pragma unroll
+  for (int g = 0; g < WPR / 4; g++) {
+    uint32_t c[4];
+    tmem_ld4_wait(taddr + 4 * g, c);
+#pragma unroll
+    for (int j = 0; j < 4; j++) w[4 * g + j] = c[j];
+  }
   if constexpr (sizeof(T) == 4) {
 #pragma unroll
-    for (int i = 0; i < 4; i++) v[i] = (T)__uint_as_float(w[i]);
+    for (int i = 0; i < V; i++) v[i] = (T)__uint_as_float(w[i]);
   } else {
 #pragma unroll
-    for (int i = 0; i < 2; i++)
+    for (int i = 0; i < V; i++)
       v[i] = (T)__longlong_as_double((long long)((unsigned long long)w[2 * i] | ((unsigned long long)w[2 * i + 1] << 32)));
   }
 }

@@ -258,10 +258,10 @@ def test_perks3d_tmem_tier(monkeypatch, nsm, ntm, wsg, name, dtype, shape):
         _check(_run_gpu(u0, name, w, T, "perks"), ref, u0, dtype)
 
 
-# k2d_perks.cu configuration index -> tile (16-warp TMEM-row tiles first, then 8-warp tiles; the last
-# three of each list are forced-only alternatives)
+# k2d_perks.cu configuration index -> tile (16-warp TMEM-row tiles first, then 8-warp tiles, then
+# forced-only alternatives: three 8-warp tiles and, fp32, the one-warp-per-band V=8 tile)
 TILE_CFGS = {np.float32: [(256, 256), (256, 192), (256, 128), (128, 128), (128, 64), (128, 32),
-                          (256, 256), (256, 192), (256, 128)],
+                          (256, 256), (256, 192), (256, 128), (256, 256)],
              np.float64: [(128, 128), (128, 96), (128, 64), (128, 32), (64, 16),
                           (128, 128), (128, 96), (128, 64)]}
 
