@@ -69,7 +69,8 @@ def spills_in_plane_loops(obj: str, func: str) -> list:
     backward-branch range (of >= 32 instructions) of the main body (before the final EXIT; the
     mbarrier retry stubs follow it) that contains an mbarrier wait.  Spills of loop-invariant state in a prologue or
     in the per-step outer loop cost one access per unit/step and are tolerated; spills in the
-    per-plane loop are not (P:859-860 register discipline)."""
+    per-plane loop are not (P:859-860 register discipline).  Kernels without such a loop (the 2D
+    kernels) get the strict rule: every spill is reported."""
     r = subprocess.run(["cuobjdump", "-sass", "-fun", func, obj], capture_output=True, text=True)
     ins = []
     for ln in r.stdout.splitlines():
@@ -88,9 +89,11 @@ def spills_in_plane_loops(obj: str, func: str) -> list:
     # (a wait's own spin loop — try_wait, timer read, compare — is a loop too: ignore tiny ones)
     hot = [lp for lp in loops if any(lp[0] <= w <= lp[1] for w in waits)
            and sum(1 for a, _ in ins if lp[0] <= a <= lp[1]) >= 32]
+    spills = [hex(a) for a, t in ins if re.search(r"\b(LDL|STL)\b", t)]
+    if not hot:  # no mbarrier-paced loop (2D kernels): any spill counts
+        return spills
     inner = [lp for lp in hot if not any(o != lp and lp[0] <= o[0] and o[1] <= lp[1] for o in hot)]
-    return [hex(a) for a, t in ins if re.search(r"\b(LDL|STL)\b", t)
-            and any(lo <= a <= hi for lo, hi in inner)]
+    return [a for a in spills if any(lo <= int(a, 16) <= hi for lo, hi in inner)]
 
 
 def build(verbose: bool = False) -> str:
