@@ -478,7 +478,18 @@ using P2D_C = Geo2P<double, 2, 1, 2, 8, 0>;    //  64 x  16 tile,  64 thr
 // 16-warp tiles with a Tensor-Memory row tier (tmem.cuh): twice the threads of the 8-warp tiles,
 // each with half the rows; TMEM (a per-thread register-file extension) holds the rows the 16-warp
 // row buffers leave no shared memory for.  C2: 9.08 -> 8.25 us/step (profiles/r01_c2_tmem_rows.txt).
-using P2F_T0 = Geo2P<float, 4, 2, 8, 4, 12, 16>;   // 256 x 256 tile, 512 thr: 4 reg + 16 TMEM + 12 smem rows
+// register / shared-memory / TMEM rows per thread of the 256 x 256 16-warp tile (sweeps only:
+// profiles/r01_c2_cache_location.txt)
+#ifndef PERKS_P2T_RR
+#define PERKS_P2T_RR 4
+#endif
+#ifndef PERKS_P2T_RS
+#define PERKS_P2T_RS 12
+#endif
+#ifndef PERKS_P2T_RT
+#define PERKS_P2T_RT 16
+#endif
+using P2F_T0 = Geo2P<float, 4, 2, 8, PERKS_P2T_RR, PERKS_P2T_RS, PERKS_P2T_RT>;  // 256 x 256 tile, 512 thr
 using P2F_T1 = Geo2P<float, 4, 2, 8, 4, 8, 12>;    // 256 x 192
 using P2F_T2 = Geo2P<float, 4, 2, 8, 4, 4, 8>;     // 256 x 128
 #ifndef PERKS_P2V8_RT
