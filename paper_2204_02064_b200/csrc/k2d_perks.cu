@@ -26,6 +26,10 @@
 #include "shapes.cuh"
 #include "tmem.cuh"
 
+#ifndef PERKS_P2D_HPMIN  // fewest warps per CTA at which every warp takes part in the halo polls
+#define PERKS_P2D_HPMIN 8
+#endif
+
 namespace perks {
 
 // RR rows per thread in registers, RT rows in Tensor Memory (tmem.cuh: each thread's rows in its own
@@ -238,7 +242,7 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
 #pragma unroll 1
     // HP warps per side (all warps take part once there are >= 8): warp w reads segment w / 4 of
     // side w % 4, so the halo phase (and the CTA barrier after it) shortens with the warp count
-    constexpr int HP = NWARP >= 8 ? NWARP / 4 : 1;
+    constexpr int HP = NWARP >= PERKS_P2D_HPMIN ? NWARP / 4 : 1;
     for (int sw = warp; sw < 4 * HP; sw += NWARP) {
       const int side = sw % 4, part = sw / 4;
       const int ddx = side < 2 ? 0 : (side == 2 ? -1 : 1);
