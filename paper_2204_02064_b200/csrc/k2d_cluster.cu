@@ -40,6 +40,8 @@ PERKS_DEVINL unsigned cluster_nctarank() {
 }
 PERKS_DEVINL void cluster_arrive_release() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory"); }
 PERKS_DEVINL void cluster_wait_acquire() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
+PERKS_DEVINL void cluster_arrive_relaxed() { asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory"); }
+PERKS_DEVINL void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory"); }
 // Shared-memory address of `local_addr` in the CTA of cluster rank `rank`.
 PERKS_DEVINL uint32_t map_rank(uint32_t local_addr, unsigned rank) {
   uint32_t r;
@@ -67,6 +69,10 @@ __global__ void __launch_bounds__(32 * WY, 1) perks2d_cluster_kernel(const T *__
   const unsigned rank = cluster_ctarank(), ncta = cluster_nctarank();
   const int y0 = ((int)rank * WY + wy) * R;  // first row of this warp
   const int x = lane * V;
+
+  // Every CTA of the cluster must have started before anyone writes its shared memory (DSMEM):
+  // arrive now, wait just before the first push, so the barrier overlaps the prologue loads.
+  cluster_arrive_relaxed();
 
   // ---- prologue: the whole domain into registers (one-time load half of 2·D_cache)
   T cur[R][V];
@@ -100,6 +106,7 @@ __global__ void __launch_bounds__(32 * WY, 1) perks2d_cluster_kernel(const T *__
       if (has_dn) st_cluster(dn_base + pb * PAR_BYTES + i * (uint32_t)sizeof(T), bot[i]);
     }
   };
+  cluster_wait();  // all CTAs of the cluster are running (their halo buffers exist)
   push(0, cur[0], cur[R - 1]);
   cluster_arrive_release();
   cluster_wait_acquire();

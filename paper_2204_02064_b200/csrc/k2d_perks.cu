@@ -51,7 +51,9 @@ struct Geo2P {
   static constexpr int CACHE = RS * NT * V;
   static constexpr int ROWBUF = 2 /*par*/ * 2 /*top,bot*/ * (WY + 1) * ROWW;
   static constexpr int COLBUF = 2 /*par*/ * 2 /*left,right*/ * (WX + 1) * TY;
-  static constexpr size_t SMEM_BYTES = (size_t)(CACHE + ROWBUF + COLBUF + 32) * sizeof(T);
+  // + one scratch word per thread: the sink of the branch-free column-buffer stores (per thread, so
+  // no two threads ever write the same word: compute-sanitizer racecheck clean)
+  static constexpr size_t SMEM_BYTES = (size_t)(CACHE + ROWBUF + COLBUF + NT) * sizeof(T);
   static constexpr int SLOT = 2 * (TX + TY);  // one parity of one tile's exchange slot
 };
 
@@ -106,7 +108,7 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
   //   sm_cache        [0, CACHE)                      row r>=RR of thread tid at (r-RR)*NT*V + tid*V
   //   row buffers     TOP(par,j) j=0..WY, BOT(par,jp1) jp1=0..WY, each ROWW wide (x=-1..TX)
   //   column buffers  LEFT(par,k) k=0..WX, RIGHT(par,kp1) kp1=0..WX, each TY tall
-  //   scratch         32 elements (sink for lanes that must not publish; branch-free stores)
+  //   scratch         NT elements (one sink word per thread for the branch-free column stores)
   constexpr int ROW0 = G::CACHE, COL0 = G::CACHE + G::ROWBUF;
   constexpr int SCR0 = G::CACHE + G::ROWBUF + G::COLBUF;
   constexpr int PAR_ROW = 2 * (WY + 1) * ROWW, PAR_COL = 2 * (WX + 1) * TY;
@@ -128,13 +130,13 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
   constexpr int W = LL<T>::WORDS;
   auto GS = [&](int t, int par) -> LLWord * { return gslot + ((size_t)t * 2 + par) * G::SLOT * W; };
 
-  for (int i = tid; i < G::ROWBUF + G::COLBUF + 32; i += NT) sm[ROW0 + i] = T(0);
+  for (int i = tid; i < G::ROWBUF + G::COLBUF + NT; i += NT) sm[ROW0 + i] = T(0);
 
   // per-thread shared-memory offsets (parity 0; add par*PAR_ROW / par*PAR_COL)
   const bool is_l = lane == 0, is_r = lane == 31;
   const int o_top = TOP(wy) + xr + 1, o_bot = BOT(wy + 1) + xr + 1;        // publish rows
-  const int o_colL = is_l ? LEFT(wx) + yr0 : SCR0 + lane;                   // publish cols
-  const int o_colR = is_r ? RIGHT(wx + 1) + yr0 : SCR0 + lane;
+  const int o_colL = is_l ? LEFT(wx) + yr0 : SCR0 + tid;                    // publish cols
+  const int o_colR = is_r ? RIGHT(wx + 1) + yr0 : SCR0 + tid;
   const int o_colL_step = is_l ? 1 : 0, o_colR_step = is_r ? 1 : 0;
   const int o_rdL = RIGHT(wx) + yr0, o_rdR = LEFT(wx + 1) + yr0;           // read cols
   const int o_above = BOT(wy) + xr, o_below = TOP(wy + 1) + xr;             // read rows
