@@ -114,7 +114,9 @@ const Plan &get_plan(perks_stencil_s *h, perks_variant v) {
   if (!h->planned[i]) {
     const Problem &p = h->p;
     Plan pl;
-    if (v == PERKS_HOSTLOOP || v == PERKS_PERSISTENT)
+    if (p.shape == SHAPE_G2D)
+      pl = plan_wide2d(p, v);
+    else if (v == PERKS_HOSTLOOP || v == PERKS_PERSISTENT)
       pl = p.ndim == 2 ? plan_stream2d(p, v) : plan_stream3d(p, v);
     else if (v == PERKS_PERKS && p.ndim == 2) {
       pl = plan_perks2d_cluster(p);  // small domains: one cluster, registers only
@@ -193,7 +195,7 @@ static perks_status create_impl(const perks_stencil_desc *d, int device, int ran
   if (!d || !out) return PERKS_ERR_INVALID_ARGUMENT;
   *out = nullptr;
   if (d->ndim != 2 && d->ndim != 3) return PERKS_ERR_INVALID_ARGUMENT;
-  if (d->npoints < 1 || d->npoints > 27 || !d->offsets || !d->weights)
+  if (d->npoints < 1 || d->npoints > (d->ndim == 2 ? kMaxPoints2D : 27) || !d->offsets || !d->weights)
     return PERKS_ERR_INVALID_ARGUMENT;
   if (d->dtype != PERKS_F32 && d->dtype != PERKS_F64) return PERKS_ERR_INVALID_ARGUMENT;
   if (d->bc != PERKS_BC_FRAME && d->bc != PERKS_BC_PERIODIC) return PERKS_ERR_INVALID_ARGUMENT;
@@ -214,7 +216,10 @@ static perks_status create_impl(const perks_stencil_desc *d, int device, int ran
   for (int a = 0; a < 3; a++)
     if (d->extent[a] > (int64_t)1 << 30) return PERKS_ERR_UNSUPPORTED;
   if (d->bc != PERKS_BC_FRAME) return PERKS_ERR_UNSUPPORTED;  // GPU kernels: FRAME only
-  const int shape = find_shape(d->ndim, d->offsets, d->npoints);
+  int shape = find_shape(d->ndim, d->offsets, d->npoints);
+  // 2D point sets without a specialised kernel (radius > 1, or another order / set): the general
+  // kernels of k2d_wide.cu (radius <= 6)
+  if (shape < 0 && d->ndim == 2 && r <= 6) shape = SHAPE_G2D;
   if (shape < 0) return PERKS_ERR_UNSUPPORTED;
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -234,6 +239,8 @@ static perks_status create_impl(const perks_stencil_desc *d, int device, int ran
   for (int i = 0; i < d->npoints; i++) {
     p.wd[i] = d->weights[i];
     p.wf[i] = (float)d->weights[i];  // reading R6: rounded once (RN-even) to the storage dtype
+    p.off[i][0] = (int16_t)d->offsets[3 * i];
+    p.off[i][1] = (int16_t)d->offsets[3 * i + 1];
   }
   p.device = device;
   p.rank = rank;
@@ -436,6 +443,10 @@ perks_status perks_stencil_run(perks_stencil_t h, perks_variant v, const void *d
     if (e != cudaSuccess) return cuda_fail(e);
     h->dist.xbase += (unsigned long long)steps + 1;  // prologue exchange + one per step
     return PERKS_OK;
+  }
+  if (p.shape == SHAPE_G2D) {
+    cudaError_t e2 = run_wide2d(p, pl, d_in, d_out, d_ws, steps, s);
+    return e2 == cudaSuccess ? PERKS_OK : cuda_fail(e2);
   }
   switch (v) {
     case PERKS_HOSTLOOP:

@@ -9,6 +9,10 @@
 
 namespace perks {
 
+// General 2D point sets (any radius <= 6, any order, <= 64 points) run on the k2d_wide.cu kernels.
+constexpr int SHAPE_G2D = 100;
+constexpr int kMaxPoints2D = 64;
+
 struct Problem {
   int ndim;
   int64_t nx, ny, nz;
@@ -16,8 +20,9 @@ struct Problem {
   perks_dtype dtype;
   perks_bc bc;
   int npts;
-  double wd[27];      // weights rounded to f64 (identity)
-  float wf[27];       // weights rounded once to f32 (reading R6)
+  double wd[kMaxPoints2D];  // weights rounded to f64 (identity)
+  float wf[kMaxPoints2D];   // weights rounded once to f32 (reading R6)
+  int16_t off[kMaxPoints2D][2];  // (dx, dy) of each point (SHAPE_G2D)
   int device;
   int rank = 0, nranks = 1;  // multi-GPU slab decomposition along z
   int num_sms;
@@ -92,6 +97,11 @@ Plan plan_perks2d_strip(const Problem &p);
 cudaError_t run_perks2d_strip(const Problem &p, const Plan &pl, const void *in, void *out, void *ws,
                               int64_t steps, cudaStream_t s);
 // PERKS (c), 3D: the persistent kernel with a shared-memory plane cache (k3d_stream.cu).
+
+// Any variant for general 2D point sets of radius <= 6 (k2d_wide.cu).
+Plan plan_wide2d(const Problem &p, perks_variant v);
+cudaError_t run_wide2d(const Problem &p, const Plan &pl, const void *in, void *out, void *ws, int64_t steps,
+                       cudaStream_t s);
 
 // Environment override helper (sweeps only): returns def if unset.
 int env_int(const char *name, int def);

@@ -138,12 +138,36 @@ def preset(name: str):
                         continue
                     offs.append((dx, dy, dz))
                     w.append({0: 1 / 4, 1: 1 / 16, 2: 1 / 32}[m])
+    elif name in STAR_RADIUS:
+        # Table II high-order stars 2ds9pt / 2d13pt / 2d17pt / 2d21pt / 2ds25pt (radius 2..6):
+        # the 4r+1 points (0,dy) and (dx,0), (dy,dx) lexicographic; dyadic convex weights: centre
+        # 2^-r, distance k along each arm 2^-(k+2) (sum exactly 1)
+        r = STAR_RADIUS[name]
+        offs, w = [], []
+        for dy in range(-r, r + 1):
+            for dx in range(-r, r + 1):
+                if dx != 0 and dy != 0:
+                    continue
+                k = abs(dx) + abs(dy)
+                offs.append((dx, dy, 0))
+                w.append(2.0 ** -r if k == 0 else 2.0 ** -(k + 2))
+    elif name == "2d25pt":
+        # Table II 2d25pt: the 5x5 box (radius 2), (dy,dx) lexicographic; binomial weights
+        # (1,4,6,4,1)/16 per axis (dyadic, sum exactly 1)
+        b = {-2: 1, -1: 4, 0: 6, 1: 4, 2: 1}
+        offs, w = [], []
+        for dy in range(-2, 3):
+            for dx in range(-2, 3):
+                offs.append((dx, dy, 0))
+                w.append(b[dx] * b[dy] / 256)
     else:
         raise KeyError(name)
     return offs, w
 
 
-PRESET_NDIM = {"2d5pt": 2, "2d9pt": 2, "3d7pt": 3, "3d27pt": 3, "3d19pt": 3}
+STAR_RADIUS = {"2ds9pt": 2, "2d13pt": 3, "2d17pt": 4, "2d21pt": 5, "2ds25pt": 6}
+PRESET_NDIM = {"2d5pt": 2, "2d9pt": 2, "3d7pt": 3, "3d27pt": 3, "3d19pt": 3, "2d25pt": 2,
+               **{k: 2 for k in STAR_RADIUS}}
 
 
 def random_convex_weights(npts: int, dtype=np.float64, seed: int = 7) -> list[float]:
@@ -180,4 +204,10 @@ SWEEP_CONFIGS = {
     "S2_2560": dict(stencil="2d9pt", dtype="f32", shape=(2560, 2560), steps=1000),
     "S2d_1024": dict(stencil="2d5pt", dtype="f64", shape=(1024, 1024), steps=1000),
     "S2d_1536": dict(stencil="2d5pt", dtype="f64", shape=(1536, 1536), steps=1000),
+    # Table II high-order stencils on the general kernels (k2d_wide.cu), fully cacheable size
+    "W_2ds9pt": dict(stencil="2ds9pt", dtype="f32", shape=(1536, 1536), steps=1000),
+    "W_2d13pt": dict(stencil="2d13pt", dtype="f32", shape=(1536, 1536), steps=1000),
+    "W_2ds25pt": dict(stencil="2ds25pt", dtype="f32", shape=(1536, 1536), steps=1000),
+    "W_2d25pt": dict(stencil="2d25pt", dtype="f32", shape=(1536, 1536), steps=1000),
+    "W_2ds9pt_f64": dict(stencil="2ds9pt", dtype="f64", shape=(1536, 768), steps=1000),
 }

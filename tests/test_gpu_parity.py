@@ -286,3 +286,57 @@ def test_perks2d_every_tile_config(monkeypatch, dtype, name):
         for T in (1, 6):
             ref = oracle.run(u0, offs, w, T, nthreads=8)
             _check(_run_gpu(u0, name, w, T, "perks"), ref, u0, dtype)
+
+
+WIDE_PRESETS = ["2ds9pt", "2d13pt", "2d17pt", "2d21pt", "2ds25pt", "2d25pt"]
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("name", WIDE_PRESETS)
+@pytest.mark.parametrize("shape", [(13, 13), (67, 131), (150, 300), (300, 270)])
+def test_parity_wide_2d(variant, dtype, name, shape):
+    """Table II high-order stencils (radius 2..6) on the general 2D kernels (k2d_wide.cu): every
+    variant bit-exact vs the oracle; domains from the minimum (2r+1 for r = 6) to several tiles
+    with ragged edges (the PERKS tile exchange crosses tile corners for the 5x5 box)."""
+    _need_gpu()
+    offs, w = si.preset(name)
+    r = max(max(abs(a), abs(b)) for a, b, _ in offs)
+    if min(shape) < 2 * r + 1:
+        pytest.skip("domain below 2r+1")
+    u0 = si.field(shape, dtype=dtype, seed=1001)
+    for T in (1, 5):
+        ref = oracle.run(u0, offs, w, T, nthreads=8)
+        _check(_run_gpu_offs(u0, offs, w, T, variant), ref, u0, dtype)
+
+
+def _run_gpu_offs(u0, offs, w, steps, variant):
+    from paper_2204_02064_b200 import Stencil
+    st = Stencil(u0.shape, offs, w, dtype=u0.dtype)
+    x = torch.from_numpy(u0).cuda()
+    out = torch.full_like(x, float("nan"))
+    nb = st.workspace_bytes(variant)
+    ws = torch.empty(max(nb, 256), dtype=torch.uint8, device="cuda")
+    ws.fill_(0xFF)
+    st.run(x, steps, variant, out=out, workspace=ws)
+    torch.cuda.synchronize()
+    res = out.cpu().numpy()
+    st.close()
+    return res
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_wide_2d_any_order_and_random_weights(dtype):
+    """Point sets with no specialised kernel — a reversed 2d9pt list, an asymmetric radius-3 set —
+    with random weights: all variants bit-identical to each other and to the oracle (the list order
+    is the accumulation order, reading R5)."""
+    _need_gpu()
+    o9, _ = si.preset("2d9pt")
+    asym = [(0, 0, 0), (3, 0, 0), (-1, 2, 0), (2, -3, 0), (-3, -1, 0), (1, 1, 0), (0, 3, 0)]
+    for offs in (o9[::-1], asym):
+        w = si.random_convex_weights(len(offs), dtype, seed=17)
+        u0 = si.field((140, 290), dtype=dtype, seed=1002)
+        ref = oracle.run(u0, offs, w, 6, nthreads=8)
+        outs = [_run_gpu_offs(u0, offs, w, 6, v) for v in VARIANTS]
+        for o in outs:
+            _check(o, ref, u0, dtype)
