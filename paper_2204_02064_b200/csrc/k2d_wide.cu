@@ -13,8 +13,9 @@
 //       as the r=1 tile kernel, k2d_perks.cu) and fills its halo ring from its <= 8 neighbours'
 //       strips (corners from the diagonal neighbours' row strips), waiting only on those tags (the
 //       dependency of P:348) — no grid barrier.  Halo cells are never cached.
-// Throughput is secondary here (generic loops over a runtime point list); the r=1 presets keep
-// their specialised kernels.
+// The Table II presets run with compile-time point sets (WideSet: immediate shared-memory offsets,
+// unrolled FMA chain); any other list runs the same kernels with a runtime loop.  The r=1 presets
+// keep their specialised kernels.
 #include <algorithm>
 #include <cstdio>
 
@@ -23,13 +24,32 @@
 
 namespace perks {
 
-constexpr int KW_THREADS = 256;
+constexpr int KW_THREADS = 256;    // stream kernels (many CTAs per SM)
+constexpr int KW_THREADS_P = 1024; // PERKS: one CTA per SM does all of its tile's work
 constexpr int KW_MAXR = 6;
 
 template <typename T> struct WideCoef {
   int n;
   int8_t dx[kMaxPoints2D], dy[kMaxPoints2D];
   T w[kMaxPoints2D];
+};
+
+// Compile-time point sets for the Table II presets (seeded_inputs.preset order, (dy,dx)
+// lexicographic): PS 1..5 = stars of radius 2..6 (2ds9pt, 2d13pt, 2d17pt, 2d21pt, 2ds25pt),
+// PS 6 = the 5x5 box (2d25pt).  PS 0 = any other list (runtime loop over WideCoef).  With a
+// compile-time set every term is one shared-memory load at an immediate offset and one FMA.
+constexpr int kNumWidePresets = 7;
+template <int PS> struct WideSet;
+template <> struct WideSet<0> { static constexpr int R = 0, N = 0; };
+template <int PS> struct WideSet {
+  static constexpr bool BOX = PS == 6;
+  static constexpr int R = BOX ? 2 : PS + 1, N = BOX ? 25 : 4 * R + 1;
+  static constexpr __host__ __device__ int dx(int p) {
+    return BOX ? p % 5 - 2 : (p < R ? 0 : p < 3 * R + 1 ? p - 2 * R : 0);
+  }
+  static constexpr __host__ __device__ int dy(int p) {
+    return BOX ? p / 5 - 2 : (p < R ? p - R : p < 3 * R + 1 ? 0 : p - 3 * R);
+  }
 };
 
 // Tile geometry: the stream kernels use 128 x 32 tiles; PERKS 128 x 128 (fp32) / 128 x 64 (fp64)
@@ -54,29 +74,40 @@ __device__ void load_tile(const T *__restrict__ src, int nx, int ny, int x0, int
 
 // New value of cell (x, y) (tile-local (lx, ly)) from the tile copy s; frame cells (within r of a
 // face, reading R1) keep their value.
-template <typename T>
+template <typename T, int PS, int TX>
 __device__ __forceinline__ T cell_update(const T *s, int P, int r, int lx, int ly, int x, int y, int nx, int ny,
                                          const WideCoef<T> &c) {
-  const T *ctr = s + (ly + r) * P + (lx + r);
-  if (x < r || x >= nx - r || y < r || y >= ny - r) return *ctr;
-  T acc = mul_rn(c.w[0], ctr[c.dy[0] * P + c.dx[0]]);
-  for (int p = 1; p < c.n; p++) acc = fma_rn(c.w[p], ctr[c.dy[p] * P + c.dx[p]], acc);
-  return acc;
+  if constexpr (PS == 0) {
+    const T *ctr = s + (ly + r) * P + (lx + r);
+    if (x < r || x >= nx - r || y < r || y >= ny - r) return *ctr;
+    T acc = mul_rn(c.w[0], ctr[c.dy[0] * P + c.dx[0]]);
+    for (int p = 1; p < c.n; p++) acc = fma_rn(c.w[p], ctr[c.dy[p] * P + c.dx[p]], acc);
+    return acc;
+  } else {
+    using WS = WideSet<PS>;
+    constexpr int R = WS::R, PC = TX + 2 * R;  // compile-time radius and pitch
+    const T *ctr = s + (ly + R) * PC + (lx + R);
+    if (x < R || x >= nx - R || y < R || y >= ny - R) return *ctr;
+    T acc = mul_rn(c.w[0], ctr[WS::dy(0) * PC + WS::dx(0)]);
+#pragma unroll
+    for (int p = 1; p < WS::N; p++) acc = fma_rn(c.w[p], ctr[WS::dy(p) * PC + WS::dx(p)], acc);
+    return acc;
+  }
 }
 
 // Compute and store the tile (x0, y0) of one step from s into dst.
-template <typename T>
-__device__ void tile_step(const T *s, T *__restrict__ dst, int nx, int ny, int x0, int y0, int TX, int TY,
-                          int r, const WideCoef<T> &c) {
+template <typename T, int PS, int TX, int TY>
+__device__ void tile_step(const T *s, T *__restrict__ dst, int nx, int ny, int x0, int y0, int r,
+                          const WideCoef<T> &c) {
   const int P = TX + 2 * r;
   for (int i = threadIdx.x; i < TX * TY; i += blockDim.x) {
     const int ly = i / TX, lx = i % TX;
     const int x = x0 + lx, y = y0 + ly;
-    if (x < nx && y < ny) dst[(size_t)y * nx + x] = cell_update(s, P, r, lx, ly, x, y, nx, ny, c);
+    if (x < nx && y < ny) dst[(size_t)y * nx + x] = cell_update<T, PS, TX>(s, P, r, lx, ly, x, y, nx, ny, c);
   }
 }
 
-template <typename T>
+template <typename T, int PS>
 __global__ void __launch_bounds__(KW_THREADS) wide_hostloop_kernel(const T *__restrict__ src, T *__restrict__ dst,
                                                                    int nx, int ny, int ntx, int r,
                                                                    const __grid_constant__ WideCoef<T> c) {
@@ -86,10 +117,10 @@ __global__ void __launch_bounds__(KW_THREADS) wide_hostloop_kernel(const T *__re
   const int x0 = (blockIdx.x % ntx) * TX, y0 = (blockIdx.x / ntx) * TY;
   load_tile(src, nx, ny, x0, y0, TX, TY, r, s);
   __syncthreads();
-  tile_step(s, dst, nx, ny, x0, y0, TX, TY, r, c);
+  tile_step<T, PS, TX, TY>(s, dst, nx, ny, x0, y0, r, c);
 }
 
-template <typename T>
+template <typename T, int PS>
 __global__ void __launch_bounds__(KW_THREADS) wide_persistent_kernel(const T *__restrict__ in, T *out, T *tmp,
                                                                      int nx, int ny, int ntx, int ntiles, int r,
                                                                      int64_t steps, unsigned *bar,
@@ -104,7 +135,7 @@ __global__ void __launch_bounds__(KW_THREADS) wide_persistent_kernel(const T *__
       const int x0 = (tile % ntx) * TX, y0 = (tile / ntx) * TY;
       load_tile(src, nx, ny, x0, y0, TX, TY, r, s);
       __syncthreads();
-      tile_step(s, dst, nx, ny, x0, y0, TX, TY, r, c);
+      tile_step<T, PS, TX, TY>(s, dst, nx, ny, x0, y0, r, c);
       __syncthreads();
     }
     if (t + 1 < steps) grid_barrier(bar, (unsigned)((t + 1) * gridDim.x));
@@ -115,8 +146,8 @@ __global__ void __launch_bounds__(KW_THREADS) wide_persistent_kernel(const T *__
 // tagged values (LL<T>::WORDS words each).  Strip element (row j, column i) of the top strip is
 // tile cell (i, j); of the bottom strip (i, TY-r+j); of the left strip (i, j) at index j*r + i; of
 // the right strip (TX-r+i, j) at index j*r + i.
-template <typename T>
-__global__ void __launch_bounds__(KW_THREADS, 1) wide_perks_kernel(const T *__restrict__ in, T *__restrict__ out,
+template <typename T, int PS>
+__global__ void __launch_bounds__(KW_THREADS_P, 1) wide_perks_kernel(const T *__restrict__ in, T *__restrict__ out,
                                                                    LLWord *gslot, int nx, int ny, int ntx, int nty,
                                                                    int r, int64_t steps,
                                                                    const __grid_constant__ WideCoef<T> c) {
@@ -202,7 +233,7 @@ __global__ void __launch_bounds__(KW_THREADS, 1) wide_perks_kernel(const T *__re
     for (int i = threadIdx.x; i < TX * TY; i += blockDim.x) {
       const int ly = i / TX, lx = i % TX;
       const int x = x0 + lx, y = y0 + ly;
-      sn[(ly + r) * P + lx + r] = (x < nx && y < ny) ? cell_update(buf[cur], P, r, lx, ly, x, y, nx, ny, c) : T(0);
+      sn[(ly + r) * P + lx + r] = (x < nx && y < ny) ? cell_update<T, PS, TX>(buf[cur], P, r, lx, ly, x, y, nx, ny, c) : T(0);
     }
     __syncthreads();
     publish(sn, par ^ 1, (unsigned)(t + 2));
@@ -240,9 +271,36 @@ template <typename T> size_t stream_smem(int r) {
 template <typename T> size_t perks_smem(int r) {
   return 2 * (size_t)(WideGeo<T>::TXP + 2 * r) * (WideGeo<T>::TYP + 2 * r) * sizeof(T);
 }
-template <typename T> void *wk(perks_variant v) {
-  return v == PERKS_HOSTLOOP ? (void *)wide_hostloop_kernel<T>
-         : v == PERKS_PERSISTENT ? (void *)wide_persistent_kernel<T> : (void *)wide_perks_kernel<T>;
+// Which compile-time set (WideSet) the problem's point list is, 0 if none.
+int wide_preset(const Problem &p) {
+  for (int ps = 1; ps < kNumWidePresets; ps++) {
+    const bool box = ps == 6;
+    const int R = box ? 2 : ps + 1, N = box ? 25 : 4 * R + 1;
+    if (p.npts != N) continue;
+    bool ok = true;
+    for (int q = 0; q < N && ok; q++) {
+      const int dx = box ? q % 5 - 2 : (q < R ? 0 : q < 3 * R + 1 ? q - 2 * R : 0);
+      const int dy = box ? q / 5 - 2 : (q < R ? q - R : q < 3 * R + 1 ? 0 : q - 3 * R);
+      ok = p.off[q][0] == dx && p.off[q][1] == dy;
+    }
+    if (ok) return ps;
+  }
+  return 0;
+}
+template <typename T, int PS> void *wk_ps(perks_variant v) {
+  return v == PERKS_HOSTLOOP ? (void *)wide_hostloop_kernel<T, PS>
+         : v == PERKS_PERSISTENT ? (void *)wide_persistent_kernel<T, PS> : (void *)wide_perks_kernel<T, PS>;
+}
+template <typename T> void *wk(perks_variant v, int ps) {
+  switch (ps) {
+    case 1: return wk_ps<T, 1>(v);
+    case 2: return wk_ps<T, 2>(v);
+    case 3: return wk_ps<T, 3>(v);
+    case 4: return wk_ps<T, 4>(v);
+    case 5: return wk_ps<T, 5>(v);
+    case 6: return wk_ps<T, 6>(v);
+    default: return wk_ps<T, 0>(v);
+  }
 }
 }  // namespace
 
@@ -255,7 +313,8 @@ Plan plan_wide2d(const Problem &p, perks_variant v) {
     return pl;
   }
   const bool f32 = p.dtype == PERKS_F32;
-  void *k = f32 ? wk<float>(v) : wk<double>(v);
+  const int ps = wide_preset(p);
+  void *k = f32 ? wk<float>(v, ps) : wk<double>(v, ps);
   const bool perks = v == PERKS_PERKS;
   const int TX = perks ? (f32 ? WideGeo<float>::TXP : WideGeo<double>::TXP) : (f32 ? WideGeo<float>::TXS : WideGeo<double>::TXS);
   const int TY = perks ? (f32 ? WideGeo<float>::TYP : WideGeo<double>::TYP) : (f32 ? WideGeo<float>::TYS : WideGeo<double>::TYS);
@@ -270,14 +329,14 @@ Plan plan_wide2d(const Problem &p, perks_variant v) {
   cudaFuncAttributes fa;
   if (cudaFuncGetAttributes(&fa, k) != cudaSuccess) { pl.why = "cudaFuncGetAttributes"; return pl; }
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, KW_THREADS, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, perks ? KW_THREADS_P : KW_THREADS, smem);
   if (occ < 1) { pl.why = "wide2d: not resident"; return pl; }
   const int ntx = (int)((p.nx + TX - 1) / TX), nty = (int)((p.ny + TY - 1) / TY);
   const int64_t tiles = (int64_t)ntx * nty;
   if (perks && tiles > (int64_t)occ * p.num_sms) { pl.why = "wide2d perks: domain does not fit on chip"; return pl; }
   pl.units = tiles;
   pl.grid = v == PERKS_PERSISTENT ? (int)std::min<int64_t>(tiles, (int64_t)occ * p.num_sms) : (int)tiles;
-  pl.block = KW_THREADS;
+  pl.block = perks ? KW_THREADS_P : KW_THREADS;
   pl.ctas_per_sm = perks ? 1 : occ;
   pl.tile[0] = TX; pl.tile[1] = TY; pl.tile[2] = 1;
   pl.regs = fa.numRegs;
@@ -295,8 +354,9 @@ Plan plan_wide2d(const Problem &p, perks_variant v) {
     pl.halo_bytes_step = S * (double)tiles * 2.0 * r * (TX + TY + 2 * r);
     pl.ws_bytes = align256((size_t)p.cells() * p.elem()) + (v == PERKS_PERSISTENT ? 256 : 0);
   }
-  snprintf(pl.name, sizeof(pl.name), "%s2d_wide_r%d_%dpt_%s_t%dx%d", perks ? "perks" : v == PERKS_PERSISTENT ? "persistent" : "hostloop",
-           r, p.npts, f32 ? "f32" : "f64", TX, TY);
+  pl.cfg = ps;  // compile-time point set (0: runtime list)
+  snprintf(pl.name, sizeof(pl.name), "%s2d_wide_r%d_%dpt%s_%s_t%dx%d", perks ? "perks" : v == PERKS_PERSISTENT ? "persistent" : "hostloop",
+           r, p.npts, ps ? "" : "_any", f32 ? "f32" : "f64", TX, TY);
   pl.ok = true;
   return pl;
 }
@@ -306,6 +366,7 @@ template <typename T>
 cudaError_t run_wide_t(const Problem &p, const Plan &pl, const T *in, T *out, void *ws, int64_t steps, cudaStream_t s) {
   const WideCoef<T> c = make_coef<T>(p);
   const int r = radius2d(p);
+  void *k = wk<T>(pl.variant, pl.cfg);
   const int nx = (int)p.nx, ny = (int)p.ny;
   const int ntx = (nx + pl.tile[0] - 1) / pl.tile[0], nty = (ny + pl.tile[1] - 1) / pl.tile[1];
   if (pl.variant == PERKS_HOSTLOOP) {
@@ -313,15 +374,15 @@ cudaError_t run_wide_t(const Problem &p, const Plan &pl, const T *in, T *out, vo
     for (int64_t t = 0; t < steps; t++) {
       const T *src = t == 0 ? in : ((((steps - t) & 1) == 0) ? out : tmp);
       T *dst = (((steps - 1 - t) & 1) == 0) ? out : tmp;
-      wide_hostloop_kernel<T><<<pl.grid, KW_THREADS, pl.smem, s>>>(src, dst, nx, ny, ntx, r, c);
-      cudaError_t e = cudaGetLastError();
+      void *args[] = {(void *)&src, (void *)&dst, (void *)&nx, (void *)&ny, (void *)&ntx, (void *)&r, (void *)&c};
+      cudaError_t e = cudaLaunchKernel(k, dim3(pl.grid), dim3(KW_THREADS), args, pl.smem, s);
       if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(pl.grid);
-  cfg.blockDim = dim3(KW_THREADS);
+  cfg.blockDim = dim3(pl.block);
   cfg.dynamicSmemBytes = pl.smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
@@ -335,11 +396,16 @@ cudaError_t run_wide_t(const Problem &p, const Plan &pl, const T *in, T *out, vo
     cudaError_t e = cudaMemsetAsync(bar, 0, 256, s);
     if (e != cudaSuccess) return e;
     const int ntiles = ntx * nty;
-    return cudaLaunchKernelEx(&cfg, wide_persistent_kernel<T>, in, out, tmp, nx, ny, ntx, ntiles, r, steps, bar, c);
+    void *args[] = {(void *)&in, (void *)&out, (void *)&tmp, (void *)&nx, (void *)&ny, (void *)&ntx,
+                    (void *)&ntiles, (void *)&r, (void *)&steps, (void *)&bar, (void *)&c};
+    return cudaLaunchKernelExC(&cfg, k, args);
   }
   cudaError_t e = cudaMemsetAsync(ws, 0, pl.ws_bytes, s);  // tags start at 0 (x^s carries s+1)
   if (e != cudaSuccess) return e;
-  return cudaLaunchKernelEx(&cfg, wide_perks_kernel<T>, in, out, (LLWord *)ws, nx, ny, ntx, nty, r, steps, c);
+  LLWord *gslot = (LLWord *)ws;
+  void *args[] = {(void *)&in, (void *)&out, (void *)&gslot, (void *)&nx, (void *)&ny, (void *)&ntx,
+                  (void *)&nty, (void *)&r, (void *)&steps, (void *)&c};
+  return cudaLaunchKernelExC(&cfg, k, args);
 }
 }  // namespace
 
