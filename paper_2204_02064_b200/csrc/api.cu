@@ -116,6 +116,8 @@ const Plan &get_plan(perks_stencil_s *h, perks_variant v) {
     Plan pl;
     if (p.shape == SHAPE_G2D)
       pl = plan_wide2d(p, v);
+    else if (p.shape == SHAPE_G3D)
+      pl = plan_wide3d(p, v);
     else if (v == PERKS_HOSTLOOP || v == PERKS_PERSISTENT)
       pl = p.ndim == 2 ? plan_stream2d(p, v) : plan_stream3d(p, v);
     else if (v == PERKS_PERKS && p.ndim == 2) {
@@ -195,7 +197,7 @@ static perks_status create_impl(const perks_stencil_desc *d, int device, int ran
   if (!d || !out) return PERKS_ERR_INVALID_ARGUMENT;
   *out = nullptr;
   if (d->ndim != 2 && d->ndim != 3) return PERKS_ERR_INVALID_ARGUMENT;
-  if (d->npoints < 1 || d->npoints > (d->ndim == 2 ? kMaxPoints2D : 27) || !d->offsets || !d->weights)
+  if (d->npoints < 1 || d->npoints > kMaxPoints2D || !d->offsets || !d->weights)
     return PERKS_ERR_INVALID_ARGUMENT;
   if (d->dtype != PERKS_F32 && d->dtype != PERKS_F64) return PERKS_ERR_INVALID_ARGUMENT;
   if (d->bc != PERKS_BC_FRAME && d->bc != PERKS_BC_PERIODIC) return PERKS_ERR_INVALID_ARGUMENT;
@@ -220,6 +222,7 @@ static perks_status create_impl(const perks_stencil_desc *d, int device, int ran
   // 2D point sets without a specialised kernel (radius > 1, or another order / set): the general
   // kernels of k2d_wide.cu (radius <= 6)
   if (shape < 0 && d->ndim == 2 && r <= 6) shape = SHAPE_G2D;
+  if (shape < 0 && d->ndim == 3 && r <= 3) shape = SHAPE_G3D;  // k3d_wide.cu
   if (shape < 0) return PERKS_ERR_UNSUPPORTED;
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -241,6 +244,7 @@ static perks_status create_impl(const perks_stencil_desc *d, int device, int ran
     p.wf[i] = (float)d->weights[i];  // reading R6: rounded once (RN-even) to the storage dtype
     p.off[i][0] = (int16_t)d->offsets[3 * i];
     p.off[i][1] = (int16_t)d->offsets[3 * i + 1];
+    p.off3z[i] = (int16_t)d->offsets[3 * i + 2];
   }
   p.device = device;
   p.rank = rank;
@@ -287,6 +291,11 @@ perks_status perks_stencil_create_dist(const perks_stencil_desc *d, int device, 
   perks_stencil_s *h = *out;
   h->p.nz = nz_local;
   if (nranks == 1) return PERKS_OK;
+  if (h->p.shape == SHAPE_G3D) {  // slabs exchange faces only in the specialised r=1 kernels
+    perks_stencil_destroy(h);
+    *out = nullptr;
+    return PERKS_ERR_UNSUPPORTED;
+  }
   DistState &ds = h->dist;
   ds.on = true;
   DeviceGuard g(device);
@@ -444,8 +453,9 @@ perks_status perks_stencil_run(perks_stencil_t h, perks_variant v, const void *d
     h->dist.xbase += (unsigned long long)steps + 1;  // prologue exchange + one per step
     return PERKS_OK;
   }
-  if (p.shape == SHAPE_G2D) {
-    cudaError_t e2 = run_wide2d(p, pl, d_in, d_out, d_ws, steps, s);
+  if (p.shape == SHAPE_G2D || p.shape == SHAPE_G3D) {
+    cudaError_t e2 = p.shape == SHAPE_G2D ? run_wide2d(p, pl, d_in, d_out, d_ws, steps, s)
+                                          : run_wide3d(p, pl, d_in, d_out, d_ws, steps, s);
     return e2 == cudaSuccess ? PERKS_OK : cuda_fail(e2);
   }
   switch (v) {

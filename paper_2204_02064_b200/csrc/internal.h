@@ -9,8 +9,10 @@
 
 namespace perks {
 
-// General 2D point sets (any radius <= 6, any order, <= 64 points) run on the k2d_wide.cu kernels.
+// General point sets run on the k2d_wide.cu (2D: radius <= 6) and k3d_wide.cu (3D: radius <= 3)
+// kernels (any order, <= 64 points).
 constexpr int SHAPE_G2D = 100;
+constexpr int SHAPE_G3D = 101;
 constexpr int kMaxPoints2D = 64;
 
 struct Problem {
@@ -22,7 +24,8 @@ struct Problem {
   int npts;
   double wd[kMaxPoints2D];  // weights rounded to f64 (identity)
   float wf[kMaxPoints2D];   // weights rounded once to f32 (reading R6)
-  int16_t off[kMaxPoints2D][2];  // (dx, dy) of each point (SHAPE_G2D)
+  int16_t off[kMaxPoints2D][2];  // (dx, dy) of each point (SHAPE_G2D / G3D)
+  int16_t off3z[kMaxPoints2D];   // dz of each point (SHAPE_G3D)
   int device;
   int rank = 0, nranks = 1;  // multi-GPU slab decomposition along z
   int num_sms;
@@ -101,6 +104,11 @@ cudaError_t run_perks2d_strip(const Problem &p, const Plan &pl, const void *in, 
 // Any variant for general 2D point sets of radius <= 6 (k2d_wide.cu).
 Plan plan_wide2d(const Problem &p, perks_variant v);
 cudaError_t run_wide2d(const Problem &p, const Plan &pl, const void *in, void *out, void *ws, int64_t steps,
+                       cudaStream_t s);
+
+// Any variant for general 3D point sets of radius <= 3 (k3d_wide.cu; PERKS = the persistent body).
+Plan plan_wide3d(const Problem &p, perks_variant v);
+cudaError_t run_wide3d(const Problem &p, const Plan &pl, const void *in, void *out, void *ws, int64_t steps,
                        cudaStream_t s);
 
 // Environment override helper (sweeps only): returns def if unset.

@@ -138,6 +138,18 @@ def preset(name: str):
                         continue
                     offs.append((dx, dy, dz))
                     w.append({0: 1 / 4, 1: 1 / 16, 2: 1 / 32}[m])
+    elif name == "3d13pt":
+        # Table II 3d13pt(2,26): the radius-2 3D star, (dz,dy,dx) lexicographic; dyadic convex
+        # weights: centre 1/16, distance 1 1/8, distance 2 1/32 (sum exactly 1)
+        offs, w = [], []
+        for dz in range(-2, 3):
+            for dy in range(-2, 3):
+                for dx in range(-2, 3):
+                    if (dx != 0) + (dy != 0) + (dz != 0) > 1:
+                        continue
+                    k = abs(dx) + abs(dy) + abs(dz)
+                    offs.append((dx, dy, dz))
+                    w.append({0: 1 / 16, 1: 1 / 8, 2: 1 / 32}[k])
     elif name in STAR_RADIUS:
         # Table II high-order stars 2ds9pt / 2d13pt / 2d17pt / 2d21pt / 2ds25pt (radius 2..6):
         # the 4r+1 points (0,dy) and (dx,0), (dy,dx) lexicographic; dyadic convex weights: centre
@@ -166,7 +178,7 @@ def preset(name: str):
 
 
 STAR_RADIUS = {"2ds9pt": 2, "2d13pt": 3, "2d17pt": 4, "2d21pt": 5, "2ds25pt": 6}
-PRESET_NDIM = {"2d5pt": 2, "2d9pt": 2, "3d7pt": 3, "3d27pt": 3, "3d19pt": 3, "2d25pt": 2,
+PRESET_NDIM = {"2d5pt": 2, "2d9pt": 2, "3d7pt": 3, "3d27pt": 3, "3d19pt": 3, "2d25pt": 2, "3d13pt": 3,
                **{k: 2 for k in STAR_RADIUS}}
 
 

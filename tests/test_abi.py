@@ -63,9 +63,9 @@ def test_create_validation_without_gpu():
     assert _create(2, (8, 8, 1), o7, w7) == "PERKS_ERR_INVALID_ARGUMENT"       # dz in 2D
     assert _create(2, (8, 8, 1), o5, w5, dtype=7) == "PERKS_ERR_INVALID_ARGUMENT"
     assert _create(2, (8, 8, 1), o5, [1.0, float("nan"), 0, 0, 0]) == "PERKS_ERR_INVALID_ARGUMENT"
-    # 3D point sets without a specialised kernel are unsupported; 2D ones run on the general
-    # kernels up to radius 6 (k2d_wide.cu)
-    assert _create(3, (8, 8, 8), o7[::-1], w7[::-1]) == "PERKS_ERR_UNSUPPORTED"
+    # point sets without a specialised kernel run on the general kernels up to radius 6 (2D,
+    # k2d_wide.cu) / 3 (3D, k3d_wide.cu); beyond that they are unsupported
+    assert _create(3, (12, 12, 12), [(0, 0, 4), (0, 0, 0)], [0.5, 0.5]) == "PERKS_ERR_UNSUPPORTED"  # 3D r = 4
     assert _create(2, (20, 20, 1), [(7, 0, 0), (0, 0, 0)], [0.5, 0.5]) == "PERKS_ERR_UNSUPPORTED"  # r = 7
     assert _create(2, (8, 8, 1), o5, w5, bc=1) == "PERKS_ERR_UNSUPPORTED"      # PERIODIC on GPU
 

@@ -76,13 +76,13 @@ def test_shift_closed_form(dtype, axis, sign):
 
 @pytest.mark.parametrize("dtype", DT)
 @pytest.mark.parametrize("name", ["2d5pt", "2d9pt", "3d7pt", "3d27pt", "3d19pt", "2ds9pt", "2d13pt",
-                                  "2d17pt", "2d21pt", "2ds25pt", "2d25pt"])
+                                  "2d17pt", "2d21pt", "2ds25pt", "2d25pt", "3d13pt"])
 @pytest.mark.parametrize("bc", [oracle.BC_FRAME, oracle.BC_PERIODIC])
 def test_constant_preserved(dtype, name, bc):
     """Dyadic presets sum to exactly 1 -> a constant field is a fixed point."""
     offs, w = si.preset(name)
     assert sum(Fraction(x) for x in w) == 1
-    shape = (15, 17) if si.PRESET_NDIM[name] == 2 else (5, 6, 7)  # >= 2r+1 for r <= 6
+    shape = (15, 17) if si.PRESET_NDIM[name] == 2 else (5, 6, 7)  # >= 2r+1 (r <= 6 in 2D, 2 in 3D)
     u = np.full(shape, 1.5, dtype=dtype)
     out = oracle.run(u, offs, w, 13, bc=bc)
     assert np.all(out == dtype(1.5))
@@ -96,7 +96,7 @@ def _lambda_hat(offs, w, k):
 
 
 @pytest.mark.parametrize("name", ["2d5pt", "2d9pt", "3d7pt", "3d27pt", "3d19pt", "2ds9pt", "2d13pt",
-                                  "2ds25pt", "2d25pt", "rand2d", "rand3d"])
+                                  "2ds25pt", "2d25pt", "3d13pt", "rand2d", "rand3d"])
 def test_fourier_mode_decay(name):
     """PERIODIC: u0 = c0 + A·cos(k·x) -> u_T = c0·(Σw)^T + A·Re(λ̂(k)^T e^{ik·x}),
     λ̂(k) = Σ_p w_p e^{i k·d_p}.  Non-symmetric random weights make λ̂ complex, which
