@@ -3,12 +3,16 @@
 // with a compile-time point set).  The FMA chain follows the list order (reading R5), so results
 // are bit-identical to the oracle and across variants.
 //
-// One CTA computes a 32 x 8 x 8 output block from a shared-memory copy of the block plus its r-wide
-// halo shell (loaded from L2/HBM each step); 256 threads sweep the block x-fastest.  A double-buffered cp.async
-// variant of the persistent kernel was measured slower (3d13pt f64 256^3: 231.9 vs 200.8 us/step —
-// it halves occupancy).  (c) runs the
-// persistent kernel with an empty on-chip cache split — the 3D policy of k3d_stream.cu, measured
-// there: on B200 the 126 MB L2 serves what an on-chip plane cache would.
+// One CTA owns a 32 x 16 (x, y) column of outputs and a chunk of KW3_ZC planes in z (one thread per
+// (x, y)); it streams the input planes z0-r .. z0+ZC-1+r through a ring of 2r+1+LA shared-memory planes
+// ((32+2r) x (16+2r), cp.async, zero outside the domain): planes z+r+1 .. z+r+LA are in flight
+// while output plane z is computed from the 2r+1 resident planes.  Every input plane is read once per chunk
+// ((16+2r)/16 x (32+2r)/32 x (ZC+2r)/ZC re-reads, served by the 126 MB L2).  (b) loops the units
+// with a grid barrier per step (zig-zag order: odd steps run the units in reverse, so a step starts
+// where the previous one ended, in L2 — [draft] P:395-404); (c) runs it with an empty on-chip cache
+// split, the 3D policy of k3d_stream.cu measured there.  An earlier block kernel
+// (32x8x8 output block + shell per CTA, no streaming) ran 3d13pt fp64 256^3 at 182.3 / 200.8 us/step
+// (host loop / persistent); a double-buffered variant of it was slower still (231.9).
 #include <algorithm>
 #include <cstdio>
 
@@ -17,7 +21,13 @@
 
 namespace perks {
 
-constexpr int KW3_THREADS = 256, KW3_TX = 32, KW3_TY = 8, KW3_TZ = 8, KW3_MAXR = 3;
+constexpr int KW3_TX = 32, KW3_TY = 16, KW3_THREADS = KW3_TX * KW3_TY, KW3_ZC = 32, KW3_MAXR = 3;
+// planes in flight ahead of the one being waited for (one-plane lookahead ran 3d13pt fp64 256^3 at
+// 176.5 us/step: each CTA waited out an L2/HBM round trip per plane)
+#ifndef PERKS_W3_LA
+#define PERKS_W3_LA 4
+#endif
+constexpr int KW3_LA = PERKS_W3_LA;
 
 template <typename T> struct WideCoef3 {
   int n;
@@ -36,66 +46,123 @@ template <> struct WideSet3<1> {
   static constexpr __host__ __device__ int dx(int p) { return p >= 4 && p < 9 ? p - 6 : 0; }
 };
 
-template <typename T, int PS>
-__device__ __forceinline__ T cell3(const T *s, int PX, int PXY, int r, int lx, int ly, int lz, int x, int y, int z,
-                                   int nx, int ny, int nz, const WideCoef3<T> &c) {
-  if constexpr (PS == 0) {
-    const T *ctr = s + (size_t)(lz + r) * PXY + (ly + r) * PX + (lx + r);
-    if (x < r || x >= nx - r || y < r || y >= ny - r || z < r || z >= nz - r) return *ctr;
-    T acc = mul_rn(c.w[0], ctr[c.dz[0] * PXY + c.dy[0] * PX + c.dx[0]]);
-    for (int p = 1; p < c.n; p++) acc = fma_rn(c.w[p], ctr[c.dz[p] * PXY + c.dy[p] * PX + c.dx[p]], acc);
-    return acc;
-  } else {
-    using WS = WideSet3<PS>;
-    constexpr int R = WS::R, QX = KW3_TX + 2 * R, QXY = QX * (KW3_TY + 2 * R);
-    const T *ctr = s + (lz + R) * QXY + (ly + R) * QX + (lx + R);
-    if (x < R || x >= nx - R || y < R || y >= ny - R || z < R || z >= nz - R) return *ctr;
-    T acc = mul_rn(c.w[0], ctr[WS::dz(0) * QXY + WS::dy(0) * QX + WS::dx(0)]);
-#pragma unroll
-    for (int p = 1; p < WS::N; p++) acc = fma_rn(c.w[p], ctr[WS::dz(p) * QXY + WS::dy(p) * QX + WS::dx(p)], acc);
-    return acc;
-  }
-}
-
-// One block of one step: src -> shared memory (zero outside the domain) -> dst.
-template <typename T, int PS>
-__device__ void block3(const T *__restrict__ src, T *__restrict__ dst, int nx, int ny, int nz, int bx, int by,
-                       int bz, int r, const WideCoef3<T> &c, T *s) {
-  const int PX = KW3_TX + 2 * r, PY = KW3_TY + 2 * r, PZ = KW3_TZ + 2 * r, PXY = PX * PY;
-  const int x0 = bx * KW3_TX, y0 = by * KW3_TY, z0 = bz * KW3_TZ;
-  for (int i = threadIdx.x; i < PXY * PZ; i += blockDim.x) {
-    const int lz = i / PXY, rem = i % PXY, ly = rem / PX, lx = rem % PX;
-    const int x = x0 - r + lx, y = y0 - r + ly, z = z0 - r + lz;
-    s[i] = (x >= 0 && x < nx && y >= 0 && y < ny && z >= 0 && z < nz)
-               ? __ldcg(src + ((size_t)z * ny + y) * nx + x) : T(0);
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < KW3_TX * KW3_TY * KW3_TZ; i += blockDim.x) {
-    const int lz = i / (KW3_TX * KW3_TY), rem = i % (KW3_TX * KW3_TY), ly = rem / KW3_TX, lx = rem % KW3_TX;
-    const int x = x0 + lx, y = y0 + ly, z = z0 + lz;
-    if (x < nx && y < ny && z < nz)
-      dst[((size_t)z * ny + y) * nx + x] = cell3<T, PS>(s, PX, PXY, r, lx, ly, lz, x, y, z, nx, ny, nz, c);
-  }
-  __syncthreads();
-}
-
 struct Blocks3 {
   int bx, by, bz;
 };
 
+// This thread's share of a plane window: up to KW3_CPT elements (smem index, x-y offset in the
+// field, inside the x-y domain?), the same for every plane of the unit (no per-plane division).
+constexpr int KW3_CPT = 2;  // (32+2r)(16+2r) <= 2 * 512 for r <= 3
+struct PlaneCopy {
+  int sidx[KW3_CPT];
+  int gxy[KW3_CPT];  // -1: outside the x-y domain or beyond the window
+};
+PERKS_DEVINL PlaneCopy plane_copy(int nx, int ny, int x0, int y0, int r) {
+  const int PX = KW3_TX + 2 * r, PXY = PX * (KW3_TY + 2 * r);
+  PlaneCopy pc;
+#pragma unroll
+  for (int k = 0; k < KW3_CPT; k++) {
+    const int i = threadIdx.x + k * KW3_THREADS;
+    const int ly = i / PX, lx = i - ly * PX;
+    const int x = x0 - r + lx, y = y0 - r + ly;
+    pc.sidx[k] = i;
+    pc.gxy[k] = (i < PXY && x >= 0 && x < nx && y >= 0 && y < ny) ? y * nx + x : (i < PXY ? -1 : -2);
+  }
+  return pc;
+}
+// Issue the cp.async copies of input plane z into s (one commit group); zero outside the domain.
+template <typename T>
+PERKS_DEVINL void load_plane3(const T *__restrict__ src, T *s, const PlaneCopy &pc, int nx, int ny, int nz, int z) {
+  const bool zok = z >= 0 && z < nz;
+  const T *pz = src + (size_t)(zok ? z : 0) * nx * ny;
+#pragma unroll
+  for (int k = 0; k < KW3_CPT; k++) {
+    if (pc.gxy[k] == -2) continue;
+    const bool ok = zok && pc.gxy[k] >= 0;
+    cp_async<(int)sizeof(T)>(s + pc.sidx[k], ok ? pz + pc.gxy[k] : src, ok);
+  }
+  cp_async_commit();
+}
+
+// One unit (32 x 16 columns x ZC planes) of one step: src -> dst.  One CTA barrier per plane: after
+// it every warp has finished the previous plane, so the slot of plane z-r-1 can be refilled.
+template <typename T, int PS>
+__device__ void unit3(const T *__restrict__ src, T *__restrict__ dst, int nx, int ny, int nz, int ux, int uy, int z0,
+                      int z1, int r, const WideCoef3<T> &c, T *ring) {
+  const int PX = KW3_TX + 2 * r, PXY = PX * (KW3_TY + 2 * r), NP = 2 * r + 1 + KW3_LA;
+  const int x0 = ux * KW3_TX, y0 = uy * KW3_TY;
+  const int lx = threadIdx.x % KW3_TX, ly = threadIdx.x / KW3_TX;
+  const int x = x0 + lx, y = y0 + ly;
+  const bool own = x < nx && y < ny;
+  const bool inner_xy = x >= r && x < nx - r && y >= r && y < ny - r;
+  const int cell = (ly + r) * PX + (lx + r);  // this thread's centre within a plane
+  const PlaneCopy pc = plane_copy(nx, ny, x0, y0, r);
+  // ring slot of input plane zz: (zz - (z0 - r)) mod NP; planes z0-r .. z0+r+LA-1 first (one
+  // commit group each; planes past the chunk's last need are empty groups)
+  for (int q = 0; q < 2 * r + KW3_LA; q++) {
+    if (z0 - r + q < z1 + r) load_plane3(src, ring + q * PXY, pc, nx, ny, nz, z0 - r + q);
+    else cp_async_commit();
+  }
+  __syncthreads();  // the previous unit's last plane is read by every warp before its slots refill
+  int base = 0;     // slot of plane z - r
+  for (int z = z0; z < z1; z++) {
+    cp_async_wait<KW3_LA - 1>();  // plane z + r has landed
+    __syncthreads();
+    {
+      int sn = base + 2 * r + KW3_LA;  // plane z + r + LA -> the slot of plane z - r - 1
+      if (sn >= NP) sn -= NP;
+      if (z + r + KW3_LA < z1 + r) load_plane3(src, ring + sn * PXY, pc, nx, ny, nz, z + r + KW3_LA);
+      else cp_async_commit();
+    }
+    if (own) {
+      const bool inner = inner_xy && z >= r && z < nz - r;
+      int sc = base + r;
+      if (sc >= NP) sc -= NP;
+      T v;
+      if (!inner) {
+        v = ring[sc * PXY + cell];  // frame (reading R1)
+      } else if constexpr (PS == 0) {
+        auto at = [&](int p) {
+          int sl = base + r + c.dz[p];
+          if (sl >= NP) sl -= NP;
+          return ring[sl * PXY + cell + c.dy[p] * PX + c.dx[p]];
+        };
+        v = mul_rn(c.w[0], at(0));
+        for (int p = 1; p < c.n; p++) v = fma_rn(c.w[p], at(p), v);
+      } else {
+        using WS = WideSet3<PS>;
+        constexpr int R = WS::R, QX = KW3_TX + 2 * R, QXY = QX * (KW3_TY + 2 * R), QP = 2 * R + 1 + KW3_LA;
+        const T *pl[2 * R + 1];
+#pragma unroll
+        for (int k = 0; k <= 2 * R; k++) {
+          int sl = base + k;
+          if (sl >= QP) sl -= QP;
+          pl[k] = ring + sl * QXY + cell;
+        }
+        v = mul_rn(c.w[0], pl[WS::dz(0) + R][WS::dy(0) * QX + WS::dx(0)]);
+#pragma unroll
+        for (int p = 1; p < WS::N; p++) v = fma_rn(c.w[p], pl[WS::dz(p) + R][WS::dy(p) * QX + WS::dx(p)], v);
+      }
+      dst[((size_t)z * ny + y) * nx + x] = v;
+    }
+    if (++base == NP) base = 0;
+  }
+  cp_async_wait<0>();
+}
+
 template <typename T, int PS>
 __global__ void __launch_bounds__(KW3_THREADS) wide3_hostloop_kernel(const T *__restrict__ src, T *__restrict__ dst,
-                                                                     int nx, int ny, int nz, Blocks3 b, int r,
+                                                                     int nx, int ny, int nz, Blocks3 b, int zc, int r,
                                                                      const __grid_constant__ WideCoef3<T> c) {
   extern __shared__ __align__(16) unsigned char kw3_smem[];
-  const int id = blockIdx.x;
-  block3<T, PS>(src, dst, nx, ny, nz, id % b.bx, (id / b.bx) % b.by, id / (b.bx * b.by), r, c,
-                reinterpret_cast<T *>(kw3_smem));
+  const int id = blockIdx.x, z0 = (id / (b.bx * b.by)) * zc;
+  unit3<T, PS>(src, dst, nx, ny, nz, id % b.bx, (id / b.bx) % b.by, z0, min(z0 + zc, nz), r, c,
+               reinterpret_cast<T *>(kw3_smem));
 }
 
 template <typename T, int PS>
 __global__ void __launch_bounds__(KW3_THREADS) wide3_persistent_kernel(const T *__restrict__ in, T *out, T *tmp,
-                                                                       int nx, int ny, int nz, Blocks3 b, int r,
+                                                                       int nx, int ny, int nz, Blocks3 b, int zc, int r,
                                                                        int64_t steps, unsigned *bar,
                                                                        const __grid_constant__ WideCoef3<T> c) {
   extern __shared__ __align__(16) unsigned char kw3_smem[];
@@ -103,9 +170,13 @@ __global__ void __launch_bounds__(KW3_THREADS) wide3_persistent_kernel(const T *
   for (int64_t t = 0; t < steps; t++) {
     const T *src = t == 0 ? in : ((((steps - t) & 1) == 0) ? out : tmp);
     T *dst = (((steps - 1 - t) & 1) == 0) ? out : tmp;
-    for (int id = blockIdx.x; id < nb; id += gridDim.x)
-      block3<T, PS>(src, dst, nx, ny, nz, id % b.bx, (id / b.bx) % b.by, id / (b.bx * b.by), r, c,
-                    reinterpret_cast<T *>(kw3_smem));
+    // units strided over the grid (concurrent CTAs share halos in L2); odd steps in reverse order
+    for (int i = blockIdx.x; i < nb; i += gridDim.x) {
+      const int id = (t & 1) ? nb - 1 - i : i;
+      const int z0 = (id / (b.bx * b.by)) * zc;
+      unit3<T, PS>(src, dst, nx, ny, nz, id % b.bx, (id / b.bx) % b.by, z0, min(z0 + zc, nz), r, c,
+                   reinterpret_cast<T *>(kw3_smem));
+    }
     if (t + 1 < steps) grid_barrier(bar, (unsigned)((t + 1) * gridDim.x));
   }
 }
@@ -140,8 +211,8 @@ template <typename T> void *wk3(bool hostloop, int ps) {
   if (hostloop) return ps == 1 ? (void *)wide3_hostloop_kernel<T, 1> : (void *)wide3_hostloop_kernel<T, 0>;
   return ps == 1 ? (void *)wide3_persistent_kernel<T, 1> : (void *)wide3_persistent_kernel<T, 0>;
 }
-size_t smem3(int r, size_t S) {
-  return (size_t)(KW3_TX + 2 * r) * (KW3_TY + 2 * r) * (KW3_TZ + 2 * r) * S;
+size_t smem3(int r, size_t S) {  // the ring: 2r+1+LA planes of (32+2r) x (16+2r)
+  return (size_t)(2 * r + 1 + KW3_LA) * (KW3_TX + 2 * r) * (KW3_TY + 2 * r) * S;
 }
 }  // namespace
 
@@ -168,22 +239,33 @@ Plan plan_wide3d(const Problem &p, perks_variant v) {
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, KW3_THREADS, smem);
   if (occ < 1) { pl.why = "wide3d: not resident"; return pl; }
-  const int bx = (int)((p.nx + KW3_TX - 1) / KW3_TX), by = (int)((p.ny + KW3_TY - 1) / KW3_TY),
-            bz = (int)((p.nz + KW3_TZ - 1) / KW3_TZ);
+  const int bx = (int)((p.nx + KW3_TX - 1) / KW3_TX), by = (int)((p.ny + KW3_TY - 1) / KW3_TY);
+  // z-chunk length: balance the units over the resident CTAs (whole waves) against the 2r-plane
+  // re-read per chunk
+  const int64_t G = (int64_t)occ * p.num_sms;
+  int zc = KW3_ZC;
+  double best = -1;
+  for (int z = 16; z <= 64; z++) {
+    const int64_t u = (int64_t)bx * by * ((p.nz + z - 1) / z);
+    const double eff = (double)u / (double)(((u + G - 1) / G) * G) * (double)z / (double)(z + 2 * r);
+    if (eff > best + 1e-9) { best = eff; zc = z; }
+  }
+  const int bz = (int)((p.nz + zc - 1) / zc);
   const int64_t blocks = (int64_t)bx * by * bz;
   pl.units = blocks;
-  pl.grid = hostloop ? (int)blocks : (int)std::min<int64_t>(blocks, (int64_t)occ * p.num_sms);
+  // persistent: every resident CTA, each with an equal share of the planes
+  pl.grid = hostloop ? (int)blocks : (int)std::min<int64_t>(blocks, G);
   pl.block = KW3_THREADS;
   pl.ctas_per_sm = occ;
-  pl.tile[0] = KW3_TX; pl.tile[1] = KW3_TY; pl.tile[2] = KW3_TZ;
+  pl.tile[0] = KW3_TX; pl.tile[1] = KW3_TY; pl.tile[2] = zc;
   pl.regs = fa.numRegs;
   pl.smem = (int)smem;
   pl.cfg = ps;
   pl.family = 5;  // (wide 3D)
   const double S = (double)p.elem();
   pl.dram_bytes_step = 2.0 * S * (double)p.cells();
-  pl.halo_bytes_step = S * (double)blocks *
-                       ((double)smem3(r, 1) - (double)KW3_TX * KW3_TY * KW3_TZ);
+  pl.halo_bytes_step = S * (double)blocks *  // window re-reads per unit (L2)
+                       ((double)(KW3_TX + 2 * r) * (KW3_TY + 2 * r) * (zc + 2 * r) - (double)KW3_TX * KW3_TY * zc);
   pl.ws_bytes = align256((size_t)p.cells() * p.elem()) + (hostloop ? 0 : 256);
   snprintf(pl.name, sizeof(pl.name), "%s3d_wide_r%d_%dpt%s_%s%s", v == PERKS_PERKS ? "perks" : hostloop ? "hostloop" : "persistent",
            r, p.npts, ps ? "" : "_any", f32 ? "f32" : "f64", v == PERKS_PERKS ? "_c0" : "");
@@ -198,15 +280,16 @@ cudaError_t run_wide3_t(const Problem &p, const Plan &pl, const T *in, T *out, v
   const WideCoef3<T> c = make_coef3<T>(p);
   int r = radius3d(p);
   int nx = (int)p.nx, ny = (int)p.ny, nz = (int)p.nz;
-  Blocks3 b{(nx + KW3_TX - 1) / KW3_TX, (ny + KW3_TY - 1) / KW3_TY, (nz + KW3_TZ - 1) / KW3_TZ};
+  int zc = pl.tile[2];
+  Blocks3 b{(nx + KW3_TX - 1) / KW3_TX, (ny + KW3_TY - 1) / KW3_TY, (nz + zc - 1) / zc};
   T *tmp = (T *)ws;
   void *k = wk3<T>(pl.variant == PERKS_HOSTLOOP, pl.cfg);
   if (pl.variant == PERKS_HOSTLOOP) {
     for (int64_t t = 0; t < steps; t++) {
       const T *src = t == 0 ? in : ((((steps - t) & 1) == 0) ? out : tmp);
       T *dst = (((steps - 1 - t) & 1) == 0) ? out : tmp;
-      void *args[] = {(void *)&src, (void *)&dst, (void *)&nx, (void *)&ny, (void *)&nz, (void *)&b, (void *)&r,
-                      (void *)&c};
+      void *args[] = {(void *)&src, (void *)&dst, (void *)&nx, (void *)&ny, (void *)&nz, (void *)&b, (void *)&zc,
+                      (void *)&r, (void *)&c};
       cudaError_t e = cudaLaunchKernel(k, dim3(pl.grid), dim3(KW3_THREADS), args, pl.smem, s);
       if (e != cudaSuccess) return e;
     }
@@ -216,7 +299,7 @@ cudaError_t run_wide3_t(const Problem &p, const Plan &pl, const T *in, T *out, v
   cudaError_t e = cudaMemsetAsync(bar, 0, 256, s);
   if (e != cudaSuccess) return e;
   void *args[] = {(void *)&in, (void *)&out, (void *)&tmp, (void *)&nx, (void *)&ny, (void *)&nz, (void *)&b,
-                  (void *)&r, (void *)&steps, (void *)&bar, (void *)&c};
+                  (void *)&zc, (void *)&r, (void *)&steps, (void *)&bar, (void *)&c};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(pl.grid);
   cfg.blockDim = dim3(KW3_THREADS);
