@@ -46,6 +46,15 @@ template <> struct WideSet3<1> {
   static constexpr __host__ __device__ int dx(int p) { return p >= 4 && p < 9 ? p - 6 : 0; }
 };
 
+// Do all out-of-plane points of the set lie on the thread's own z column (dx = dy = 0)?  Then the
+// column values of planes z-R .. z+R live in registers (2.5D blocking) and only plane z's in-plane
+// neighbours are read from shared memory (3d13pt: 9 shared-memory loads per cell instead of 13).
+template <int PS> constexpr bool column_only_dz() {
+  for (int p = 0; p < WideSet3<PS>::N; p++)
+    if (WideSet3<PS>::dz(p) != 0 && (WideSet3<PS>::dx(p) != 0 || WideSet3<PS>::dy(p) != 0)) return false;
+  return true;
+}
+
 struct Blocks3 {
   int bx, by, bz;
 };
@@ -105,9 +114,22 @@ __device__ void unit3(const T *__restrict__ src, T *__restrict__ dst, int nx, in
   }
   __syncthreads();  // the previous unit's last plane is read by every warp before its slots refill
   int base = 0;     // slot of plane z - r
+  constexpr bool COL = PS != 0 && column_only_dz<PS != 0 ? PS : 1>();
+  constexpr int CR = PS != 0 ? WideSet3<PS != 0 ? PS : 1>::R : 0;
+  T col[2 * CR + 1];  // COL: own-column values of planes z-R .. z+R
   for (int z = z0; z < z1; z++) {
     cp_async_wait<KW3_LA - 1>();  // plane z + r has landed
     __syncthreads();
+    if constexpr (COL) {
+      constexpr int QXY = (KW3_TX + 2 * CR) * (KW3_TY + 2 * CR), QP = 2 * CR + 1 + KW3_LA;
+      if (z == z0) {
+#pragma unroll
+        for (int k = 0; k < 2 * CR; k++) col[k] = ring[(base + k) * QXY + cell];  // base = 0 here
+      }
+      int sl = base + 2 * CR;
+      if (sl >= QP) sl -= QP;
+      col[2 * CR] = ring[sl * QXY + cell];
+    }
     {
       int sn = base + 2 * r + KW3_LA;  // plane z + r + LA -> the slot of plane z - r - 1
       if (sn >= NP) sn -= NP;
@@ -121,6 +143,17 @@ __device__ void unit3(const T *__restrict__ src, T *__restrict__ dst, int nx, in
       T v;
       if (!inner) {
         v = ring[sc * PXY + cell];  // frame (reading R1)
+      } else if constexpr (COL) {
+        using WS = WideSet3<PS>;
+        constexpr int R = WS::R, QX = KW3_TX + 2 * R, QXY = QX * (KW3_TY + 2 * R);
+        const T *pz = ring + sc * QXY + cell;
+        auto at = [&](int p) -> T {
+          if (WS::dz(p) != 0 || (WS::dx(p) == 0 && WS::dy(p) == 0)) return col[WS::dz(p) + R];
+          return pz[WS::dy(p) * QX + WS::dx(p)];
+        };
+        v = mul_rn(c.w[0], at(0));
+#pragma unroll
+        for (int p = 1; p < WS::N; p++) v = fma_rn(c.w[p], at(p), v);
       } else if constexpr (PS == 0) {
         auto at = [&](int p) {
           int sl = base + r + c.dz[p];
@@ -144,6 +177,10 @@ __device__ void unit3(const T *__restrict__ src, T *__restrict__ dst, int nx, in
         for (int p = 1; p < WS::N; p++) v = fma_rn(c.w[p], pl[WS::dz(p) + R][WS::dy(p) * QX + WS::dx(p)], v);
       }
       dst[((size_t)z * ny + y) * nx + x] = v;
+    }
+    if constexpr (COL) {
+#pragma unroll
+      for (int k = 0; k < 2 * CR; k++) col[k] = col[k + 1];
     }
     if (++base == NP) base = 0;
   }
