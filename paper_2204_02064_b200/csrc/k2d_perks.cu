@@ -172,8 +172,28 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
       sm[(is_l ? pc : 0) + o_colL + o_colL_step * r] = v[0];
       sm[(is_r ? pc : 0) + o_colR + o_colR_step * r] = v[V - 1];
     }
-    if (g_l) LL<T>::put(g + (2 * TX + yr0 + r) * W, v[0], tag);
-    if (g_r) LL<T>::put(g + (2 * TX + TY + yr0 + r) * W, v[V - 1], tag);
+    // tile-edge columns: WX > 1 publishes them once per step from the column buffers (flush_cols);
+    // one warp per row band has no column buffer and publishes row by row
+    if constexpr (WX == 1) {
+      if (g_l) LL<T>::put(g + (2 * TX + yr0 + r) * W, v[0], tag);
+      if (g_r) LL<T>::put(g + (2 * TX + TY + yr0 + r) * W, v[V - 1], tag);
+    }
+  };
+  // WX > 1: after a sweep, the tile-edge warps copy their R column values (lane 0 / 31 wrote them to
+  // LEFT(0) / RIGHT(WX) of parity pb) to the exchange slot, one lane per row: one store instruction per
+  // step instead of one divergent store per row (the exchange is off the critical path:
+  // profiles/r01_c2_tile_scaling.txt)
+  auto flush_cols = [&](int pb, LLWord *g, unsigned tag) {
+    if constexpr (WX > 1) {
+      const int pc = pb * PAR_COL;
+      if (wx == 0 || wx == WX - 1) {
+        __syncwarp();
+        for (int i = lane; i < R; i += 32) {
+          if (wx == 0) LL<T>::put(g + (2 * TX + yr0 + i) * W, sm[pc + LEFT(0) + yr0 + i], tag);
+          if (wx == WX - 1) LL<T>::put(g + (2 * TX + TY + yr0 + i) * W, sm[pc + RIGHT(WX) + yr0 + i], tag);
+        }
+      }
+    }
   };
 
   // ---- TMEM rows: one warp allocates, every CTA relinquishes its permit (tmem.cuh)
@@ -224,6 +244,7 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
       vstore<T, V>(my_smc + (size_t)(r - RS0) * NT * V, v);
       publish_row(0, g0, 1u, r, v);
     }
+    flush_cols(0, g0, 1u);
   }
 
   // frame predicates (reading R1): most threads own no frame cell and skip the select
@@ -408,6 +429,7 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
       finish_row(R - 1, nv);
       vstore<T, V>(my_smc + (size_t)(R - 1 - RS0) * NT * V, nv);
     }
+    flush_cols(np, gnp, tag_out);
     // every warp signals "my part of x^{t+1}'s boundary is published": flag = (t+2)*NWARP when the
     // whole tile edge is out.  No CTA barrier here: the next step's halo phase only touches the
     // other parity's buffers, and its __syncthreads orders this step's smem edge writes.
