@@ -137,7 +137,11 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
   const int o_top = TOP(wy) + xr + 1, o_bot = BOT(wy + 1) + xr + 1;        // publish rows
   const int o_colL = is_l ? LEFT(wx) + yr0 : SCR0 + tid;                    // publish cols
   const int o_colR = is_r ? RIGHT(wx + 1) + yr0 : SCR0 + tid;
-  const int o_colL_step = is_l ? 1 : 0, o_colR_step = is_r ? 1 : 0;
+  // row strides of the column stores (1 for lanes 0 / 31, 0 for the scratch sink), opaque to the
+  // compiler so each row's address is one IMAD (base + r * step) rather than a select chain
+  int o_colL_step = is_l ? 1 : 0, o_colR_step = is_r ? 1 : 0;
+  asm volatile("" : "+r"(o_colL_step), "+r"(o_colR_step));
+  int colL_at = o_colL, colR_at = o_colR;  // + this step's parity offset (set per step)
   const int o_rdL = RIGHT(wx) + yr0, o_rdR = LEFT(wx + 1) + yr0;           // read cols
   const int o_above = BOT(wy) + xr, o_below = TOP(wy + 1) + xr;             // read rows
   const bool g_top = wy == 0, g_bot = wy == WY - 1;
@@ -169,8 +173,8 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
     // stores measured 30 % slower: 11.9 vs 9.1 us/step on C2).  One warp per tile row (WX == 1):
     // no warp has a neighbour inside the tile, nothing to store.
     if constexpr (WX > 1) {
-      sm[(is_l ? pc : 0) + o_colL + o_colL_step * r] = v[0];
-      sm[(is_r ? pc : 0) + o_colR + o_colR_step * r] = v[V - 1];
+      sm[colL_at + o_colL_step * r] = v[0];
+      sm[colR_at + o_colR_step * r] = v[V - 1];
     }
     // tile-edge columns: WX > 1 publishes them once per step from the column buffers (flush_cols);
     // one warp per row band has no column buffer and publishes row by row
@@ -250,6 +254,9 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
   // frame predicates (reading R1): most threads own no frame cell and skip the select
   const int ylo = max(0, 1 - (y0 + yr0)), yhi = min(R, ny - 1 - (y0 + yr0));
   const bool all_interior = ylo == 0 && yhi == R && x >= 1 && x + V - 1 <= nx - 2;
+  // warp-uniform: does any lane of this warp own a frame cell?  (a uniform branch per row instead of a
+  // divergent one; the selects inside stay per lane)
+  const bool warp_frame = __any_sync(0xffffffffu, !all_interior);
   unsigned xmask = 0;
 #pragma unroll
   for (int i = 0; i < V; i++) xmask |= ((x + i) >= 1 && (x + i) <= nx - 2) ? (1u << i) : 0u;
@@ -310,6 +317,8 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
     // ---- compute x^{t+1} for the thread's V x R cells (sliding window over rows)
     LLWord *gnp = GS(tile, np);
     const unsigned tag_out = (unsigned)(t + 2);
+    colL_at = o_colL + (is_l ? np * PAR_COL : 0);
+    colR_at = o_colR + (is_r ? np * PAR_COL : 0);
     T prev[V + 2], cur[V + 2], nxt[V + 2];
     // own row (old values) + x-neighbours: shuffles inside the warp; lanes 0/31 take the
     // neighbouring warp's / tile's edge column (broadcast reads, branch free)
@@ -345,11 +354,10 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
         }
         nv[i] = acc;
       }
-      if (!all_interior) {
+      if (warp_frame) {
         const bool rin = r >= ylo && r < yhi;
 #pragma unroll
-        for (int i = 0; i < V; i++)
-          if (!(rin && ((xmask >> i) & 1u))) nv[i] = cur[i + 1];
+        for (int i = 0; i < V; i++) nv[i] = (rin && ((xmask >> i) & 1u)) ? nv[i] : cur[i + 1];
       }
       publish_row(np, gnp, tag_out, r, nv, maybe_edge_row);
 #pragma unroll
