@@ -212,6 +212,7 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
     __syncthreads();
     tmem_fence_after_sync();
     tb = tmem_base_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * RT * G::WPR);
+    tb = __shfl_sync(0xffffffffu, tb, 0);  // warp-uniform by construction: lets ptxas keep it in a uniform register
   }
   auto trow = [&](int r) { return tb + (uint32_t)((r - RR) * G::WPR); };  // TMEM address of row r
 
