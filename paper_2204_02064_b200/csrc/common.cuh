@@ -19,6 +19,40 @@ PERKS_DEVINL double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 PERKS_DEVINL float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 PERKS_DEVINL double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
 
+// Packed FP32 pairs (sm_100a FFMA2 / FMUL2, PTX fma.rn.f32x2 / mul.rn.f32x2): two cells of one
+// chain term in one instruction, each lane rounded exactly as fma_rn / mul_rn (so the results stay
+// bit-identical to the scalar chain, reading R5).  B200 runs FFMA2 at the same FMA-pipe rate as
+// two FFMAs (profiles/r02_ffma2_probe.txt: 127.5 vs 124.4 FMA/clk/SM) but in HALF the issue slots:
+// the stencil bodies are issue-bound, so the freed slots go to loads, stores and bookkeeping.
+#ifndef PERKS_FFMA2
+#define PERKS_FFMA2 1
+#endif
+// 64-bit register pairs of two fp32 cells.
+using f32x2 = unsigned long long;
+PERKS_DEVINL f32x2 pack2(float a, float b) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+PERKS_DEVINL void unpack2(f32x2 p, float &a, float &b) { asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(p)); }
+// w*a + c per lane (one rounding each); the weight is broadcast to both lanes
+PERKS_DEVINL f32x2 fma2_rn(float w, f32x2 a, f32x2 c) {
+  f32x2 r;
+  asm("{\n.reg .b64 pw;\nmov.b64 pw, {%1, %1};\nfma.rn.f32x2 %0, pw, %2, %3;\n}" : "=l"(r) : "f"(w), "l"(a), "l"(c));
+  return r;
+}
+// (w.lo*a + c.lo, w.hi*a + c.hi): a weight pair times one broadcast cell
+PERKS_DEVINL f32x2 fma2_bc_rn(f32x2 w, float a, f32x2 c) {
+  f32x2 r;
+  asm("{\n.reg .b64 pa;\nmov.b64 pa, {%2, %2};\nfma.rn.f32x2 %0, %1, pa, %3;\n}" : "=l"(r) : "l"(w), "f"(a), "l"(c));
+  return r;
+}
+PERKS_DEVINL f32x2 mul2_rn(float w, f32x2 a) {
+  f32x2 r;
+  asm("{\n.reg .b64 pw;\nmov.b64 pw, {%1, %1};\nmul.rn.f32x2 %0, pw, %2;\n}" : "=l"(r) : "f"(w), "l"(a));
+  return r;
+}
+
 // A register copy the compiler cannot see through.  Used when a register-cached value is moved
 // into the stencil's sliding window: the cached SSA value then dies at the copy, so ptxas can
 // write the new value back into the same physical register instead of keeping a second copy of
