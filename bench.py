@@ -1,8 +1,10 @@
 """bench.py — the driver's benchmark contract for the PERKS stencil library on B200.
 
 One bench "step" = one pass of the whole hot path: perks_stencil_run over the full time loop
-(T time steps) of the configured workload (default: BASELINE.json configs[1] = C2, 2D 9-point
-box stencil fp32 3072x3072, T=1000 — the workload the metric is quoted on, which fits one GPU).
+(T time steps) of the configured workload.  Default: C4 = BASELINE.json configs[3], 3D 27-point
+box stencil fp32 512^3, T=500 — BASELINE.json's metric names no config, so the headline is the
+largest configuration that fits one GPU (C5 is the multi-GPU slab workload; C1-C3 and C5 are
+selectable with --config and are parity-test cases, not the headline).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mine|reference]
                     [--config C1..C5] [--variant perks|persistent|hostloop|auto]
@@ -169,8 +171,9 @@ def run_reference(args):
 
 # ----------------------------------------------------------------------------- our arm
 
-def cpu_baseline(c, budget_s=12.0):
-    """Oracle timed on the host cores on a bounded sample (rank 0, N=1 only)."""
+def cpu_baseline(c, budget_s=12.0, budget_1t_s=6.0):
+    """Oracle timed on the host cores on a bounded sample (rank 0, N=1 only): all cores
+    (OpenMP over rows) and one thread (the plain, slow oracle), SURVEY §8(d)."""
     import oracle
 
     offs, w = si.preset(c["stencil"])
@@ -183,9 +186,22 @@ def cpu_baseline(c, budget_s=12.0):
     t0 = time.perf_counter()
     oracle.run(u0, offs, w, T_s, nthreads=cores)
     dt = time.perf_counter() - t0
+    # one thread: a slab of the domain's slowest axis (rows/planes 0..k), one time step, sized to
+    # about budget_1t_s from the all-core rate (the oracle's per-cell cost is size independent)
+    per_cell_1t = dt * cores / (c["cells"] * T_s)  # estimate, refined by the measurement itself
+    n0 = c["shape"][0]
+    k = int(max(3, min(n0, budget_1t_s / max(per_cell_1t * c["cells"] / n0, 1e-12))))
+    sub = np.ascontiguousarray(u0[:k])
+    t0 = time.perf_counter()
+    oracle.run(sub, offs, w, 1, nthreads=1)
+    dt1 = time.perf_counter() - t0
+    cells1 = int(np.prod(sub.shape))
     return {"value": c["cells"] * T_s / dt / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"full domain, {T_s} of {c['steps']} time steps, {cores} OpenMP threads, "
-                      f"{dt:.1f} s"}
+                      f"{dt:.1f} s",
+            "single_thread": {"value": cells1 / dt1 / 1e9, "unit": UNIT, "cores": 1,
+                              "sample": f"{k} of {n0} slowest-axis slices x 1 time step, 1 thread, "
+                                        f"{dt1:.1f} s"}}
 
 
 def _traffic_from_profiles(kernel_prefix, config):
@@ -264,6 +280,7 @@ def run_mine(args):
     clocks = sampler.stop()
     per = [a.elapsed_time(b) for a, b in ev]
     tot_ms = sum(per)
+    best_ms, med_ms = min(per), statistics.median(per)
     if dist:
         t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
@@ -341,8 +358,24 @@ def run_mine(args):
 
     cached = (q["cached_cells_reg"] + q["cached_cells_smem"] + q["cached_cells_tmem"]
               if q["variant"] == "perks" else 0)
+    # ℙ (Eq. maxpeak) with T_sm (Eq. time_sm): D^sm_cache = the cells the plan
+    # keeps in shared memory, A_sm(KERNEL) = the kernel's own shared-memory accesses per cell and
+    # step (the paper's small-domain example counts 4): 3D plane streaming = one TMA write +
+    # the (R+2)(V+2)/(R·V) neighbourhood reads of each cell; the 2D tile kernels keep x/y
+    # neighbours in registers/shuffles (edge columns only, ~0).  B_sm = SMs x 128 B/clk x the SM
+    # clock sampled under load (P:495 convention, 108 x 128 B x 1.41 GHz on A100).
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    f_sm = (clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    B_sm = model.b_sm(sms, 128, f_sm)
+    if c["stencil"].startswith("3d"):
+        V, R = (4, 2) if S == 4 else (2, 2)
+        k_sm = 1.0 + (R + 2) * (V + 2) / (R * V)
+    else:
+        k_sm = 0.0
+    D_sm = min(q["cached_cells_smem"], cells) if q["variant"] == "perks" else 0
     proj = model.project(cells, min(cached, cells), T, S, peaks["hbm_gbs"] * 1e9,
-                         A_halo=q["halo_bytes_per_step"] / S * T)
+                         A_halo=q["halo_bytes_per_step"] / S * T, D_sm_cache=D_sm, B_sm=B_sm,
+                         A_sm_kernel=k_sm * cells * T)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per, "higher_is_better": True,
@@ -363,8 +396,13 @@ def run_mine(args):
         "us_per_time_step": 1e3 * ms_per / T,
         "hostloop_ms_per_step": hl,
         "speedup_vs_hostloop": (hl / ms_per) if hl else None,
+        "ms_per_step_best": best_ms, "ms_per_step_median": med_ms,
         "model": {"P_gcells": proj.peak_cells_per_s / 1e9,
-                  "M_over_P": (value / ws) / (proj.peak_cells_per_s / 1e9)},
+                  "M_over_P": (value / ws) / (proj.peak_cells_per_s / 1e9),
+                  "T_gm_s": proj.t_gm, "T_halo_s": proj.t_halo, "T_sm_s": proj.t_sm,
+                  "D_sm_cache": int(D_sm), "A_sm_kernel_per_cell_step": k_sm,
+                  "B_sm_gbs": B_sm / 1e9,
+                  "ref": "P:519 A_gm, P:565-571 T_sm, P:578-584 T_halo, P:587-603 T_PERKS, P"},
         "roofline": roof,
         "gpu_launches": int(launches_per_step * args.steps),
         "clocks": clocks,
@@ -387,7 +425,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
-    ap.add_argument("--config", default="C2", choices=sorted(si.CONFIGS),
+    ap.add_argument("--config", default="C4", choices=sorted(si.CONFIGS),
                     help="C5 = the slab-decomposed multi-GPU workload (N>1 under torchrun)")
     ap.add_argument("--variant", default="perks",
                     choices=["perks", "persistent", "hostloop", "auto"])

@@ -70,12 +70,6 @@ def _load():
                 f.argtypes = [ctypes.c_int, i64p, ctypes.c_int, i32p, ctypes.c_void_p,
                               ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                               ctypes.c_int]
-            for name in ("oracle_one_step_at_f64", "oracle_one_step_at_f32"):
-                f = getattr(lib, name)
-                f.restype = ctypes.c_int
-                f.argtypes = [ctypes.c_int, i64p, ctypes.c_int, i32p, ctypes.c_void_p,
-                              ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, i64p,
-                              ctypes.c_void_p]
             lib.oracle_max_threads.restype = ctypes.c_int
             _lib = lib
     return _lib
@@ -119,23 +113,6 @@ def run(u0: np.ndarray, offsets, weights, steps: int, bc: int = BC_FRAME,
     if st != 0:
         raise OracleError(st)
     return out
-
-
-def one_step_at(x: np.ndarray, offsets, weights, cells: np.ndarray, bc: int = BC_FRAME,
-                ndim: int | None = None) -> np.ndarray:
-    """One application of the operator evaluated only at linear cell indices ``cells``."""
-    lib = _load()
-    x, ndim, ext, offs, w = _prep(x, offsets, weights, ndim)
-    cells = np.ascontiguousarray(np.asarray(cells, dtype=np.int64))
-    vals = np.empty(cells.shape[0], dtype=x.dtype)
-    fn = lib.oracle_one_step_at_f64 if x.dtype == np.float64 else lib.oracle_one_step_at_f32
-    st = fn(ndim, ext.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), offs.shape[0],
-            offs.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), w.ctypes.data, int(bc),
-            x.ctypes.data, cells.shape[0], cells.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
-            vals.ctypes.data)
-    if st != 0:
-        raise OracleError(st)
-    return vals
 
 
 def max_threads() -> int:

@@ -179,64 +179,6 @@ int oracle_stencil_f32(int ndim, const int64_t ext[3], int npts, const int32_t *
   return ORACLE_OK;
 }
 
-/* Single-cell evaluation of x^T at one cell is not closed-form; for sampled
- * checks at full size the tests use one step (T=1) at sampled cells: */
-int oracle_one_step_at_f64(int ndim, const int64_t ext[3], int npts, const int32_t *offsets,
-                           const double *weights, int bc, const double *x, int64_t ncells,
-                           const int64_t *cells, double *vals) {
-  int r = 0;
-  int st = check_args(ndim, ext, npts, offsets, bc, 1, &r);
-  if (st != ORACLE_OK) return st;
-  const int64_t nx = ext[0], ny = ext[1], nz = ext[2];
-  for (int64_t i = 0; i < ncells; i++) {
-    const int64_t c = cells[i];
-    const int64_t xx = c % nx, yy = (c / nx) % ny, zz = c / (nx * ny);
-    int frame = 0;
-    if (bc == ORACLE_BC_FRAME) {
-      if (xx < r || xx >= nx - r || yy < r || yy >= ny - r) frame = 1;
-      if (ndim == 3 && (zz < r || zz >= nz - r)) frame = 1;
-    }
-    if (frame) { vals[i] = x[c]; continue; }
-    double acc = 0.0;
-    for (int p = 0; p < npts; p++) {
-      int64_t qx = xx + offsets[3 * p], qy = yy + offsets[3 * p + 1], qz = zz + offsets[3 * p + 2];
-      if (bc == ORACLE_BC_PERIODIC) { qx = wrap(qx, nx); qy = wrap(qy, ny); qz = wrap(qz, nz); }
-      const double v = x[(qz * ny + qy) * nx + qx];
-      if (p == 0) acc = weights[0] * v; else acc = fma(weights[p], v, acc);
-    }
-    vals[i] = acc;
-  }
-  return ORACLE_OK;
-}
-
-int oracle_one_step_at_f32(int ndim, const int64_t ext[3], int npts, const int32_t *offsets,
-                           const float *weights, int bc, const float *x, int64_t ncells,
-                           const int64_t *cells, float *vals) {
-  int r = 0;
-  int st = check_args(ndim, ext, npts, offsets, bc, 1, &r);
-  if (st != ORACLE_OK) return st;
-  const int64_t nx = ext[0], ny = ext[1], nz = ext[2];
-  for (int64_t i = 0; i < ncells; i++) {
-    const int64_t c = cells[i];
-    const int64_t xx = c % nx, yy = (c / nx) % ny, zz = c / (nx * ny);
-    int frame = 0;
-    if (bc == ORACLE_BC_FRAME) {
-      if (xx < r || xx >= nx - r || yy < r || yy >= ny - r) frame = 1;
-      if (ndim == 3 && (zz < r || zz >= nz - r)) frame = 1;
-    }
-    if (frame) { vals[i] = x[c]; continue; }
-    float acc = 0.0f;
-    for (int p = 0; p < npts; p++) {
-      int64_t qx = xx + offsets[3 * p], qy = yy + offsets[3 * p + 1], qz = zz + offsets[3 * p + 2];
-      if (bc == ORACLE_BC_PERIODIC) { qx = wrap(qx, nx); qy = wrap(qy, ny); qz = wrap(qz, nz); }
-      const float v = x[(qz * ny + qy) * nx + qx];
-      if (p == 0) acc = weights[0] * v; else acc = fmaf(weights[p], v, acc);
-    }
-    vals[i] = acc;
-  }
-  return ORACLE_OK;
-}
-
 int oracle_max_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

@@ -6,6 +6,8 @@
 
 #include <unistd.h>
 
+#include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -21,6 +23,19 @@ int env_int(const char *name, int def) {
   const char *v = std::getenv(name);
   if (!v || !*v) return def;
   return std::atoi(v);
+}
+
+namespace {
+__global__ void reset_bar_kernel(unsigned *bar, unsigned base) {
+  if (threadIdx.x < 64) bar[threadIdx.x] = threadIdx.x < 2 ? base : 0u;
+}
+}  // namespace
+cudaError_t reset_grid_barrier(unsigned *bar, cudaStream_t s) {
+  const char *v = std::getenv("PERKS_TEST_BAR_BASE");
+  const unsigned base = (v && *v) ? (unsigned)std::strtoul(v, nullptr, 0) : 0u;
+  if (base == 0) return cudaMemsetAsync(bar, 0, 256, s);  // (no kernel launch in the normal case)
+  reset_bar_kernel<<<1, 64, 0, s>>>(bar, base);
+  return cudaGetLastError();
 }
 }  // namespace perks
 
@@ -553,6 +568,16 @@ perks_status perks_stencil_run_group(const perks_stencil_t *hs, int n, perks_var
     drs[i].noncoop = 1;
   }
   cudaError_t e = cudaSuccess;
+  if (rv != PERKS_HOSTLOOP) {
+    // every slab's persistent grid spins on its neighbours: all grids must be resident at once
+    // (a grid that cannot start would leave the others waiting until the watchdog trap)
+    int64_t sum = 0, cap = INT64_MAX;
+    for (int i = 0; i < n; i++) {
+      sum += pls[i]->grid;
+      cap = std::min<int64_t>(cap, (int64_t)pls[i]->ctas_per_sm * ps[i]->num_sms);
+    }
+    if (sum > cap) return PERKS_ERR_NOT_CORESIDENT;
+  }
   if (rv == PERKS_HOSTLOOP) {
     e = run_stream3d_hostloop_group(ps.data(), pls.data(), d_in, d_out, d_ws, drs.data(), n, steps, s);
   } else {

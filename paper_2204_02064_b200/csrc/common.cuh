@@ -262,18 +262,25 @@ __device__ __noinline__ inline void watchdog_fire(const char *what, unsigned a, 
   __trap();
 }
 
-// Grid barrier on a monotonically increasing counter (reset to 0 before the launch).
-// Every CTA calls it with the same `target` = (barrier index + 1) * gridDim.x.
+// Grid barrier on a monotonically increasing 32-bit counter ctr[0] (ctr[1] = its value at launch,
+// set by reset_grid_barrier).  Barrier n (n = 1, 2, ...) completes when every CTA has arrived n
+// times: ctr[0] reaches ctr[1] + n * gridDim.x.  Counter and target wrap modulo 2^32 together and are
+// compared wrap-safely (the signed difference): CTAs are at most one barrier apart, so the counter
+// never trails the target by 2^31 and any step count (steps is int64) is safe.
 // CTA-level __syncthreads + one releasing arrive per CTA + acquiring spin (P:1068 grid.sync).
-PERKS_DEVINL void grid_barrier(unsigned *ctr, unsigned target) {
+PERKS_DEVINL bool grid_barrier_pending(const unsigned *ctr, unsigned target) {
+  return (int)(ld_acquire_gpu(ctr) - target) < 0;
+}
+PERKS_DEVINL void grid_barrier(unsigned *ctr, unsigned n) {
   __syncthreads();
   if (threadIdx.x == 0) {
+    const unsigned target = ld_relaxed_gpu(ctr + 1) + n * gridDim.x;
     red_release_gpu(ctr, 1u);
-    if (ld_acquire_gpu(ctr) < target) {
+    if (grid_barrier_pending(ctr, target)) {
       const unsigned long long t0 = globaltimer_ns();
-      unsigned n = 0;
-      while (ld_acquire_gpu(ctr) < target)
-        if ((++n & 1023u) == 0 && globaltimer_ns() - t0 > PERKS_WATCHDOG_NS)
+      unsigned k = 0;
+      while (grid_barrier_pending(ctr, target))
+        if ((++k & 1023u) == 0 && globaltimer_ns() - t0 > PERKS_WATCHDOG_NS)
           watchdog_fire("grid barrier", ld_acquire_gpu(ctr), target);
     }
   }

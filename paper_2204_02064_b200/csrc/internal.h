@@ -111,6 +111,10 @@ Plan plan_wide3d(const Problem &p, perks_variant v);
 cudaError_t run_wide3d(const Problem &p, const Plan &pl, const void *in, void *out, void *ws, int64_t steps,
                        cudaStream_t s);
 
+// Reset a grid-barrier block (common.cuh grid_barrier): ctr[0] = ctr[1] = base, base = 0 unless
+// PERKS_TEST_BAR_BASE sets it (tests start the counter just below 2^32 to exercise the wrap).
+cudaError_t reset_grid_barrier(unsigned *bar, cudaStream_t s);
+
 // Environment override helper (sweeps only): returns def if unset.
 int env_int(const char *name, int def);
 

@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(K2D_THREADS) persistent2d_kernel(
     T *dst = step_dst(out, tmp, t, steps);
     for (int s = gw; s < nstrips; s += nw)
       strip2d<T, S, V, RW>(src, dst, nx, ny, (s % sx) * 32 * V, (s / sx) * RW, c, lane);
-    if (t + 1 < steps) grid_barrier(bar, (unsigned)((t + 1) * gridDim.x));
+    if (t + 1 < steps) grid_barrier(bar, (unsigned)(t + 1));
   }
 }
 
@@ -206,7 +206,7 @@ static cudaError_t launch2d(const Problem &p, const Plan &pl, int V, const T *in
     return cudaSuccess;
   }
   void *k = pick_kernel(p, V, true);
-  cudaError_t e = cudaMemsetAsync(bar, 0, 256, s);
+  cudaError_t e = reset_grid_barrier(bar, s);
   if (e != cudaSuccess) return e;
   void *args[] = {(void *)&in, (void *)&out, (void *)&tmp, (void *)&nx, (void *)&ny, (void *)&sx,
                   (void *)&nstrips, (void *)&steps, (void *)&bar, (void *)&c};

@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(KW_THREADS) wide_persistent_kernel(const T *__
       tile_step<T, PS, TX, TY>(s, dst, nx, ny, x0, y0, r, c);
       __syncthreads();
     }
-    if (t + 1 < steps) grid_barrier(bar, (unsigned)((t + 1) * gridDim.x));
+    if (t + 1 < steps) grid_barrier(bar, (unsigned)(t + 1));
   }
 }
 
@@ -393,7 +393,7 @@ cudaError_t run_wide_t(const Problem &p, const Plan &pl, const T *in, T *out, vo
   if (pl.variant == PERKS_PERSISTENT) {
     T *tmp = (T *)ws;
     unsigned *bar = (unsigned *)((char *)ws + align256((size_t)p.cells() * p.elem()));
-    cudaError_t e = cudaMemsetAsync(bar, 0, 256, s);
+    cudaError_t e = reset_grid_barrier(bar, s);
     if (e != cudaSuccess) return e;
     const int ntiles = ntx * nty;
     void *args[] = {(void *)&in, (void *)&out, (void *)&tmp, (void *)&nx, (void *)&ny, (void *)&ntx,

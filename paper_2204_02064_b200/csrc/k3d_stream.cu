@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(k3d_threads<TMA, WSG>(), DIST ? 1 : wsg_minb(W
         stream_unit<T, S, G, TMA, DIST>(ring, src, &maps.box[src_idx], dst, d, x0, y0, zs, ze, c, ds);
       }
     }
-    if (t + 1 < steps) grid_barrier(bar, (unsigned)((t + 1) * gridDim.x));
+    if (t + 1 < steps) grid_barrier(bar, (unsigned)(t + 1));
   }
 
   if constexpr (CACHE) {  // epilogue: cached planes to `out` (store half of 2·D_cache)
@@ -740,7 +740,7 @@ struct Launch3 {
     void *k = pk_s<T, S>(tma, dist, cache, wsg);
     Units3 uu = u;
     uu.rev = zigzag;
-    cudaError_t e = cudaMemsetAsync(bar, 0, 256, s);
+    cudaError_t e = reset_grid_barrier(bar, s);
     if (e != cudaSuccess) return e;
     void *args[] = {(void *)&in, (void *)&out, (void *)&tmp, (void *)&maps, (void *)&d, (void *)&uu,
                     (void *)&steps, (void *)&bar, (void *)&c, (void *)&dk, (void *)&xbase, (void *)&ch};

@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(KW3_THREADS) wide3_persistent_kernel(const T *
       unit3<T, PS>(src, dst, nx, ny, nz, id % b.bx, (id / b.bx) % b.by, z0, min(z0 + zc, nz), r, c,
                    reinterpret_cast<T *>(kw3_smem));
     }
-    if (t + 1 < steps) grid_barrier(bar, (unsigned)((t + 1) * gridDim.x));
+    if (t + 1 < steps) grid_barrier(bar, (unsigned)(t + 1));
   }
 }
 
@@ -333,7 +333,7 @@ cudaError_t run_wide3_t(const Problem &p, const Plan &pl, const T *in, T *out, v
     return cudaSuccess;
   }
   unsigned *bar = (unsigned *)((char *)ws + align256((size_t)p.cells() * p.elem()));
-  cudaError_t e = cudaMemsetAsync(bar, 0, 256, s);
+  cudaError_t e = reset_grid_barrier(bar, s);
   if (e != cudaSuccess) return e;
   void *args[] = {(void *)&in, (void *)&out, (void *)&tmp, (void *)&nx, (void *)&ny, (void *)&nz, (void *)&b,
                   (void *)&zc, (void *)&r, (void *)&steps, (void *)&bar, (void *)&c};

@@ -82,6 +82,10 @@ class Stencil:
 
         return torch.float64 if self.dtype_code == _lib.F64 else torch.float32
 
+    @property
+    def np_dtype(self):
+        return np.float64 if self.dtype_code == _lib.F64 else np.float32
+
     def workspace_bytes(self, variant="auto") -> int:
         b = ctypes.c_size_t()
         check(lib.perks_stencil_workspace_bytes(self._h, _variant(variant), ctypes.byref(b)),
@@ -127,12 +131,11 @@ class Stencil:
         """Enqueue ``steps`` steps on the current torch stream; returns ``out``."""
         import torch
 
-        if not (isinstance(x, torch.Tensor) and x.is_cuda):
-            raise TypeError("x must be a CUDA tensor (use run_host for host arrays)")
-        if tuple(x.shape) != self.shape or x.dtype != self.torch_dtype or not x.is_contiguous():
-            raise ValueError("x must be a contiguous tensor of the handle's shape and dtype")
+        self._check_device_tensor(x, "x")
         if out is None:
             out = torch.empty_like(x)
+        else:
+            self._check_device_tensor(out, "out")
         v = _variant(variant)
         ws = workspace
         if ws is None and steps > 0:
@@ -145,16 +148,49 @@ class Stencil:
             ctypes.c_void_p(s.cuda_stream)), "perks_stencil_run")
         return out
 
+    def _check_device_tensor(self, t, what):
+        """A CUDA tensor of the handle's shape and dtype, dense, on the handle's device (the
+        library reads/writes cells*elem bytes through its pointer)."""
+        import torch
+
+        if not (isinstance(t, torch.Tensor) and t.is_cuda):
+            raise TypeError(f"{what} must be a CUDA tensor (use run_host for host arrays)")
+        if tuple(t.shape) != self.shape or t.dtype != self.torch_dtype or not t.is_contiguous():
+            raise ValueError(f"{what} must be a contiguous tensor of the handle's shape {self.shape} "
+                             f"and dtype {self.torch_dtype}")
+        if (t.device.index or 0) != self.device:
+            raise ValueError(f"{what} is on cuda:{t.device.index}, the handle on cuda:{self.device}")
+
+    def _check_host_array(self, a, what):
+        """A C-contiguous CPU array/tensor of the handle's shape and dtype (run_host copies
+        cells*elem bytes through its raw pointer)."""
+        import torch
+
+        if isinstance(a, np.ndarray):
+            ok = (a.shape == self.shape and a.dtype == self.np_dtype and a.flags.c_contiguous)
+        elif isinstance(a, torch.Tensor):
+            if a.is_cuda:
+                raise TypeError(f"{what} must be host memory (use run() for CUDA tensors)")
+            ok = (tuple(a.shape) == self.shape and a.dtype == self.torch_dtype and a.is_contiguous())
+        else:
+            raise TypeError(f"{what} must be a numpy array or a CPU torch tensor")
+        if not ok:
+            raise ValueError(f"{what} must be C-contiguous with the handle's shape {self.shape} and "
+                             f"dtype {np.dtype(self.np_dtype).name}")
+
     def run_host(self, x_host, steps: int, variant="auto", out=None):
         """End-to-end call with host buffers (H2D, run, D2H, synchronise) — blocking."""
         import torch
 
+        self._check_host_array(x_host, "x_host")
+        if out is not None:
+            self._check_host_array(out, "out")
         if isinstance(x_host, np.ndarray):
-            src = np.ascontiguousarray(x_host)
+            src = x_host
             dst = np.empty_like(src) if out is None else out
             p_in, p_out = src.ctypes.data, dst.ctypes.data
         else:
-            src = x_host.contiguous()
+            src = x_host
             dst = torch.empty_like(src) if out is None else out
             p_in, p_out = src.data_ptr(), dst.data_ptr()
         check(lib.perks_stencil_run_host(self._h, _variant(variant), ctypes.c_void_p(p_in),
@@ -212,8 +248,15 @@ def run_group(stencils, xs, steps, variant="auto", outs=None, stream=None):
     import torch
 
     n = len(stencils)
+    if len(xs) != n or (outs is not None and len(outs) != n):
+        raise ValueError("run_group: one input (and output) per handle")
+    for st, x in zip(stencils, xs):
+        st._check_device_tensor(x, "xs[i]")
     if outs is None:
         outs = [torch.empty_like(x) for x in xs]
+    else:
+        for st, o in zip(stencils, outs):
+            st._check_device_tensor(o, "outs[i]")
     v = _variant(variant)
     wss = [st.workspace(v) for st in stencils]
     VP = ctypes.c_void_p

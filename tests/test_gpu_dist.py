@@ -60,3 +60,38 @@ def test_many_slabs_long_run(tmp_path):
     for variant in ("persistent", "perks", "perks_cache"):
         got = _dist(tmp_path, name, shape, dtype, 4, variant, [1, 10, 5])
         assert np.array_equal(got, ref), variant
+
+
+def test_two_process_ipc_slabs(tmp_path):
+    """Two PROCESSES on one GPU, one z-slab each: the neighbour's ghost planes are mapped with
+    cudaIpcOpenMemHandle (the cross-process exchange path, api.cu), host-loop variant (each step's
+    kernel waits only for the neighbour's face counter, so time-sliced processes make progress).
+    The gathered result equals the global oracle bit-exactly."""
+    _need_gpu()
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    shape, name, dtype = (17, 24, 64), "3d7pt", np.float64
+    prefix = str(tmp_path / "slab")
+    procs = []
+    for r in range(2):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", MASTER_ADDR="127.0.0.1",
+                   MASTER_PORT=str(port))
+        cmd = [sys.executable, os.path.join(HERE, "dist_ipc_worker.py"), prefix, name,
+               *map(str, shape), "f64", "hostloop", "3", "2"]
+        procs.append(subprocess.Popen(cmd, env=env, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
+                                      text=True))
+    logs = []
+    for p in procs:
+        try:
+            out, _ = p.communicate(timeout=240)
+        except subprocess.TimeoutExpired:
+            p.kill()
+            out, _ = p.communicate()
+        logs.append(out)
+        assert p.returncode == 0, "\n".join(logs)
+    got = np.concatenate([np.load(f"{prefix}{r}.npy") for r in range(2)], axis=0)
+    offs, w = si.preset(name)
+    ref = oracle.run(si.field(shape, dtype=dtype, seed=505), offs, w, 5, nthreads=4)
+    assert np.array_equal(got, ref), f"{int(np.sum(got != ref))} cells differ"

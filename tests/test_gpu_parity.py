@@ -363,3 +363,53 @@ def test_parity_wide_3d(variant, dtype, shape):
         for T in (1, 4):
             ref = oracle.run(u0, offs, w, T, nthreads=8)
             _check(_run_gpu_offs(u0, offs, w, T, variant), ref, u0, dtype)
+
+
+@pytest.mark.parametrize("name,shape,dtype,variant", [
+    ("2d9pt", (300, 520), np.float32, "persistent"),
+    ("3d7pt", (24, 40, 64), np.float64, "persistent"),
+    ("3d27pt", (20, 36, 128), np.float32, "perks"),
+    ("2ds25pt", (200, 300), np.float32, "persistent"),
+    ("3d13pt", (20, 24, 64), np.float64, "persistent")])
+def test_grid_barrier_counter_wrap(monkeypatch, name, shape, dtype, variant):
+    """The device-wide barrier's 32-bit arrival counter wraps modulo 2^32 mid-run (ADVICE r1:
+    started just below 2^32 with PERKS_TEST_BAR_BASE) and the run stays bit-exact."""
+    _need_gpu()
+    monkeypatch.setenv("PERKS_TEST_BAR_BASE", str(2**32 - 700))
+    u0 = si.field(shape, dtype=dtype, seed=505)
+    offs, w = si.preset(name)
+    ref = oracle.run(u0, offs, w, 12, nthreads=4)
+    _check(_run_gpu(u0, name, w, 12, variant), ref, u0, dtype)
+
+
+def test_binding_validates_buffers():
+    """The binding rejects buffers whose size/type/device/layout differ from the handle's before
+    any raw pointer reaches the library."""
+    _need_gpu()
+    from paper_2204_02064_b200 import Stencil
+    from paper_2204_02064_b200.stencil import run_group
+    offs, w = si.preset("2d5pt")
+    st = Stencil((16, 16), offs, w, dtype="f64")
+    x = torch.ones((16, 16), dtype=torch.float64, device="cuda")
+    for bad in (torch.empty((16, 15), dtype=torch.float64, device="cuda"),
+                torch.empty((16, 16), dtype=torch.float32, device="cuda"),
+                torch.empty((16, 32), dtype=torch.float64, device="cuda")[:, ::2]):
+        with pytest.raises(ValueError):
+            st.run(x, 1, "hostloop", out=bad)
+    with pytest.raises(TypeError):
+        st.run(x, 1, "hostloop", out=torch.empty((16, 16), dtype=torch.float64))
+    with pytest.raises(ValueError):
+        st.run(x.float(), 1, "hostloop")
+    with pytest.raises(ValueError):
+        st.run_host(np.ones((16, 16), dtype=np.float32), 1)
+    with pytest.raises(ValueError):
+        st.run_host(np.ones((8, 16), dtype=np.float64), 1)
+    with pytest.raises(ValueError):
+        st.run_host(np.ones((16, 32), dtype=np.float64)[:, ::2], 1)
+    with pytest.raises(TypeError):
+        st.run_host(x, 1)
+    with pytest.raises(ValueError):
+        st.run_host(np.ones((16, 16)), 1, out=np.empty((16, 16), dtype=np.float32))
+    with pytest.raises(ValueError):
+        run_group([st], [x.float()], 1)
+    st.close()
