@@ -146,8 +146,12 @@ const Plan &get_plan(perks_stencil_s *h, perks_variant v) {
         if (pl.ok && env_int("PERKS_STRIP", 0)) pl.family = 3;
         else pl = plan_perks2d(p);   // square tiles
       }
-    } else if (v == PERKS_PERKS)
-      pl = plan_stream3d(p, PERKS_PERKS);
+    } else if (v == PERKS_PERKS) {
+      // domains that fit in the SMs' shared memory: resident bricks (k3d_brick.cu); larger ones:
+      // the plane-streaming persistent kernel (k3d_stream.cu).  PERKS_P3D_BRICK=0 disables bricks.
+      if (env_int("PERKS_P3D_BRICK", 1) && p.nranks == 1) pl = plan_brick3d(p);
+      if (!pl.ok) pl = plan_stream3d(p, PERKS_PERKS);
+    }
     h->plans[i] = pl;
     h->planned[i] = true;
   }
@@ -484,6 +488,8 @@ perks_status perks_stencil_run(perks_stencil_t h, perks_variant v, const void *d
         e = pl.family == 1 ? run_perks2d_cluster(p, pl, d_in, d_out, steps, s)
             : pl.family == 3 ? run_perks2d_strip(p, pl, d_in, d_out, d_ws, steps, s)
                              : run_perks2d(p, pl, d_in, d_out, d_ws, steps, s);
+      else if (pl.family == 4)
+        e = run_brick3d(p, pl, d_in, d_out, d_ws, steps, s);
       else
         e = run_stream3d(p, pl, d_in, d_out, d_ws, steps, s);
       break;

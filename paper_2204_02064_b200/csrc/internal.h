@@ -100,6 +100,10 @@ Plan plan_perks2d_strip(const Problem &p);
 cudaError_t run_perks2d_strip(const Problem &p, const Plan &pl, const void *in, void *out, void *ws,
                               int64_t steps, cudaStream_t s);
 // PERKS (c), 3D: the persistent kernel with a shared-memory plane cache (k3d_stream.cu).
+// PERKS (c), 3D domains that fit on chip: resident bricks, tagged surface exchange (k3d_brick.cu).
+Plan plan_brick3d(const Problem &p);
+cudaError_t run_brick3d(const Problem &p, const Plan &pl, const void *in, void *out, void *ws, int64_t steps,
+                        cudaStream_t s);
 
 // Any variant for general 2D point sets of radius <= 6 (k2d_wide.cu).
 Plan plan_wide2d(const Problem &p, perks_variant v);

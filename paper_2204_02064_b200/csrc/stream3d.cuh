@@ -53,7 +53,7 @@ struct Geo3D {
   static constexpr size_t BAR_BYTES = (3 * NS * 8 + 16 + 127) / 128 * 128;
   static constexpr size_t RING_BYTES = (size_t)NS * SLOT_BYTES + BAR_BYTES;
 
-  static_assert(V * (int)sizeof(T) == 16, "one 16-byte vector per thread per row");
+  static_assert(V * (int)sizeof(T) == 16 || V * (int)sizeof(T) == 8, "one 16- or 8-byte vector per thread per row");
   static_assert(NT >= 2 * ROWS, "halo-column loaders");
   static_assert(P <= 256 && ROWS <= 256, "TMA box dims <= 256");
 };
