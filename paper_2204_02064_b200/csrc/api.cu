@@ -147,9 +147,10 @@ const Plan &get_plan(perks_stencil_s *h, perks_variant v) {
         else pl = plan_perks2d(p);   // square tiles
       }
     } else if (v == PERKS_PERKS) {
-      // domains that fit in the SMs' shared memory: resident bricks (k3d_brick.cu); larger ones:
-      // the plane-streaming persistent kernel (k3d_stream.cu).  PERKS_P3D_BRICK=0 disables bricks.
-      if (env_int("PERKS_P3D_BRICK", 1) && p.nranks == 1) pl = plan_brick3d(p);
+      // resident bricks (k3d_brick.cu) are opt-in (PERKS_P3D_BRICK=1): measured slower than the
+      // plane-streaming persistent kernel on every 3D domain that fits them, because such domains
+      // also fit B200's L2 (profiles/r02_brick3d.txt); default: the streaming kernel (k3d_stream.cu)
+      if (env_int("PERKS_P3D_BRICK", 0) && p.nranks == 1) pl = plan_brick3d(p);
       if (!pl.ok) pl = plan_stream3d(p, PERKS_PERKS);
     }
     h->plans[i] = pl;

@@ -214,6 +214,41 @@ PERKS_DEVINL LLWord ld_ll(const LLWord *p) {
   asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];\n" : "=r"(w.v), "=r"(w.tag) : "l"(p) : "memory");
   return w;
 }
+// GPU-scope relaxed variants (exchange between CTAs of one launch on one device): the value/tag
+// pair still travels in one single-copy-atomic 8-byte access, without the system-scope ordering
+// of volatile accesses (which compile to .STRONG.SYS and serialise in the memory system).
+PERKS_DEVINL void st_llg(LLWord *p, unsigned v, unsigned tag) {
+  asm volatile("st.relaxed.gpu.global.v2.u32 [%0], {%1, %2};\n" ::"l"(p), "r"(v), "r"(tag) : "memory");
+}
+PERKS_DEVINL LLWord ld_llg(const LLWord *p) {
+  LLWord w;
+  asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];\n" : "=r"(w.v), "=r"(w.tag) : "l"(p) : "memory");
+  return w;
+}
+template <typename T> struct LLG;
+template <> struct LLG<float> {
+  static constexpr int WORDS = 1;
+  PERKS_DEVINL static void put(LLWord *p, float x, unsigned tag) { st_llg(p, __float_as_uint(x), tag); }
+  PERKS_DEVINL static bool get(const LLWord *p, unsigned tag, float &x) {
+    LLWord w = ld_llg(p);
+    x = __uint_as_float(w.v);
+    return w.tag == tag;
+  }
+};
+template <> struct LLG<double> {
+  static constexpr int WORDS = 2;
+  PERKS_DEVINL static void put(LLWord *p, double x, unsigned tag) {
+    const unsigned long long b = __double_as_longlong(x);
+    st_llg(p, (unsigned)b, tag);
+    st_llg(p + 1, (unsigned)(b >> 32), tag);
+  }
+  PERKS_DEVINL static bool get(const LLWord *p, unsigned tag, double &x) {
+    const LLWord a = ld_llg(p), b = ld_llg(p + 1);
+    x = __longlong_as_double((long long)(((unsigned long long)b.v << 32) | a.v));
+    return a.tag == tag && b.tag == tag;
+  }
+};
+
 template <typename T> struct LL;
 template <> struct LL<float> {
   static constexpr int WORDS = 1;

@@ -34,14 +34,20 @@
 
 namespace perks {
 
-// Brick geometries: one thread owns V x R cells of every plane (8-byte rows: V = 1 fp64, 2 fp32),
-// 8 warps, R = 2 rows: tiles of 32 x 16 (fp64) / 64 x 16 (fp32) cells.
-template <typename T> struct GBrick;
-template <> struct GBrick<double> { using G = Geo3D<double, 1, 2, 8, 2>; };
-template <> struct GBrick<float> { using G = Geo3D<float, 2, 2, 8, 2>; };
+// Brick geometries: one thread owns V x R cells of every plane, 8 warps: tiles of TX x TY cells.
+#ifndef PERKS_BRICK_R
+#define PERKS_BRICK_R 2
+#endif
+#ifndef PERKS_BRICK_V
+#define PERKS_BRICK_V 2
+#endif
+template <typename T> struct GBrick { using G = Geo3D<T, PERKS_BRICK_V, PERKS_BRICK_R, 8, 2>; };
 constexpr int kBrickThreads = 256;
 constexpr int kMaxSegs = 26;
-constexpr int kGatherMax = 20;  // halo words one thread holds in flight per pass
+#ifndef PERKS_BRICK_GMAX
+#define PERKS_BRICK_GMAX 16
+#endif
+constexpr int kGatherMax = PERKS_BRICK_GMAX;  // halo words one thread holds in flight per pass
 
 struct BrickGeo {
   int ntx, nty, nbz;  // bricks along x, y, z
@@ -49,7 +55,7 @@ struct BrickGeo {
   long long bw;       // exchange cells per brick (per parity)
 };
 
-// Exchange block of one brick (cells; x LL<T>::WORDS words): the surface of the brick.
+// Exchange block of one brick (cells; x LLG<T>::WORDS words): the surface of the brick.
 //   W/E columns [NZ][TY], low/high rows [NZ][TX], low/high z faces [TY][TX].
 template <class G> struct Sec {
   int NZ;
@@ -149,50 +155,70 @@ PERKS_DEVINL int build_segs(const BrickGeo &bg, const Dom3 &d, const BrickPos &m
 // kGatherMax tagged loads, then re-polls the words whose tag has not arrived (watchdog), and
 // writes the values into the slots.
 template <typename T>
-PERKS_DEVINL void gather(const Seg *segs, int nseg, const LLWord *ll, unsigned tag, T *slots) {
-  constexpr int W = LL<T>::WORDS;
+__device__ __noinline__ void gather(const Seg *segs, int nseg, const LLWord *ll, unsigned tag, T *slots) {
+  constexpr int W = LLG<T>::WORDS;
   const int total = nseg > 0 ? segs[nseg - 1].end : 0;
+  // element e of the list -> (segment, kz, ki); e grows with k, so the segment index only moves
+  // forward (nothing but the values is kept in registers between the passes below)
+  auto locate = [&](int e, int &si, long long &src, int &dst) {
+    while (segs[si].end <= e) si++;
+    const Seg &sg = segs[si];
+    const int rel = e - (sg.end - sg.nz * sg.ni);
+    const int kz = rel / sg.ni, ki = rel - kz * sg.ni;
+    src = sg.src + (long long)kz * sg.ssz + (long long)ki * sg.ssi;
+    dst = sg.dst + kz * sg.dsz + ki * sg.dsi;
+  };
   int si = 0;
   for (int e0 = (int)threadIdx.x; e0 < total; e0 += kBrickThreads * kGatherMax) {
     T val[kGatherMax];
-    int src[kGatherMax];
-    int dst[kGatherMax];
     unsigned pend = 0;
+    const int si0 = si;
 #pragma unroll
     for (int k = 0; k < kGatherMax; k++) {
       const int e = e0 + k * kBrickThreads;
-      src[k] = -1;
       if (e < total) {
-        while (segs[si].end <= e) si++;
-        const Seg &s = segs[si];
-        const int rel = e - (s.end - s.nz * s.ni);
-        const int kz = rel / s.ni, ki = rel - kz * s.ni;
-        src[k] = (int)(s.src + (long long)kz * s.ssz + (long long)ki * s.ssi);
-        dst[k] = s.dst + kz * s.dsz + ki * s.dsi;
-        if (!LL<T>::get(ll + (size_t)src[k] * W, tag, val[k])) pend |= 1u << k;
+        long long src;
+        int dst;
+        locate(e, si, src, dst);
+        if (!LLG<T>::get(ll + src * W, tag, val[k])) pend |= 1u << k;
       }
     }
     if (pend) {
       const unsigned long long t0 = globaltimer_ns();
       while (pend) {
+        int s2 = si0;
 #pragma unroll
-        for (int k = 0; k < kGatherMax; k++)
-          if (((pend >> k) & 1u) && LL<T>::get(ll + (size_t)src[k] * W, tag, val[k])) pend &= ~(1u << k);
+        for (int k = 0; k < kGatherMax; k++) {
+          if ((pend >> k) & 1u) {
+            long long src;
+            int dst;
+            locate(e0 + k * kBrickThreads, s2, src, dst);
+            if (LLG<T>::get(ll + src * W, tag, val[k])) pend &= ~(1u << k);
+          }
+        }
         if (pend && globaltimer_ns() - t0 > PERKS_WATCHDOG_NS) watchdog_fire("perks3d brick halo", pend, tag);
       }
     }
+    int s3 = si0;
 #pragma unroll
-    for (int k = 0; k < kGatherMax; k++)
-      if (src[k] >= 0) slots[dst[k]] = val[k];
+    for (int k = 0; k < kGatherMax; k++) {
+      const int e = e0 + k * kBrickThreads;
+      if (e < total) {
+        long long src;
+        int dst;
+        locate(e, s3, src, dst);
+        slots[dst] = val[k];
+      }
+    }
   }
 }
 
 template <typename T, int S>
 __global__ void __launch_bounds__(kBrickThreads, 1)
     perks3d_brick_kernel(const T *__restrict__ in, T *__restrict__ out, LLWord *__restrict__ xch, Dom3 d,
-                         BrickGeo bg, int64_t steps, Coef<T, Shape<S>::N> c) {
+                         BrickGeo bg, int64_t steps, Coef<T, Shape<S>::N> c, int dbg) {
   using G = typename GBrick<T>::G;
-  constexpr int W = LL<T>::WORDS;
+  constexpr int W = LLG<T>::WORDS;
   constexpr bool CORNERS = has_corners<S>();  // shapes with diagonal terms read ring corners / z-halo rings
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T *slots = reinterpret_cast<T *>(smem_raw);
@@ -236,12 +262,12 @@ __global__ void __launch_bounds__(kBrickThreads, 1)
       for (int i = 0; i < G::V; i++) {
         const int xl = xl0 + i;
         if (xl >= me.txc) continue;
-        if (xl == 0) LL<T>::put(buf + (xbase + sec.wcol(o, yl)) * W, v[r][i], tag);
-        if (xl == me.txc - 1) LL<T>::put(buf + (xbase + sec.ecol(o, yl)) * W, v[r][i], tag);
-        if (yl == 0) LL<T>::put(buf + (xbase + sec.ylo(o, xl)) * W, v[r][i], tag);
-        if (yl == me.tyc - 1) LL<T>::put(buf + (xbase + sec.yhi(o, xl)) * W, v[r][i], tag);
-        if (zl) LL<T>::put(buf + (xbase + sec.zlo(yl, xl)) * W, v[r][i], tag);
-        if (zh) LL<T>::put(buf + (xbase + sec.zhi(yl, xl)) * W, v[r][i], tag);
+        if (xl == 0) LLG<T>::put(buf + (xbase + sec.wcol(o, yl)) * W, v[r][i], tag);
+        if (xl == me.txc - 1) LLG<T>::put(buf + (xbase + sec.ecol(o, yl)) * W, v[r][i], tag);
+        if (yl == 0) LLG<T>::put(buf + (xbase + sec.ylo(o, xl)) * W, v[r][i], tag);
+        if (yl == me.tyc - 1) LLG<T>::put(buf + (xbase + sec.yhi(o, xl)) * W, v[r][i], tag);
+        if (zl) LLG<T>::put(buf + (xbase + sec.zlo(yl, xl)) * W, v[r][i], tag);
+        if (zh) LLG<T>::put(buf + (xbase + sec.zhi(yl, xl)) * W, v[r][i], tag);
       }
     }
   };
@@ -250,12 +276,12 @@ __global__ void __launch_bounds__(kBrickThreads, 1)
   const size_t par_words = (size_t)gridDim.x * (size_t)bg.bw * W;
 
   for (int64_t t = 0; t < steps; t++) {
-    if (t > 0) {  // 1. halo refresh: x^t surfaces of the neighbours (parity t&1, tag t)
+    if (t > 0 && !(dbg & 1)) {  // 1. halo refresh: x^t surfaces of the neighbours (parity t&1, tag t)
       gather<T>(segs, nseg, xch + (size_t)(t & 1) * par_words, (unsigned)t, slots);
       __syncthreads();
     }
     // 2. sweep: arrivals of planes zb-1 .. zb+nzc (slots 0 .. nzc+1)
-    const bool pub = t + 1 < steps;
+    const bool pub = t + 1 < steps && !(dbg & 2);
     LLWord *pbuf = xch + (size_t)((t + 1) & 1) * par_words;
     const unsigned ptag = (unsigned)(t + 1);
     StreamState<T, G> st;
@@ -377,7 +403,8 @@ cudaError_t launch_brick(const Problem &p, const Plan &pl, const T *in, T *out, 
   cudaError_t e = cudaMemsetAsync(xch, 0, pl.ws_bytes, s);  // tags restart at 1 every run
   if (e != cudaSuccess) return e;
   void *k = (void *)perks3d_brick_kernel<T, S>;
-  void *args[] = {(void *)&in, (void *)&out, (void *)&xch, (void *)&d, (void *)&bg, (void *)&steps, (void *)&c};
+  int dbg = env_int("PERKS_BRICK_DEBUG", 0);  // timing experiments only: 1 skip the halo refresh, 2 skip publishing
+  void *args[] = {(void *)&in, (void *)&out, (void *)&xch, (void *)&d, (void *)&bg, (void *)&steps, (void *)&c, (void *)&dbg};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(pl.grid);
   cfg.blockDim = dim3(pl.block);

@@ -413,3 +413,24 @@ def test_binding_validates_buffers():
     with pytest.raises(ValueError):
         run_group([st], [x.float()], 1)
     st.close()
+
+
+@pytest.mark.parametrize("name", ["3d7pt", "3d27pt", "3d19pt"])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("shape", [(3, 3, 3), (9, 17, 33), (34, 40, 132), (37, 24, 128), (64, 48, 100)])
+def test_perks3d_resident_bricks(monkeypatch, name, dtype, shape):
+    """PERKS-3D resident-brick kernel (opt-in, k3d_brick.cu): the whole domain in shared memory,
+    brick surfaces exchanged as tagged words every step; bit-exact for ragged bricks, both step
+    parities and back-to-back runs."""
+    _need_gpu()
+    monkeypatch.setenv("PERKS_P3D_BRICK", "1")
+    from paper_2204_02064_b200 import Stencil
+    offs, w = si.preset(name)
+    st = Stencil(shape, offs, w, dtype=dtype)
+    q = st.query("perks")
+    st.close()
+    assert q["kernel"].startswith("perks3d_brick"), q
+    u0 = si.field(shape, dtype=dtype, seed=606)
+    for T in (1, 2, 7):
+        ref = oracle.run(u0, offs, w, T, nthreads=4)
+        _check(_run_gpu(u0, name, w, T, "perks"), ref, u0, dtype)
