@@ -150,6 +150,22 @@ def preset(name: str):
                     k = abs(dx) + abs(dy) + abs(dz)
                     offs.append((dx, dy, dz))
                     w.append({0: 1 / 16, 1: 1 / 8, 2: 1 / 32}[k])
+    elif name == "3d17pt":
+        # Table II 3d17pt(1,34): order 1, 17 points.  The text fixes only (order, FLOPs); no
+        # 17-point subset of the 3x3x3 cube is invariant under all cube symmetries (orbits 1, 6, 12,
+        # 8), so reading R3e takes the set invariant under the symmetries that keep z:
+        # the centre plane's 3x3 box (9) plus the 8 cube corners (|dx| = |dy| = |dz| = 1).
+        # (dz,dy,dx) lexicographic; dyadic convex weights: centre 1/4, in-plane faces 1/8, in-plane
+        # corners 1/32, cube corners 1/64 (sum exactly 1)
+        offs, w = [], []
+        for dz in (-1, 0, 1):
+            for dy in (-1, 0, 1):
+                for dx in (-1, 0, 1):
+                    if dz != 0 and (dx == 0 or dy == 0):
+                        continue
+                    offs.append((dx, dy, dz))
+                    m = abs(dx) + abs(dy)
+                    w.append(1 / 64 if dz != 0 else {0: 1 / 4, 1: 1 / 8, 2: 1 / 32}[m])
     elif name in STAR_RADIUS:
         # Table II high-order stars 2ds9pt / 2d13pt / 2d17pt / 2d21pt / 2ds25pt (radius 2..6):
         # the 4r+1 points (0,dy) and (dx,0), (dy,dx) lexicographic; dyadic convex weights: centre
@@ -178,7 +194,7 @@ def preset(name: str):
 
 
 STAR_RADIUS = {"2ds9pt": 2, "2d13pt": 3, "2d17pt": 4, "2d21pt": 5, "2ds25pt": 6}
-PRESET_NDIM = {"2d5pt": 2, "2d9pt": 2, "3d7pt": 3, "3d27pt": 3, "3d19pt": 3, "2d25pt": 2, "3d13pt": 3,
+PRESET_NDIM = {"2d5pt": 2, "2d9pt": 2, "3d7pt": 3, "3d27pt": 3, "3d19pt": 3, "2d25pt": 2, "3d13pt": 3, "3d17pt": 3,
                **{k: 2 for k in STAR_RADIUS}}
 
 

@@ -346,14 +346,15 @@ def test_wide_2d_any_order_and_random_weights(dtype):
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 @pytest.mark.parametrize("shape", [(5, 6, 7), (20, 35, 70), (37, 24, 40)])
 def test_parity_wide_3d(variant, dtype, shape):
-    """General 3D kernels (k3d_wide.cu): Table II 3d13pt (radius-2 star, compile-time point set), a
-    reversed 3d7pt list and an asymmetric radius-3 list with random weights (runtime point list):
+    """General 3D kernels (k3d_wide.cu): Table II 3d13pt (radius-2 star, compile-time point set),
+    3d17pt (reading R3e, runtime point list), a reversed 3d7pt list and an asymmetric radius-3 list with random weights (runtime point list):
     every variant bit-exact vs the oracle, ragged 32 x 8 x 8 blocks."""
     _need_gpu()
     o7, _ = si.preset("3d7pt")
     asym = [(0, 0, 0), (3, 0, 0), (-1, 2, 0), (0, -3, 1), (1, 1, -2), (0, 0, 3), (-2, -1, -1)]
     o13, w13 = si.preset("3d13pt")
-    cases = [(o13, w13), (o7[::-1], si.random_convex_weights(7, dtype, seed=21)),
+    o17, w17 = si.preset("3d17pt")
+    cases = [(o13, w13), (o17, w17), (o7[::-1], si.random_convex_weights(7, dtype, seed=21)),
              (asym, si.random_convex_weights(len(asym), dtype, seed=22))]
     for offs, w in cases:
         r = max(max(abs(a), abs(b), abs(c)) for a, b, c in offs)

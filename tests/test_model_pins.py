@@ -55,7 +55,10 @@ def test_table2_flops_of_presets():
     """Reading R3: flops/cell = 2·|P| (FMA counted as 2) matches Table II for the hot-path shapes."""
     import seeded_inputs as si
     rows = {r[0]: (r[1], r[2]) for r in GOLD["table2"]["rows"]}
-    for name in ("2d5pt", "2d9pt", "3d7pt", "3d27pt"):
+    for name in ("2d5pt", "2d9pt", "3d7pt", "3d27pt", "3d17pt", "3d13pt", "2ds9pt", "2d13pt",
+                 "2d17pt", "2d21pt", "2d25pt"):
         offs, _ = si.preset(name)
         order = max(max(abs(d) for d in o) for o in offs)
-        assert (order, 2 * len(offs)) == rows[name]
+        assert (order, 2 * len(offs)) == rows[name], name
+    offs, _ = si.preset("3d19pt")  # Table II "poisson" (reading R3b)
+    assert (max(max(abs(d) for d in o) for o in offs), 2 * len(offs)) == rows["poisson"]
