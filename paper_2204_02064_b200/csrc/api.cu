@@ -129,8 +129,11 @@ const Plan &get_plan(perks_stencil_s *h, perks_variant v) {
   if (!h->planned[i]) {
     const Problem &p = h->p;
     Plan pl;
-    if (p.shape == SHAPE_G2D)
+    if (p.shape == SHAPE_G2D) {
       pl = plan_wide2d(p, v);
+      // beyond the on-chip capacity: Tiled PERKS over the wide2d resident kernel (k2d_tiled.cu)
+      if (!pl.ok && v == PERKS_PERKS && env_int("PERKS_TILED", 1)) pl = plan_tiled2d(p, 1000);
+    }
     else if (p.shape == SHAPE_G3D)
       pl = plan_wide3d(p, v);
     else if (v == PERKS_HOSTLOOP || v == PERKS_PERSISTENT)
@@ -145,6 +148,9 @@ const Plan &get_plan(perks_stencil_s *h, perks_variant v) {
         if (env_int("PERKS_STRIP", 0)) pl = plan_perks2d_strip(p);
         if (pl.ok && env_int("PERKS_STRIP", 0)) pl.family = 3;
         else pl = plan_perks2d(p);   // square tiles
+        // beyond the on-chip capacity: Tiled PERKS (device-sized tiles with a redundant halo,
+        // Tb steps per pass, k2d_tiled.cu); PERKS_TILED=0 disables it
+        if (!pl.ok && env_int("PERKS_TILED", 1)) pl = plan_tiled2d(p, 1000);
       }
     } else if (v == PERKS_PERKS) {
       // resident bricks (k3d_brick.cu) are opt-in (PERKS_P3D_BRICK=1): measured slower than the
@@ -162,7 +168,11 @@ const Plan &get_plan(perks_stencil_s *h, perks_variant v) {
 perks_variant resolve(perks_stencil_s *h, perks_variant v) {
   if (v != PERKS_AUTO) return v;
   if (h->dist.on && !dist_perks_ok(h)) return PERKS_PERSISTENT;
-  if (get_plan(h, PERKS_PERKS).ok) return PERKS_PERKS;
+  const Plan &pp = get_plan(h, PERKS_PERKS);
+  // Tiled PERKS over the general (radius >= 2) kernels: its r*Tb halo makes it slower than the
+  // host loop (profiles/r02_tiled2d.txt); AUTO takes the host loop there (explicit PERKS still tiles)
+  if (pp.ok && pp.family == 5 && h->p.shape == SHAPE_G2D) return PERKS_HOSTLOOP;
+  if (pp.ok) return PERKS_PERKS;
   return PERKS_PERSISTENT;
 }
 
@@ -436,6 +446,11 @@ perks_status perks_stencil_launch_count(perks_stencil_t h, perks_variant v, int6
   DeviceGuard g(h->p.device);
   v = resolve(h, v);
   if (steps == 0) { *launches = 0; return PERKS_OK; }
+  const Plan &pl = get_plan(h, v);
+  if (pl.ok && pl.family == 5 && h->p.ndim == 2) {  // Tiled PERKS: one resident launch per tile and pass
+    *launches = ((steps + pl.zchunk - 1) / pl.zchunk) * pl.units;
+    return PERKS_OK;
+  }
   *launches = v == PERKS_HOSTLOOP ? steps : 1;
   return PERKS_OK;
 }
@@ -473,6 +488,10 @@ perks_status perks_stencil_run(perks_stencil_t h, perks_variant v, const void *d
     h->dist.xbase += (unsigned long long)steps + 1;  // prologue exchange + one per step
     return PERKS_OK;
   }
+  if (pl.family == 5 && p.ndim == 2) {  // Tiled PERKS (2D, beyond the on-chip capacity)
+    e = run_tiled2d(p, pl, d_in, d_out, d_ws, steps, s);
+    return e == cudaSuccess ? PERKS_OK : cuda_fail(e);
+  }
   if (p.shape == SHAPE_G2D || p.shape == SHAPE_G3D) {
     cudaError_t e2 = p.shape == SHAPE_G2D ? run_wide2d(p, pl, d_in, d_out, d_ws, steps, s)
                                           : run_wide3d(p, pl, d_in, d_out, d_ws, steps, s);
@@ -489,7 +508,7 @@ perks_status perks_stencil_run(perks_stencil_t h, perks_variant v, const void *d
         e = pl.family == 1 ? run_perks2d_cluster(p, pl, d_in, d_out, steps, s)
             : pl.family == 3 ? run_perks2d_strip(p, pl, d_in, d_out, d_ws, steps, s)
                              : run_perks2d(p, pl, d_in, d_out, d_ws, steps, s);
-      else if (pl.family == 4)
+      else if (pl.family == 6)
         e = run_brick3d(p, pl, d_in, d_out, d_ws, steps, s);
       else
         e = run_stream3d(p, pl, d_in, d_out, d_ws, steps, s);

@@ -95,6 +95,11 @@ cudaError_t run_perks2d(const Problem &p, const Plan &pl, const void *in, void *
 Plan plan_perks2d_cluster(const Problem &p);
 cudaError_t run_perks2d_cluster(const Problem &p, const Plan &pl, const void *in, void *out,
                                 int64_t steps, cudaStream_t s);
+// Tiled PERKS, 2D domains beyond the on-chip capacity ([draft] P:416-441): device-sized tiles with a
+// redundant halo advanced Tb steps per pass by the resident kernels (k2d_tiled.cu).
+Plan plan_tiled2d(const Problem &p, int64_t steps_hint);
+cudaError_t run_tiled2d(const Problem &p, const Plan &pl, const void *in, void *out, void *ws, int64_t steps,
+                        cudaStream_t s);
 // PERKS (c), 2D fp32 domains 1025..3072 wide: full-width strips, edge rows first.
 Plan plan_perks2d_strip(const Problem &p);
 cudaError_t run_perks2d_strip(const Problem &p, const Plan &pl, const void *in, void *out, void *ws,

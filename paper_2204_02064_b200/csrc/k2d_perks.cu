@@ -74,13 +74,17 @@ PERKS_DEVINL void poll_copy(const LLWord *src, int n, unsigned tag, bool exists,
     const int i = lane + 32 * e;
     if (i < n && !LL<T>::get(src + i * W, tag, val[e])) pending |= 1u << e;
   }
-  while (pending) {
+  if (pending) {
+    const unsigned long long t0 = globaltimer_ns();
+    while (pending) {
 #pragma unroll
-    for (int e = 0; e < E; e++)
-      if ((pending >> e) & 1u) {
-        const int i = lane + 32 * e;
-        if (LL<T>::get(src + i * W, tag, val[e])) pending &= ~(1u << e);
-      }
+      for (int e = 0; e < E; e++)
+        if ((pending >> e) & 1u) {
+          const int i = lane + 32 * e;
+          if (LL<T>::get(src + i * W, tag, val[e])) pending &= ~(1u << e);
+        }
+      if (pending && globaltimer_ns() - t0 > PERKS_WATCHDOG_NS) watchdog_fire("perks2d halo", pending, tag);
+    }
   }
 #pragma unroll
   for (int e = 0; e < E; e++) {
@@ -291,9 +295,11 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
           const bool cex = cx >= 0 && cx < tl.ntx && nty >= 0 && nty < tl.nty;
           const LLWord *cs = GS(cex ? nty * tl.ntx + cx : 0, par) + ((side == 0 ? TX : 0) + (lane == 0 ? TX - 1 : 0)) * W;
           T val = T(0);
-          if (cex)
-            while (!LL<T>::get(cs, tag_in, val)) {
-            }
+          if (cex && !LL<T>::get(cs, tag_in, val)) {
+            const unsigned long long t0 = globaltimer_ns();
+            while (!LL<T>::get(cs, tag_in, val))
+              if (globaltimer_ns() - t0 > PERKS_WATCHDOG_NS) watchdog_fire("perks2d halo corner", 0u, tag_in);
+          }
           sm[dst + (lane == 0 ? 0 : TX + 1)] = val;
         }
       } else {
@@ -480,490 +486,9 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
   }
 }
 
-// ------------------------------------------------------------------ dataflow variant
-// perks2d_flow_kernel: the same tile, tiers and FMA chain as perks2d_kernel, but WITHOUT the CTA
-// barrier per step.  Each warp advances on its own as soon as the data it reads is there:
-//  * tile-edge warps poll their own halo segments from the neighbouring tiles' tagged exchange
-//    words (top row straight into the window registers; left/right columns incl. the corner rows
-//    and the bottom row into warp-private shared memory);
-//  * inside the CTA, a warp publishes "top row of x^{t+1} out" (pub_top) after its first row and
-//    "all edges of x^{t+1} out" (pub_all) after its last row (st.release.cta); a warp starts step t
-//    once the warps above it and beside it have pub_all >= t+1 and reads the row below only when it
-//    reaches its last row, after the warps below have pub_top >= t+1 (ld.acquire.cta).
-// The CTA is no longer in lock-step: warps away from the tile edge run ahead of the edge warps, so
-// the exchange latency of P:348's neighbour dependency overlaps other warps' rows instead of
-// stalling the whole SM at a barrier (C2: 33 % of perks2d_kernel's samples sat at that barrier,
-// profiles/r01_c2_perks2d_tmem_T1000_ncu_full.txt).  No write-after-read hazard: every buffer a
-// warp overwrites (parity (t+1)&1) was last read by a warp whose output the writer has already
-// consumed.
-PERKS_DEVINL unsigned ld_acq_cta(const unsigned *p) {
-  unsigned v;
-  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];\n" : "=r"(v) : "r"(smem_u32(p)) : "memory");
-  return v;
-}
-PERKS_DEVINL void st_rel_cta(unsigned *p, unsigned v) {
-  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;\n" ::"r"(smem_u32(p)), "r"(v) : "memory");
-}
-// %tid.x re-read (asm volatile: not hoisted), so values needed only at step boundaries are
-// recomputed there instead of occupying registers through the row sweep
-PERKS_DEVINL int tid_fresh() {
-  int v;
-  asm volatile("mov.u32 %0, %%tid.x;\n" : "=r"(v));
-  return v;
-}
-#ifndef PERKS_FLOW_TUNROLL  // unroll factor of the dataflow kernel's TMEM-row loop
-#define PERKS_FLOW_TUNROLL 2
-#endif
-constexpr int kFlowTU = PERKS_FLOW_TUNROLL;
-#ifndef PERKS_FLOW_SLEEP  // ns of __nanosleep per spin iteration of a waiting warp (0: busy spin)
-#define PERKS_FLOW_SLEEP 0
-#endif
-PERKS_DEVINL void flow_backoff() {
-  if (PERKS_FLOW_SLEEP > 0) __nanosleep(PERKS_FLOW_SLEEP);
-}
-PERKS_DEVINL void wait_flag_cta(const unsigned *f, unsigned want) {
-  if (ld_acq_cta(f) >= want) return;
-  const unsigned long long t0 = globaltimer_ns();
-  while (ld_acq_cta(f) < want) {
-    flow_backoff();
-    if (globaltimer_ns() - t0 > PERKS_WATCHDOG_NS) watchdog_fire("perks2d flow flag", ld_acq_cta(f), want);
-  }
-}
+// (The barrier-free dataflow variant of round 1 was measured slower on C2, 8.33 vs 7.39 us/step,
+// profiles/r01_c2_flow.txt, and removed; this kernel keeps the one CTA barrier per step.)
 
-template <class G> struct FlowSmem {
-  static constexpr int R = G::R, V = G::V, WX = G::WX, WY = G::WY, NWARP = G::NT / 32;
-  static constexpr int COLH = 2 * WY * (R + 2);   // polled halo columns, per (side, warp row): rows -1..R
-  static constexpr int BH = WX * 32 * (V + 2);    // polled bottom halo, per bottom-row thread: x-1..x+V
-  static constexpr int FLAGS = 2 * NWARP;         // pub_top[NWARP], pub_all[NWARP] (u32)
-};
-template <typename T, class G>
-constexpr size_t flow_smem_bytes() {
-  using F = FlowSmem<G>;
-  return G::SMEM_BYTES + (size_t)(F::COLH + F::BH) * sizeof(T) + F::FLAGS * 4;
-}
-
-template <typename T, int S, class G>
-__global__ void __launch_bounds__(G::NT, 1) perks2d_flow_kernel(const T *__restrict__ in,
-                                                                T *__restrict__ out, LLWord *gslot,
-                                                                int nx, int ny,
-                                                                Tiles2 tl, int64_t steps,
-                                                                Coef<T, Shape<S>::N> c) {
-  constexpr int V = G::V, R = G::R, RR = G::RR, RT = G::RT, RS0 = G::RS0, NT = G::NT, TX = G::TX, TY = G::TY;
-  constexpr int WX = G::WX, WY = G::WY, ROWW = G::ROWW, NWARP = NT / 32;
-  constexpr bool BOX = has_corners<S>();
-  using F = FlowSmem<G>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T *const sm = reinterpret_cast<T *>(smem_raw);
-  constexpr int ROW0 = G::CACHE, COL0 = G::CACHE + G::ROWBUF;
-  constexpr int SCR0 = G::CACHE + G::ROWBUF + G::COLBUF;
-  constexpr int COLH0 = SCR0 + NT, BH0 = COLH0 + F::COLH, FLG_BYTE = (BH0 + F::BH) * (int)sizeof(T);
-  constexpr int PAR_ROW = 2 * (WY + 1) * ROWW, PAR_COL = 2 * (WX + 1) * TY;
-  auto TOP = [](int j) { return ROW0 + j * ROWW; };
-  auto BOT = [](int jp1) { return ROW0 + (WY + 1 + jp1) * ROWW; };
-  auto LEFT = [](int k) { return COL0 + k * TY; };
-  auto RIGHT = [](int kp1) { return COL0 + (WX + 1 + kp1) * TY; };
-  unsigned *const pub_top = reinterpret_cast<unsigned *>(smem_raw + FLG_BYTE);
-  unsigned *const pub_all = pub_top + NWARP;
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wx = warp % WX, wy = warp / WX;
-  const int tile = blockIdx.x;
-  const int tx = tile % tl.ntx, ty = tile / tl.ntx;
-  const int x0 = tx * TX, y0 = ty * TY;
-  const int xr = (wx * 32 + lane) * V;
-  const int yr0 = wy * R;
-  const int x = x0 + xr;
-  constexpr int W = LL<T>::WORDS;
-  auto GS = [&](int t, int par) -> LLWord * { return gslot + ((size_t)t * 2 + par) * G::SLOT * W; };
-  // exchange word of tile (tx+dtx, ty+dty) at slot offset off, parity par; nullptr if no such tile
-  auto GW = [&](int dtx, int dty, int off, int par) -> const LLWord * {
-    const int a = tx + dtx, b = ty + dty;
-    if (a < 0 || a >= tl.ntx || b < 0 || b >= tl.nty) return nullptr;
-    return GS(b * tl.ntx + a, par) + (size_t)off * W;
-  };
-
-  for (int i = tid; i < G::ROWBUF + G::COLBUF + NT; i += NT) sm[ROW0 + i] = T(0);
-  if (tid < NWARP) {
-    pub_top[tid] = 1u;  // x^0 is published by the prologue below (ordered by its __syncthreads)
-    pub_all[tid] = 1u;
-  }
-
-  const bool is_l = lane == 0, is_r = lane == 31;
-  const int o_top = TOP(wy) + xr + 1, o_bot = BOT(wy + 1) + xr + 1;
-  const int o_colL = is_l ? LEFT(wx) + yr0 : SCR0 + tid;
-  const int o_colR = is_r ? RIGHT(wx + 1) + yr0 : SCR0 + tid;
-  const int o_colL_step = is_l ? 1 : 0, o_colR_step = is_r ? 1 : 0;
-  const bool g_top = wy == 0, g_bot = wy == WY - 1;
-  const bool g_l = is_l && wx == 0, g_r = is_r && wx == WX - 1;
-  T *const my_smc = sm + (size_t)tid * V;
-  // Step-boundary quantities from a fresh %tid.x (not live through the row sweep):
-  //   colh_l/colh_r  this warp row's polled halo columns (rows yr0-1 .. yr0+R, warp-private)
-  //   bh             this bottom-row thread's polled bottom halo (x-1 .. x+V)
-  //   hl/hr          lane 0 / 31 at the tile's left / right edge (reads the polled columns)
-  struct Who {
-    int tid, lane, warp, wx, wy, xr, yr0, colh_l, colh_r, bh;
-    bool hl, hr;
-  };
-  auto who = [&]() {
-    Who w;
-    w.tid = tid_fresh();
-    w.lane = w.tid & 31;
-    w.warp = w.tid >> 5;
-    w.wx = w.warp % WX;
-    w.wy = w.warp / WX;
-    w.xr = (w.wx * 32 + w.lane) * V;
-    w.yr0 = w.wy * R;
-    w.colh_l = COLH0 + w.wy * (R + 2);
-    w.colh_r = COLH0 + (WY + w.wy) * (R + 2);
-    w.bh = BH0 + (w.wy == WY - 1 ? (w.tid - (WY - 1) * WX * 32) * (V + 2) : 0);
-    w.hl = w.lane == 0 && w.wx == 0;
-    w.hr = w.lane == 31 && w.wx == WX - 1;
-    return w;
-  };
-
-  auto publish_row = [&](int pb, LLWord *g, unsigned tag, int r, const T (&v)[V],
-                         bool maybe_edge_row = true) {
-    const int pr = pb * PAR_ROW, pc = pb * PAR_COL;
-    if (maybe_edge_row && r == 0) {
-#pragma unroll
-      for (int i = 0; i < V; i++) sm[pr + o_top + i] = v[i];
-      if (g_top) {
-#pragma unroll
-        for (int i = 0; i < V; i++) LL<T>::put(g + (xr + i) * W, v[i], tag);
-      }
-    }
-    if (maybe_edge_row && r == R - 1) {
-#pragma unroll
-      for (int i = 0; i < V; i++) sm[pr + o_bot + i] = v[i];
-      if (g_bot) {
-#pragma unroll
-        for (int i = 0; i < V; i++) LL<T>::put(g + (TX + xr + i) * W, v[i], tag);
-      }
-    }
-    if constexpr (WX > 1) {
-      sm[(is_l ? pc : 0) + o_colL + o_colL_step * r] = v[0];
-      sm[(is_r ? pc : 0) + o_colR + o_colR_step * r] = v[V - 1];
-    }
-    if (g_l) LL<T>::put(g + (2 * TX + yr0 + r) * W, v[0], tag);
-    if (g_r) LL<T>::put(g + (2 * TX + TY + yr0 + r) * W, v[V - 1], tag);
-  };
-
-  __shared__ uint32_t tmem_base_slot;
-  uint32_t tb = 0;
-  if constexpr (RT > 0) {
-    if (warp == 0) {
-      tmem_alloc(&tmem_base_slot, (uint32_t)G::TCOLS);
-      tmem_relinquish();
-    }
-    tmem_fence_before_sync();
-    __syncthreads();
-    tmem_fence_after_sync();
-    tb = tmem_base_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * RT * G::WPR);
-  }
-  auto trow = [&](int r) { return tb + (uint32_t)((r - RR) * G::WPR); };
-
-  T reg[RR > 0 ? RR : 1][V];
-  auto load_row = [&](int r, T (&v)[V]) {
-    const int y = y0 + yr0 + r;
-#pragma unroll
-    for (int i = 0; i < V; i++) v[i] = (y < ny && x + i < nx) ? in[(size_t)y * nx + x + i] : T(0);
-  };
-  __syncthreads();  // zeroed buffers before anyone publishes
-  {
-    LLWord *g0 = GS(tile, 0);
-#pragma unroll
-    for (int r = 0; r < RR; r++) {
-      T v[V];
-      load_row(r, v);
-#pragma unroll
-      for (int i = 0; i < V; i++) reg[r][i] = v[i];
-      publish_row(0, g0, 1u, r, v);
-    }
-#pragma unroll
-    for (int r = RR; r < RS0; r++) {
-      T v[V];
-      load_row(r, v);
-      tmem_st_row<T, V>(trow(r), v);
-      publish_row(0, g0, 1u, r, v);
-    }
-    if constexpr (RT > 0) tmem_wait_st();
-#pragma unroll 1
-    for (int r = RS0; r < R; r++) {
-      T v[V];
-      load_row(r, v);
-      vstore<T, V>(my_smc + (size_t)(r - RS0) * NT * V, v);
-      publish_row(0, g0, 1u, r, v);
-    }
-  }
-  __syncthreads();  // x^0 edges in shared memory (the only CTA barrier before the epilogue)
-
-  const int ylo = max(0, 1 - (y0 + yr0)), yhi = min(R, ny - 1 - (y0 + yr0));
-  const bool all_interior = ylo == 0 && yhi == R && x >= 1 && x + V - 1 <= nx - 2;
-  unsigned xmask = 0;
-#pragma unroll
-  for (int i = 0; i < V; i++) xmask |= ((x + i) >= 1 && (x + i) <= nx - 2) ? (1u << i) : 0u;
-
-  // poll V+2 consecutive tagged row words x-1..x+V of the tile row dty away (dty = -1: the
-  // bottom row of the tile above, +1: the top row of the tile below)
-  auto poll_row = [&](const Who &me, int dty, int par, unsigned tag, T (&w)[V + 2]) {
-    const int off_row = dty < 0 ? TX : 0;
-    const int xr = me.xr;
-    unsigned pend = 0;
-#pragma unroll
-    for (int k = 0; k < V + 2; k++) {
-      const int xx = xr - 1 + k;
-      const LLWord *p = GW(xx < 0 ? -1 : (xx >= TX ? 1 : 0), dty, off_row + (xx + TX) % TX, par);
-      w[k] = T(0);
-      if (p && !LL<T>::get(p, tag, w[k])) pend |= 1u << k;
-    }
-    if (pend) {
-      const unsigned long long t0 = globaltimer_ns();
-      while (pend) {
-#pragma unroll
-        for (int k = 0; k < V + 2; k++)
-          if ((pend >> k) & 1u) {
-            const int xx = xr - 1 + k;
-            const LLWord *p = GW(xx < 0 ? -1 : (xx >= TX ? 1 : 0), dty, off_row + (xx + TX) % TX, par);
-            if (LL<T>::get(p, tag, w[k])) pend &= ~(1u << k);
-          }
-        if (pend) flow_backoff();
-        if (pend && globaltimer_ns() - t0 > PERKS_WATCHDOG_NS) watchdog_fire("perks2d flow row halo", pend, tag);
-      }
-    }
-  };
-  // poll this warp row's halo column (rows yr0-1 .. yr0+R) of the tile dtx away into dst
-  auto poll_col = [&](const Who &me, int dtx, int par, unsigned tag, int dst) {
-    const int off_col = 2 * TX + (dtx < 0 ? TY : 0);
-    for (int i = me.lane; i < R + 2; i += 32) {
-      const int yy = me.yr0 - 1 + i;
-      const LLWord *p = GW(dtx, yy < 0 ? -1 : (yy >= TY ? 1 : 0), off_col + (yy + TY) % TY, par);
-      T v = T(0);
-      if (p && !LL<T>::get(p, tag, v)) {
-        const unsigned long long t0 = globaltimer_ns();
-        while (!LL<T>::get(p, tag, v)) {
-          flow_backoff();
-          if (globaltimer_ns() - t0 > PERKS_WATCHDOG_NS) watchdog_fire("perks2d flow column halo", i, tag);
-        }
-      }
-      sm[dst + i] = v;
-    }
-  };
-
-  for (int64_t t = 0; t < steps; t++) {
-    const int par = (int)(t & 1), np = par ^ 1;
-    const int pr = par * PAR_ROW, pc = par * PAR_COL;
-    const unsigned tag_in = (unsigned)(t + 1);
-    T prev[V + 2], cur[V + 2], nxt[V + 2];
-    int rdL, rdR;
-    {
-      const Who me = who();
-      // ---- this warp's halos from the neighbouring tiles (tile-edge warps only)
-      if (me.wy == 0) poll_row(me, -1, par, tag_in, prev);
-      if (me.wx == 0) poll_col(me, -1, par, tag_in, me.colh_l);
-      if (me.wx == WX - 1) poll_col(me, 1, par, tag_in, me.colh_r);
-      if (me.wy == WY - 1) {
-        T w[V + 2];
-        poll_row(me, 1, par, tag_in, w);
-#pragma unroll
-        for (int k = 0; k < V + 2; k++) sm[me.bh + k] = w[k];
-      }
-      __syncwarp();
-      // ---- in-CTA neighbours: the warps above (x^t bottom rows) and beside (x^t columns) are
-      //      done with step t-1
-      if (me.wy > 0) {
-        wait_flag_cta(&pub_all[me.warp - WX], tag_in);
-        if (BOX && me.wx > 0) wait_flag_cta(&pub_all[me.warp - WX - 1], tag_in);
-        if (BOX && me.wx < WX - 1) wait_flag_cta(&pub_all[me.warp - WX + 1], tag_in);
-        const int o = pr + BOT(me.wy) + me.xr;
-#pragma unroll
-        for (int i = BOX ? 0 : 1; i < (BOX ? V + 2 : V + 1); i++) prev[i] = sm[o + i];
-        if (BOX && me.hl) prev[0] = sm[me.colh_l];
-        if (BOX && me.hr) prev[V + 1] = sm[me.colh_r];
-      }
-      if (me.wx > 0) wait_flag_cta(&pub_all[me.warp - 1], tag_in);
-      if (me.wx < WX - 1) wait_flag_cta(&pub_all[me.warp + 1], tag_in);
-      // column reads for row r: lanes 0/31 at the tile edge read the polled column (index r+1),
-      // the other warp-edge lanes the neighbour warp's column buffer of parity par
-      rdL = me.hl ? me.colh_l + 1 : pc + RIGHT(me.wx) + me.yr0;
-      rdR = me.hr ? me.colh_r + 1 : pc + LEFT(me.wx + 1) + me.yr0;
-    }
-    LLWord *gnp = GS(tile, np);
-    const unsigned tag_out = (unsigned)(t + 2);
-    T pcl = sm[rdL], pcr = sm[rdR];
-    auto widen = [&](T (&w)[V + 2], const T (&v)[V], int r) {
-      const T l = __shfl_up_sync(0xffffffffu, v[V - 1], 1);
-      const T rr = __shfl_down_sync(0xffffffffu, v[0], 1);
-      const T cl = pcl, cr = pcr;
-      pcl = sm[rdL + r + 1];
-      pcr = sm[rdR + r + 1];
-      w[0] = is_l ? cl : l;
-      w[V + 1] = is_r ? cr : rr;
-#pragma unroll
-      for (int i = 0; i < V; i++) w[i + 1] = v[i];
-    };
-    auto halo_below = [&](T (&w)[V + 2]) {
-      const Who me = who();
-      if (me.wy == WY - 1) {
-#pragma unroll
-        for (int k = 0; k < V + 2; k++) w[k] = sm[me.bh + k];
-      } else {
-        wait_flag_cta(&pub_top[me.warp + WX], tag_in);
-        if (BOX && me.wx > 0) wait_flag_cta(&pub_top[me.warp + WX - 1], tag_in);
-        if (BOX && me.wx < WX - 1) wait_flag_cta(&pub_top[me.warp + WX + 1], tag_in);
-        const int o = pr + TOP(me.wy + 1) + me.xr;
-#pragma unroll
-        for (int i = BOX ? 0 : 1; i < (BOX ? V + 2 : V + 1); i++) w[i] = sm[o + i];
-        if (BOX && me.hl) w[0] = sm[me.colh_l + R + 1];
-        if (BOX && me.hr) w[V + 1] = sm[me.colh_r + R + 1];
-      }
-    };
-    auto finish_row = [&](int r, T (&nv)[V], bool maybe_edge_row = true) {
-#pragma unroll
-      for (int i = 0; i < V; i++) {
-        T acc;
-#pragma unroll
-        for (int p = 0; p < Shape<S>::N; p++) {
-          const int dy = Shape<S>::dy(p), dx = Shape<S>::dx(p);
-          const T val = dy < 0 ? prev[i + 1 + dx] : (dy > 0 ? nxt[i + 1 + dx] : cur[i + 1 + dx]);
-          acc = (p == 0) ? mul_rn(c.w[0], val) : fma_rn(c.w[p], val, acc);
-        }
-        nv[i] = acc;
-      }
-      if (!all_interior) {
-        const bool rin = r >= ylo && r < yhi;
-#pragma unroll
-        for (int i = 0; i < V; i++)
-          if (!(rin && ((xmask >> i) & 1u))) nv[i] = cur[i + 1];
-      }
-      publish_row(np, gnp, tag_out, r, nv, maybe_edge_row);
-      if (maybe_edge_row && r == 0) {  // top row of x^{t+1} out
-        __syncwarp();
-        const int tf = tid_fresh();
-        if ((tf & 31) == 0) st_rel_cta(&pub_top[tf >> 5], tag_out);
-      }
-#pragma unroll
-      for (int i = 0; i < V + 2; i++) {
-        prev[i] = cur[i];
-        cur[i] = nxt[i];
-      }
-    };
-    {
-      T v[V];
-      if (RR > 0) {
-#pragma unroll
-        for (int i = 0; i < V; i++) v[i] = opaque_copy(reg[0][i]);
-      } else if (RT > 0) {
-        tmem_ld_row<T, V>(trow(0), v);
-      } else {
-        vload<T, V>(v, my_smc);
-      }
-      widen(cur, v, 0);
-    }
-    auto next_tier_row = [&](int rn) {
-      if (RT > 0 && rn < RS0) {
-        T v[V];
-        tmem_ld_row<T, V>(trow(rn), v);
-        widen(nxt, v, rn);
-      } else if (RS0 < R) {
-        T v[V];
-        vload<T, V>(v, my_smc + (size_t)(rn - RS0) * NT * V);
-        widen(nxt, v, rn);
-      } else {
-        halo_below(nxt);
-      }
-    };
-#pragma unroll
-    for (int r = 0; r < RR; r++) {
-      if (r + 1 < RR) {
-        T v[V];
-#pragma unroll
-        for (int i = 0; i < V; i++) v[i] = opaque_copy(reg[r + 1 < RR ? r + 1 : 0][i]);
-        widen(nxt, v, r + 1);
-      } else {
-        next_tier_row(r + 1);
-      }
-      T nv[V];
-      finish_row(r, nv);
-#pragma unroll
-      for (int i = 0; i < V; i++) reg[r][i] = nv[i];
-    }
-    // TMEM rows: a rolled loop (runtime TMEM addresses) + the peeled last row.  Warps of the
-    // dataflow kernel run at different rows/steps, so the step's code must stay small enough for
-    // the instruction cache (fully unrolled, `no_instructions` was the top stall)
-    if constexpr (RS0 > RR) {
-#pragma unroll kFlowTU
-      for (int r = RR; r < RS0 - 1; r++) {
-        T v[V];
-        tmem_ld_row<T, V>(trow(r + 1), v);
-        widen(nxt, v, r + 1);
-        T nv[V];
-        finish_row(r, nv, RR == 0 && r == 0);
-        tmem_st_row<T, V>(trow(r), nv);
-      }
-      {
-        constexpr int r = RS0 - 1;
-        next_tier_row(r + 1);
-        T nv[V];
-        finish_row(r, nv);
-        tmem_st_row<T, V>(trow(r), nv);
-      }
-    }
-    if constexpr (RT > 0) tmem_wait_st();
-    if (RS0 < R) {
-#pragma unroll 3
-      for (int r = RS0; r < R - 1; r++) {
-        T v[V];
-        vload<T, V>(v, my_smc + (size_t)(r + 1 - RS0) * NT * V);
-        widen(nxt, v, r + 1);
-        T nv[V];
-        finish_row(r, nv, RS0 == 0 && r == 0);
-        vstore<T, V>(my_smc + (size_t)(r - RS0) * NT * V, nv);
-      }
-      halo_below(nxt);
-      T nv[V];
-      finish_row(R - 1, nv);
-      vstore<T, V>(my_smc + (size_t)(R - 1 - RS0) * NT * V, nv);
-    }
-    // all of x^{t+1}'s edges of this warp out
-    __syncwarp();
-    {
-      const int tf = tid_fresh();
-      if ((tf & 31) == 0) st_rel_cta(&pub_all[tf >> 5], tag_out);
-    }
-  }
-
-  int ybase = y0 + yr0, xe = x;
-  T *oute = out;
-  asm volatile("" : "+r"(ybase), "+r"(xe), "+l"(oute));
-  auto store_row = [&](int r, const T (&v)[V]) {
-    const int y = ybase + r;
-    if (y < ny) {
-#pragma unroll
-      for (int i = 0; i < V; i++)
-        if (xe + i < nx) oute[(size_t)y * nx + xe + i] = v[i];
-    }
-  };
-#pragma unroll
-  for (int r = 0; r < RR; r++) store_row(r, reg[r]);
-#pragma unroll
-  for (int r = RR; r < RS0; r++) {
-    T v[V];
-    tmem_ld_row<T, V>(trow(r), v);
-    store_row(r, v);
-  }
-#pragma unroll 1
-  for (int r = RS0; r < R; r++) {
-    T v[V];
-    vload<T, V>(v, my_smc + (size_t)(r - RS0) * NT * V);
-    store_row(r, v);
-  }
-  if constexpr (RT > 0) {
-    tmem_fence_before_sync();
-    __syncthreads();
-    tmem_fence_after_sync();
-    if (warp == 0) tmem_dealloc(tmem_base_slot, (uint32_t)G::TCOLS);
-  }
-}
 
 // ------------------------------------------------------------------ host side
 
@@ -1035,24 +560,10 @@ struct CfgInfo {
   int tcols;
 };
 
-// flow: the dataflow kernel (perks2d_flow_kernel, no CTA barrier per step).  Measured slower than
-// the barrier kernel on C2 (8.33 vs 7.39 us/step, profiles/r01_c2_flow.txt), so it is compiled
-// only into development builds (-DPERKS_P2D_FLOW_BUILD=1, tools/build_variant.sh) and selected
-// there with PERKS_P2D_FLOW=1.
-#ifndef PERKS_P2D_FLOW_BUILD
-#define PERKS_P2D_FLOW_BUILD 0
-#endif
 template <typename T, int S, class G> CfgInfo info(bool flow) {
   void *k = (void *)perks2d_kernel<T, S, G>;
   size_t smem = G::SMEM_BYTES;
-#if PERKS_P2D_FLOW_BUILD
-  if (flow) {
-    k = (void *)perks2d_flow_kernel<T, S, G>;
-    smem = flow_smem_bytes<T, G>();
-  }
-#else
   (void)flow;
-#endif
   return CfgInfo{k, G::TX, G::TY, G::NT, smem,
                  (int64_t)G::RR * G::V * G::NT, (int64_t)G::RS * G::V * G::NT,
                  (int64_t)G::RT * G::V * G::NT, G::TCOLS};
@@ -1123,12 +634,6 @@ Plan plan_perks2d(const Problem &p) {
     if (tiles <= p.num_sms && ci.smem <= (size_t)p.max_smem_optin) { best = cfg; break; }
   }
   if (best < 0) { pl.why = "perks2d: domain does not fit on chip (tiles > SMs)"; return pl; }
-  // dataflow kernel (no CTA barrier per step) for the multi-warp-row tiles
-  const bool flow = PERKS_P2D_FLOW_BUILD && env_int("PERKS_P2D_FLOW", 0) != 0;
-  if (flow) {
-    CfgInfo cf = cfg_info(p, best | kFlowBit);
-    if (cf.smem <= (size_t)p.max_smem_optin) best |= kFlowBit;
-  }
   CfgInfo ci = cfg_info(p, best);
   if (cudaFuncSetAttribute(ci.k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ci.smem) != cudaSuccess) {
     pl.why = "cudaFuncSetAttribute"; return pl;

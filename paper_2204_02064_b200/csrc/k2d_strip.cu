@@ -263,6 +263,7 @@ __global__ void __launch_bounds__(32 * NWX, 1) perks2d_strip_kernel(const float 
         if (up && in_x && !LL<float>::get(gt + xx, tag_out, htop[i])) pending |= 1u << i;
         if (dn && in_x && !LL<float>::get(gb + xx, tag_out, hbot[i])) pending |= 1u << (8 + i);
       }
+      const unsigned long long t0 = pending ? globaltimer_ns() : 0ull;
       while (pending) {
 #pragma unroll
         for (int i = 0; i < V + 2; i++) {
@@ -270,6 +271,7 @@ __global__ void __launch_bounds__(32 * NWX, 1) perks2d_strip_kernel(const float 
           if (((pending >> i) & 1u) && LL<float>::get(gt + xx, tag_out, htop[i])) pending &= ~(1u << i);
           if (((pending >> (8 + i)) & 1u) && LL<float>::get(gb + xx, tag_out, hbot[i])) pending &= ~(1u << (8 + i));
         }
+        if (pending && globaltimer_ns() - t0 > PERKS_WATCHDOG_NS) watchdog_fire("perks2d strip halo", pending, tag_out);
       }
     }
     __syncthreads();  // column buffers of parity np complete before the next step reads them

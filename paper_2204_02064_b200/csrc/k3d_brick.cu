@@ -370,7 +370,7 @@ Plan plan_brick3d(const Problem &p) {
   pl.regs = fa.numRegs;
   pl.smem = (int)smem;
   pl.units = pl.grid;
-  pl.family = 4;
+  pl.family = 6;  // (3D resident bricks)
   pl.cfg = nbz;
   const double S = (double)p.elem();
   pl.cached_smem = p.cells();

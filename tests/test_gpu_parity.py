@@ -435,3 +435,28 @@ def test_perks3d_resident_bricks(monkeypatch, name, dtype, shape):
     for T in (1, 2, 7):
         ref = oracle.run(u0, offs, w, T, nthreads=4)
         _check(_run_gpu(u0, name, w, T, "perks"), ref, u0, dtype)
+
+
+@pytest.mark.parametrize("name,dtype", [("2d9pt", np.float32), ("2d5pt", np.float64), ("2ds9pt", np.float32),
+                                        ("2d25pt", np.float64)])
+@pytest.mark.parametrize("shape", [(700, 900), (517, 1333)])
+@pytest.mark.parametrize("tb", ["", "3", "8"])
+def test_tiled_perks_2d(monkeypatch, name, dtype, shape, tb):
+    """Tiled PERKS ([draft] P:416-441): a domain larger than the (here artificially small: 6 SMs)
+    on-chip capacity is cut into device tiles with a redundant halo of r*Tb cells, each advanced Tb
+    steps per pass by the resident kernel; bit-exact vs the oracle for step counts that are / are
+    not multiples of Tb, both pass parities, ragged tiles."""
+    _need_gpu()
+    monkeypatch.setenv("PERKS_NUM_SMS", "6")
+    if tb:
+        monkeypatch.setenv("PERKS_TILED_TB", tb)
+    from paper_2204_02064_b200 import Stencil
+    offs, w = si.preset(name)
+    st = Stencil(shape, offs, w, dtype=dtype)
+    q = st.query("perks")
+    st.close()
+    assert q["kernel"].startswith("perks2d_tiled"), q
+    u0 = si.field(shape, dtype=dtype, seed=707)
+    for T in (1, 7, 16, 17):
+        ref = oracle.run(u0, offs, w, T, nthreads=8)
+        _check(_run_gpu(u0, name, w, T, "perks"), ref, u0, dtype)
