@@ -5,7 +5,7 @@ loop as three sm_100a execution variants (host loop / persistent / PERKS) behind
 ``Stencil`` and ``run`` load the CUDA library on first use and raise if it is missing — there
 is no CPU fallback.  ``model`` (the paper's §4 performance model) is pure Python.
 """
-__all__ = ["Stencil", "run", "run_group", "VARIANTS", "model", "build"]
+__all__ = ["Stencil", "run", "run_group", "CG", "VARIANTS", "model", "build"]
 
 
 def __getattr__(name):
@@ -13,6 +13,10 @@ def __getattr__(name):
         from . import stencil
 
         return getattr(stencil, name)
+    if name == "CG":
+        from .cg import CG
+
+        return CG
     if name == "VARIANTS":
         from ._lib import VARIANTS
 

@@ -58,7 +58,42 @@ class PlanInfo(ctypes.Structure):
     ]
 
 
-# Every symbol include/perks/perks_stencil.h declares, with (restype, argtypes).
+class CsrDesc(ctypes.Structure):  # perks_csr_desc (include/perks/perks_cg.h)
+    _fields_ = [
+        ("n_rows", ctypes.c_int64),
+        ("nnz", ctypes.c_int64),
+        ("row_offsets", ctypes.POINTER(ctypes.c_int64)),
+        ("col_indices", ctypes.POINTER(ctypes.c_int32)),
+        ("values", ctypes.POINTER(ctypes.c_double)),
+        ("dtype", ctypes.c_int),
+    ]
+
+
+class CgInfo(ctypes.Structure):  # perks_cg_info
+    _fields_ = [
+        ("variant", ctypes.c_int32),
+        ("policy", ctypes.c_int32),
+        ("grid", ctypes.c_int32),
+        ("block", ctypes.c_int32),
+        ("items_per_thread", ctypes.c_int32),
+        ("tiles", ctypes.c_int32),
+        ("smem_per_cta", ctypes.c_int32),
+        ("regs_per_thread", ctypes.c_int32),
+        ("cached_nnz_smem", ctypes.c_int64),
+        ("cached_rows_smem", ctypes.c_int64),
+        ("n_rows", ctypes.c_int64),
+        ("nnz", ctypes.c_int64),
+        ("dram_bytes_per_iter", ctypes.c_double),
+        ("unfused_bytes_per_iter", ctypes.c_double),
+        ("workspace_bytes", ctypes.c_size_t),
+        ("kernel_name", ctypes.c_char * 64),
+    ]
+
+
+CG_POLICIES = {"auto": 0, "imp": 1, "vec": 2, "mat": 3, "mix": 4}
+CG_POLICY_NAMES = {v: k for k, v in CG_POLICIES.items()}
+
+# Every symbol include/perks/perks_stencil.h and perks_cg.h declare, with (restype, argtypes).
 _VP = ctypes.c_void_p
 SIGNATURES = {
     "perks_stencil_create": (ctypes.c_int, [ctypes.POINTER(Desc), ctypes.c_int, ctypes.POINTER(_VP)]),
@@ -81,6 +116,17 @@ SIGNATURES = {
     "perks_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "perks_last_cuda_error": (ctypes.c_int, []),
     "perks_version": (ctypes.c_char_p, []),
+    # include/perks/perks_cg.h
+    "perks_cg_create": (ctypes.c_int, [ctypes.POINTER(CsrDesc), ctypes.c_int, ctypes.POINTER(_VP)]),
+    "perks_cg_workspace_bytes": (ctypes.c_int, [_VP, ctypes.POINTER(ctypes.c_size_t)]),
+    "perks_cg_spmv": (ctypes.c_int, [_VP, _VP, _VP, _VP, ctypes.c_size_t, _VP]),
+    "perks_cg_solve": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.c_int, _VP, _VP, ctypes.c_int64,
+                                      ctypes.c_double, _VP, _VP, _VP, ctypes.c_size_t, _VP]),
+    "perks_cg_solve_host": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.c_int, _VP, _VP, ctypes.c_int64,
+                                           ctypes.c_double, _VP, _VP]),
+    "perks_cg_query": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.c_int, ctypes.POINTER(CgInfo)]),
+    "perks_cg_partition": (ctypes.c_int, [_VP, ctypes.POINTER(ctypes.c_int64), ctypes.c_int32]),
+    "perks_cg_destroy": (ctypes.c_int, [_VP]),
 }
 
 

@@ -100,6 +100,10 @@ perks_status cuda_fail(cudaError_t e) {
   return PERKS_ERR_CUDA;
 }
 
+}  // namespace
+perks_status perks::cuda_status(cudaError_t e) { return cuda_fail(e); }
+namespace {
+
 template <int S> bool match_shape(const int32_t *off, int n) {
   if (n != Shape<S>::N) return false;
   for (int p = 0; p < n; p++)

@@ -124,6 +124,9 @@ cudaError_t run_wide3d(const Problem &p, const Plan &pl, const void *in, void *o
 // PERKS_TEST_BAR_BASE sets it (tests start the counter just below 2^32 to exercise the wrap).
 cudaError_t reset_grid_barrier(unsigned *bar, cudaStream_t s);
 
+// Map a failing CUDA call to a perks_status, recording it for perks_last_cuda_error (api.cu).
+perks_status cuda_status(cudaError_t e);
+
 // Environment override helper (sweeps only): returns def if unset.
 int env_int(const char *name, int def);
 
