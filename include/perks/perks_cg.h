@@ -18,12 +18,15 @@
  *                        device-wide barriers per iteration, nothing cached explicitly
  *                        (the paper's IMP policy);
  *   PERKS_PERKS      (c) (b) plus the cache policy: VEC keeps each CTA's own rows of r, x, p
- *                        and A p in shared memory, MAT keeps the CTA's CSR tiles resident in
- *                        shared memory across iterations, MIX both.
+ *                        and A p in shared memory, MAT keeps the CTA's matrix tiles resident in
+ *                        Tensor Memory and shared memory across iterations, MIX both
+ *                        (P:1749-1766).
  * SpMV is merge-based: each CTA owns a row-aligned share of the merge path of
  * (row ends, nonzeros) (the "TB-level search", done once at create and kept in device memory);
- * inside a CTA the share is cut into tiles of NT*IPT path items and each thread walks an equal
- * slice of a tile found by a merge-path search in shared memory (the "thread-level search").
+ * inside a CTA the share's nonzeros are cut into tiles of NT*IPT items, each thread owning IPT
+ * consecutive items (the "thread-level search", also done once at create: the library stores
+ * the matrix in this thread-interleaved item layout, with row-end marks and per-thread headers).
+ * MAT keeps the first tiles of each CTA in Tensor Memory and shared memory across iterations.
  * All variants and policies use the same partition and the same reduction order, so they are
  * bit-identical to one another (checked by the tests); against the oracle they agree within the
  * rounding bound of a reordered sum (RC1).
@@ -48,7 +51,7 @@ typedef enum {
   PERKS_CG_AUTO = 0, /* MIX                                                                   */
   PERKS_CG_IMP = 1,  /* nothing cached explicitly (L2 only)                                   */
   PERKS_CG_VEC = 2,  /* own rows of r, x, p, Ap in shared memory                              */
-  PERKS_CG_MAT = 3,  /* CSR tiles resident in shared memory, the rest streamed               */
+  PERKS_CG_MAT = 3,  /* matrix tiles resident in Tensor Memory + shared memory, rest streamed */
   PERKS_CG_MIX = 4   /* VEC + MAT                                                            */
 } perks_cg_policy;
 
@@ -77,13 +80,16 @@ typedef struct {
   int32_t tiles;              /* tiles over all CTAs                                          */
   int32_t smem_per_cta;       /* dynamic shared memory bytes                                  */
   int32_t regs_per_thread;
-  int64_t cached_nnz_smem;    /* nonzeros resident in shared memory across iterations (MAT)   */
+  int64_t cached_nnz_smem;    /* item slots (nonzeros) resident in shared memory (MAT)        */
   int64_t cached_rows_smem;   /* vector rows resident in shared memory (VEC; r, x, p, Ap each) */
   int64_t n_rows, nnz;
   double dram_bytes_per_iter; /* modelled DRAM bytes per iteration (CG rows)    */
   double unfused_bytes_per_iter; /* algorithmic bytes of one unfused iteration (the metric)   */
   size_t workspace_bytes;
   char kernel_name[64];
+  int64_t cached_nnz_tmem;    /* item slots resident in Tensor Memory across iterations (MAT) */
+  int32_t tmem_tiles_per_cta; /* resident tiles per CTA: Tensor Memory, shared memory          */
+  int32_t smem_tiles_per_cta;
 } perks_cg_info;
 
 /* Validates the CSR (INVALID_ARGUMENT on bad offsets or column indices; UNSUPPORTED when nnz or

@@ -87,6 +87,9 @@ class CgInfo(ctypes.Structure):  # perks_cg_info
         ("unfused_bytes_per_iter", ctypes.c_double),
         ("workspace_bytes", ctypes.c_size_t),
         ("kernel_name", ctypes.c_char * 64),
+        ("cached_nnz_tmem", ctypes.c_int64),
+        ("tmem_tiles_per_cta", ctypes.c_int32),
+        ("smem_tiles_per_cta", ctypes.c_int32),
     ]
 
 

@@ -5,21 +5,28 @@
 // kernel with device-wide barriers, (c) as PERKS with the cache policies IMP / VEC / MAT / MIX
 // (P:1749-1766).  B200 design (DESIGN.md §5 "CG"):
 //
-//   * Partition.  Merge path of (row ends, nonzeros) (length n + nnz).  CTA c owns a row-aligned
-//     share [R_c, R_{c+1}) (the CTA-level search, done once on the host at create and kept in
-//     device memory — "We save the search result of thread block workloads in global memory",
-//     P:1123).  Row-aligned shares need no cross-CTA carry, so A p for a CTA's own rows is
-//     complete inside the CTA and never leaves the SM.  The share is cut into tiles of NT*IPT
-//     path items (tile start coordinates also precomputed).
-//   * Tile = three contiguous CSR ranges (row offsets, column indices, values) moved into shared
-//     memory by 1D bulk copies (cp.async.bulk, mbarrier completion), double buffered; MAT keeps
-//     the first tiles of each CTA resident in shared memory for the whole solve instead.
-//   * SpMV of a tile: phase 1, coalesced over the tile's nonzeros, prod[k] = val[k] * p[col[k]]
-//     (independent gathers, full memory-level parallelism); phase 2, each thread finds its slice
-//     of the tile's merge path by a binary search in shared memory (the "thread-level search",
-//     P:1123) and sums products row by row; rows split between threads (or tiles) are combined
-//     from the per-thread carries in thread order — a fixed order, so every launch, variant and
-//     policy produces the same bits.
+//   * Partition (the paper's "TB-level search", saved once because "the matrix is static
+//     throughout the entire iteration").  CTA c owns a row-aligned share [R_c, R_{c+1})
+//     of the merge path of (row ends, nonzeros), so A p of its own rows is complete inside the
+//     CTA and never leaves the SM.
+//   * Thread-level work (the "thread-level search", also static, so done once at create): the
+//     share is a sequence of ITEMS — each nonzero of each row in storage order, an empty row
+//     contributing one zero item — cut into tiles of NT*IPT items, thread t of a tile owning IPT
+//     consecutive items.  Each item stores (value, column | END) where END marks the last item
+//     of a row; each thread has a header (its first row | OPEN, OPEN = that row began in an
+//     earlier thread).  Items are stored thread-interleaved ([e*NT + t]) so every warp load is
+//     coalesced.  This is the merge path with its search results precomputed: no per-iteration
+//     search, no row-offset reads, and the per-thread walk is a fully unrolled chain over
+//     registers: acc = fma(val, p[col], acc), a row ends -> store (bit-identical to the oracle's
+//     row sum unless the row is split between threads).
+//   * Rows split between threads or tiles: the thread whose first row is OPEN combines the
+//     partial sums of the preceding threads (and the previous tile's carry) in thread order —
+//     a fixed order, so every launch, variant and policy produces the same bits.
+//   * Where the items live across iterations (MAT / MIX): the first tiles of each CTA in Tensor
+//     Memory (each thread's items in its own TMEM lane/columns, read back with tcgen05.ld straight
+//     into the registers that use them; sm_100a's 256 KiB/SM that a non-contraction leaves idle),
+//     the next in shared memory (bulk-copied once at the start), the rest streamed from HBM with
+//     coalesced loads every iteration.
 //   * Two device-wide barriers per iteration instead of three: p_k of OTHER CTAs' rows is never
 //     read from memory during the SpMV; it is recomputed at the gather as fma(beta, p_{k-1}, r_k)
 //     from the published r_k and p_{k-1} (the owner computes its own rows with the same fma, so
@@ -44,76 +51,66 @@
 namespace perks {
 namespace cg {
 
-constexpr int NT = 512;       // threads per CTA (16 warps; one CTA per SM)
-constexpr int IPT = 6;        // merge-path items per thread per tile
-constexpr int TILE = NT * IPT;
+#ifndef PERKS_CG_IPT
+#define PERKS_CG_IPT 8
+#endif
+constexpr int NT = 512;             // threads per CTA (16 warps; one CTA per SM)
+constexpr int IPT = PERKS_CG_IPT;   // items per thread per tile
+constexpr int TI = NT * IPT;        // items per tile
 constexpr int kSmemMax = 227 * 1024;
+constexpr int kMaxG = 256;
+constexpr int PAD = 0x7fffffff;     // an empty item slot (after the CTA's last item)
+constexpr int COLMASK = 0x7fffffff; // column bits of an item word; 0x7fffffff = no column
+constexpr int TMEM_COLS = 512;      // one CTA per SM allocates all of TMEM
+constexpr int TMEM_COLS_PER_THREAD = TMEM_COLS / 4;  // 4 warps share each lane quarter
 
-// ------------------------------------------------------------------ tile geometry (host+device)
-// A tile covers path items [(i0,k0), (i1,k1)): rows_t = i1 - i0 completions, nnz_t = k1 - k0.
-// Shared-memory image: row_off[i0 - sro .. i1] | col[k0 - sc .. k1) | val[k0 - sv .. k1), each
-// part a 16-byte multiple starting 16-byte aligned (bulk copies need 16-B aligned addresses and
-// sizes); the shifts s* (< 16 bytes) absorb the misalignment of the global source.
-__host__ __device__ inline int a16(long long b) { return (int)((b + 15) & ~15ll); }
-template <typename T> struct TileGeo {
-  int sro, sc, sv;          // element shifts
-  int ro_b, col_b, val_b;   // copy bytes (16-multiples; 0 if nothing to copy)
-  __host__ __device__ TileGeo(int i0, int rows_t, int k0, int nnz_t) {
-    sro = i0 & 3;
-    sc = k0 & 3;
-    sv = k0 & (16 / (int)sizeof(T) - 1);
-    ro_b = a16((long long)(rows_t + 1 + sro) * 4);
-    col_b = nnz_t ? a16((long long)(nnz_t + sc) * 4) : 0;
-    val_b = nnz_t ? a16((long long)(nnz_t + sv) * (int)sizeof(T)) : 0;
-  }
-  __host__ __device__ int bytes() const { return ro_b + col_b + val_b; }
-};
-// Upper bound of any tile's image (rows_t + nnz_t <= TILE).
-template <typename T> constexpr int tile_max_bytes() {
-  return ((TILE + 1 + 3) * 4 + 15) / 16 * 16 + ((TILE + 3) * 4 + 15) / 16 * 16 +
-         ((TILE + 16 / (int)sizeof(T) - 1) * (int)sizeof(T) + 15) / 16 * 16;
-}
+// Bytes of one tile record (global and shared memory): values [TI] | item words [TI] | headers [NT].
+template <typename T> constexpr int tile_bytes() { return TI * ((int)sizeof(T) + 4) + NT * 4; }
+// TMEM words per thread per tile (values, item words, header), rounded to 8-column loads.
+template <typename T> constexpr int tmem_wpt() { return (IPT * (int)sizeof(T) / 4 + IPT + 1 + 7) / 8 * 8; }
+template <typename T> constexpr int tmem_tiles() { return TMEM_COLS_PER_THREAD / tmem_wpt<T>(); }
 
 template <typename T> struct Params {
   int n, G;
-  const int *row_off;     // n+1 (+pad)
-  const int *col;         // nnz (+pad)
-  const T *val;           // nnz (+pad)
-  const int2 *coords;     // tile start coordinates (row, nnz); CTA c: coords[ctile[c] .. ctile[c+1]-1]
-  const int *ctile;       //   (its last entry is the CTA's end coordinate)
-  const int *crow;        // G+1 row boundaries
+  const unsigned char *tiles;  // tile records, CTA c's at [ctile[c], ctile[c+1])
+  const int *ctile;            // G+1
+  const int *crow;             // G+1 row boundaries
   const T *b;
-  T *x;                   // output
-  T *r, *p0, *p1, *q;     // workspace vectors (global)
-  const T *xin;           // spmv: input vector (output in q)
-  double *slots;          // 2*G partial sums
-  double *scal;           // host loop: <r,r> by iteration parity [2]
-  long long *state;       // host loop: [0] done, [1] iterations, [2] status
-  unsigned *bar;          // grid barrier words
-  double *hist;           // nullable, kmax+1
-  long long *info;        // nullable, 2
+  T *x;                        // output
+  T *r, *p0, *p1, *q;          // workspace vectors (global)
+  const T *xin;                // spmv: input vector (output in q)
+  double *slots;               // 2*G partial sums
+  double *scal;                // host loop: <r,r> by iteration parity [2]
+  long long *state;            // host loop: [0] done, [1] iterations, [2] status
+  unsigned *bar;               // grid barrier words
+  LLWord *ll;                  // persistent (PERKS_CG_LL=1): 2*G tagged all-reduce slots
+  unsigned long long *dbg;     // nullable: phase timer (PERKS_CG_TIMING)
+  double *hist;                // nullable, kmax+1
+  long long *info;             // nullable, 2
   long long kmax;
   double tol2;
-  int rows_max;           // max own rows over CTAs (VEC arrays)
-  int res_budget;         // bytes of resident-tile region (MAT); 0 = stream everything
-  int stream;             // 1 if this launch streams tiles (double buffer present)
+  int rows_max;                // max own rows over CTAs (VEC arrays)
+  int tm_tiles;                // tiles per CTA resident in TMEM (MAT)
+  int sm_tiles;                // tiles per CTA resident in shared memory (MAT)
+  int nbuf;                    // stream ring buffers (0: direct loads)
+  int fused;                   // persistent: 2 barriers/iteration (p recomputed at the gather)
+  int use_ll;
 };
 
 // Dynamic shared memory layout.
 struct Smem {
-  static constexpr int RED = 0;                       // 32 doubles
-  static constexpr int MBAR = RED + 32 * 8;           // 3 mbarriers (2 stream + 1 resident)
-  static constexpr int TCAR = MBAR + 32;              // tile carries [2]: valid + value (16 B each)
-  static constexpr int BCAST = TCAR + 32;             // reduction broadcasts [4] (doubles)
-  static constexpr int CROW = BCAST + 32;             // NT ints
-  static constexpr int CVAL = CROW + NT * 4;          // NT doubles (T)
-  static constexpr int PROD = CVAL + NT * 8;          // TILE values
-  template <typename T> static constexpr int vec_off() { return PROD + TILE * (int)sizeof(T); }
+  static constexpr int RED = 0;                        // 32 doubles
+  static constexpr int MBAR = RED + 256;               // mbarriers: resident tiles, ring [<= 7]
+  static constexpr int TMEMB = MBAR + 64;              // TMEM base address
+  static constexpr int BCAST = TMEMB + 16;             // reduction broadcasts [4] (doubles)
+  static constexpr int TCAR = BCAST + 32;              // tile carries [2]: row, have, value (16 B each)
+  static constexpr int CROW = TCAR + 32;               // [2][NT] ints: carry row | HAVE
+  static constexpr int CVAL = CROW + 2 * NT * 4;       // [2][NT] T (8-byte slots)
+  static constexpr int VEC = CVAL + 2 * NT * 8;        // VEC arrays, then resident tiles
 };
-template <typename T> inline int smem_bytes(int vec_rows, bool stream, int res_budget) {
-  int b = Smem::vec_off<T>() + 4 * a16((long long)vec_rows * (int)sizeof(T));
-  if (stream) b += 2 * tile_max_bytes<T>();
-  return b + res_budget;
+__host__ __device__ inline int a16(long long b) { return (int)((b + 15) & ~15ll); }
+template <typename T> inline int smem_bytes(int vec_rows, int nbuf, int sm_tiles) {
+  return Smem::VEC + 4 * a16((long long)vec_rows * (int)sizeof(T)) + (nbuf + sm_tiles) * tile_bytes<T>();
 }
 
 // ------------------------------------------------------------------------ reductions
@@ -136,7 +133,6 @@ PERKS_DEVINL double block_sum(double v, double *s_red) {
 // Sum of the G slot partials (written by other CTAs before a grid barrier), fixed order.  One
 // warp reads the slots (all loads in flight together; lane l sums slots l, l+32, ... in order),
 // reduces, and broadcasts through shared memory — every thread gets the same value.
-constexpr int kMaxG = 256;
 PERKS_DEVINL double slots_sum(const double *slots, int G, double *s_bc) {
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
@@ -153,235 +149,285 @@ PERKS_DEVINL double slots_sum(const double *slots, int G, double *s_bc) {
   return *s_bc;
 }
 
-// ------------------------------------------------------------------------ tile pipeline
-template <typename T> struct TileView {
-  const int *ro;   // ro[m] = row_off[i0 + m], m = 0..rows_t
-  const int *col;  // col[e] = col[k0 + e]
-  const T *val;
-  int i0, k0, rows_t, nnz_t;
+// ------------------------------------------------------------------------ tiles
+// One thread's items of one tile, in registers.
+template <typename T> struct Items {
+  T v[IPT];
+  int w[IPT];  // column | END (bit 31); PAD = empty slot
+  int hdr;     // first row | OPEN (bit 31)
 };
 
 template <typename T>
-PERKS_DEVINL TileView<T> tile_view(unsigned char *base, int i0, int k0, int rows_t, int nnz_t) {
-  const TileGeo<T> g(i0, rows_t, k0, nnz_t);
-  TileView<T> v;
-  v.ro = reinterpret_cast<const int *>(base) + g.sro;
-  v.col = reinterpret_cast<const int *>(base + g.ro_b) + g.sc;
-  v.val = reinterpret_cast<const T *>(base + g.ro_b + g.col_b) + g.sv;
-  v.i0 = i0; v.k0 = k0; v.rows_t = rows_t; v.nnz_t = nnz_t;
-  return v;
-}
-
-// One thread: bulk copies of a tile image into `dst`, completing on `mb` (expect_tx included).
-template <typename T>
-PERKS_DEVINL void issue_tile(const Params<T> &P, unsigned char *dst, int i0, int k0, int rows_t, int nnz_t,
-                             uint64_t *mb, bool arm = true) {
-  const TileGeo<T> g(i0, rows_t, k0, nnz_t);
-  if (arm) mbar_arrive_tx(mb, (unsigned)g.bytes());
-  bulk_load(dst, P.row_off + (i0 - g.sro), (unsigned)g.ro_b, mb);
-  if (nnz_t) {
-    bulk_load(dst + g.ro_b, P.col + (k0 - g.sc), (unsigned)g.col_b, mb);
-    bulk_load(dst + g.ro_b + g.col_b, P.val + (k0 - g.sv), (unsigned)g.val_b, mb);
+PERKS_DEVINL void items_from(const unsigned char *rec, Items<T> &it, bool stream) {
+  const T *val = reinterpret_cast<const T *>(rec);
+  const int *wrd = reinterpret_cast<const int *>(rec + TI * sizeof(T));
+  const int *hdr = reinterpret_cast<const int *>(rec + TI * (sizeof(T) + 4));
+  const int t = threadIdx.x;
+  if (stream) {  // HBM stream: read once per iteration, do not keep in L1
+#pragma unroll
+    for (int e = 0; e < IPT; ++e) { it.v[e] = __ldcs(val + e * NT + t); it.w[e] = __ldcs(wrd + e * NT + t); }
+    it.hdr = __ldcs(hdr + t);
+  } else {       // shared-memory resident tile
+#pragma unroll
+    for (int e = 0; e < IPT; ++e) { it.v[e] = val[e * NT + t]; it.w[e] = wrd[e * NT + t]; }
+    it.hdr = hdr[t];
   }
 }
 
-// Tile carry between consecutive tiles of one CTA (the partial sum of the row a tile ends in).
+// TMEM: thread (warp w, lane l) owns lane 32*(w%4)+l, columns (w/4)*128 + slot*WPT .. +WPT.
+template <typename T> PERKS_DEVINL uint32_t tmem_addr(uint32_t base, int slot) {
+  const int w = threadIdx.x >> 5;
+  return base + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)((w >> 2) * TMEM_COLS_PER_THREAD + slot * tmem_wpt<T>());
+}
+template <typename T> PERKS_DEVINL void items_to_tmem(uint32_t taddr, const Items<T> &it) {
+  constexpr int W = tmem_wpt<T>();
+  uint32_t wd[W];
+#pragma unroll
+  for (int i = 0; i < W; ++i) wd[i] = 0;
+#pragma unroll
+  for (int e = 0; e < IPT; ++e) {
+    if constexpr (sizeof(T) == 8) {
+      const unsigned long long b = (unsigned long long)__double_as_longlong((double)it.v[e]);
+      wd[2 * e] = (uint32_t)b;
+      wd[2 * e + 1] = (uint32_t)(b >> 32);
+    } else {
+      wd[e] = __float_as_uint((float)it.v[e]);
+    }
+    wd[IPT * sizeof(T) / 4 + e] = (uint32_t)it.w[e];
+  }
+  wd[IPT * sizeof(T) / 4 + IPT] = (uint32_t)it.hdr;
+#pragma unroll
+  for (int g = 0; g < W / 8; ++g) {
+    uint32_t c[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) c[j] = wd[8 * g + j];
+    tmem_st8(taddr + 8 * g, c);
+  }
+}
+template <typename T> PERKS_DEVINL void items_from_tmem(uint32_t taddr, Items<T> &it) {
+  constexpr int W = tmem_wpt<T>();
+  uint32_t wd[W];
+#pragma unroll
+  for (int g = 0; g < W / 8; ++g) {
+    uint32_t c[8];
+    tmem_ld8(taddr + 8 * g, c);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) wd[8 * g + j] = c[j];
+  }
+  tmem_wait_ld();
+#pragma unroll
+  for (int e = 0; e < IPT; ++e) {
+    if constexpr (sizeof(T) == 8)
+      it.v[e] = (T)__longlong_as_double((long long)((unsigned long long)wd[2 * e] | ((unsigned long long)wd[2 * e + 1] << 32)));
+    else
+      it.v[e] = (T)__uint_as_float(wd[e]);
+    it.w[e] = (int)wd[IPT * sizeof(T) / 4 + e];
+  }
+  it.hdr = (int)wd[IPT * sizeof(T) / 4 + IPT];
+}
+
+// Tile carry between consecutive tiles of one CTA: the partial sum of the row a tile ends in.
 template <typename T> struct TileCarry {
-  int valid;
-  int pad;
+  int row, have;
   T val;
 };
 
-// SpMV of one tile (see the header comment).  gather(j) returns the vector value at column j;
-// qstore(row, v) stores a completed row.  Ends with __syncthreads.
-// The tile carry is double buffered by tile parity (read tc[par], write tc[par ^ 1]) so the
-// writer of the next carry never races the readers of this one.
+// SpMV of one tile's items (see the header comment).  gather.load(col, a, b) issues the loads
+// for column `col` (col < 0: none), gather.value(col, a, b) returns the vector value;
+// qstore(row, v) stores a completed row.  `m` = tile index in the CTA (parity of the carry
+// buffers); `last` = no carry into a next tile.  Contains one __syncthreads (between the walk
+// and the carry fix-up); the fix-up's q stores become visible after the caller's next barrier.
 template <typename T, class Gather, class QStore>
-PERKS_DEVINL void tile_spmv(const TileView<T> &t, unsigned char *smem, int par, bool last, Gather gather,
+PERKS_DEVINL void tile_spmv(const Items<T> &it, unsigned char *smem, int m, bool last, const Gather &gather,
                             QStore qstore) {
-  T *s_prod = reinterpret_cast<T *>(smem + Smem::PROD);
-  int *s_crow = reinterpret_cast<int *>(smem + Smem::CROW);
-  T *s_cval = reinterpret_cast<T *>(smem + Smem::CVAL);
+  const int par = m & 1;
+  int *s_crow = reinterpret_cast<int *>(smem + Smem::CROW) + par * NT;
+  T *s_cval = reinterpret_cast<T *>(smem + Smem::CVAL + par * NT * 8);
   const TileCarry<T> *tc = reinterpret_cast<TileCarry<T> *>(smem + Smem::TCAR) + par;
   TileCarry<T> *tn = reinterpret_cast<TileCarry<T> *>(smem + Smem::TCAR) + (par ^ 1);
   const int tid = threadIdx.x;
-  // phase 1: products, coalesced over the nonzeros; all IPT gathers of a thread in flight at once
-  {
-    int cj[IPT];
-    T vj[IPT], gj[IPT];
+  // gathers: every load issued before any is used
+  int jc[IPT];
+  T ga[IPT], gb[IPT];
 #pragma unroll
-    for (int j = 0; j < IPT; ++j) {
-      const int e = tid + j * NT;
-      cj[j] = e < t.nnz_t ? t.col[e] : -1;
-      vj[j] = e < t.nnz_t ? t.val[e] : T(0);
-    }
-#pragma unroll
-    for (int j = 0; j < IPT; ++j) gj[j] = cj[j] >= 0 ? gather(cj[j]) : T(0);
-#pragma unroll
-    for (int j = 0; j < IPT; ++j) {
-      const int e = tid + j * NT;
-      if (e < t.nnz_t) s_prod[e] = mul_rn(vj[j], gj[j]);
-    }
+  for (int e = 0; e < IPT; ++e) {
+    const int c = it.w[e] & COLMASK;  // PAD and empty-row items carry no column
+    jc[e] = c == COLMASK ? -1 : c;
+    gather.load(jc[e], ga[e], gb[e]);
   }
-  __syncthreads();
-  // phase 2: thread-level merge-path search + row sums
-  const int items = t.rows_t + t.nnz_t;
-  const int ipt = (items + NT - 1) / NT;
-  int d = min(tid * ipt, items);
-  const int dend = min(d + ipt, items);
-  int lo = max(0, d - t.nnz_t), hi = min(d, t.rows_t);
-  while (lo < hi) {  // rows completed before diagonal d: row m ends (ro[m+1]-k0) at or before nnz d-1-m
-    const int mid = (lo + hi) >> 1;
-    if (t.ro[mid + 1] - t.k0 <= d - 1 - mid) lo = mid + 1;
-    else hi = mid;
-  }
-  int i = lo, k = d - lo;
-  bool pending = (k + t.k0 > t.ro[i]);  // row i0+i already has terms before this thread's slice
+  // the walk: an unrolled fma chain per row segment
+  int row = it.hdr & 0x7fffffff;
+  bool open = it.hdr < 0;
   T acc = T(0), sval = T(0);
+  bool have = false;
   int srow = -1;
-  for (; d < dend; ++d) {
-    if (i < t.rows_t && k + t.k0 >= t.ro[i + 1]) {  // row i complete
-      if (pending) { srow = i; sval = acc; pending = false; }
-      else qstore(t.i0 + i, acc);
+  // (PAD slots only follow the CTA's last row: their zero terms and `have` are never read)
+#pragma unroll
+  for (int e = 0; e < IPT; ++e) {
+    acc = fma_rn(it.v[e], gather.value(jc[e], ga[e], gb[e]), acc);
+    have = true;
+    if (it.w[e] < 0) {  // END: row complete
+      if (open) { srow = row; sval = acc; open = false; }
+      else qstore(row, acc);
       acc = T(0);
-      ++i;
-    } else {
-      acc = acc + s_prod[k];
-      ++k;
+      have = false;
+      ++row;
     }
   }
-  s_crow[tid] = i;
+  s_crow[tid] = row | (have ? (int)0x80000000 : 0);
   s_cval[tid] = acc;
   __syncthreads();
-  if (srow >= 0) {  // first completed row of a slice that started mid-row: carries in thread order
+  if (srow >= 0) {  // the first row of this thread began earlier: partials in thread order
+    const int key = srow | (int)0x80000000;
     int t0 = tid;
-    while (t0 > 0 && s_crow[t0 - 1] == srow) --t0;
-    bool have = false;
+    while (t0 > 0 && s_crow[t0 - 1] == key) --t0;
+    bool h = false;
     T v = T(0);
-    if (t0 == 0 && srow == 0 && tc->valid) { v = tc->val; have = true; }
-    for (int u = t0; u < tid; ++u) { v = have ? v + s_cval[u] : s_cval[u]; have = true; }
-    v = have ? v + sval : sval;
-    qstore(t.i0 + srow, v);
+    if (t0 == 0 && tc->have && tc->row == srow) { v = tc->val; h = true; }
+    for (int u = t0; u < tid; ++u) { v = h ? v + s_cval[u] : s_cval[u]; h = true; }
+    qstore(srow, h ? v + sval : sval);
   }
-  if (!last && tid == NT - 1) {  // carry into the next tile: the partial sum of row i0 + rows_t
-                                 // (the CTA's last tile ends on a row boundary: no carry)
-    int t0 = NT;
-    while (t0 > 0 && s_crow[t0 - 1] == t.rows_t) --t0;
-    bool have = false;
-    T v = T(0);
-    if (t0 == 0 && t.rows_t == 0 && tc->valid) { v = tc->val; have = true; }
-    for (int u = t0; u < NT; ++u) { v = have ? v + s_cval[u] : s_cval[u]; have = true; }
-    tn->val = v;
-    tn->valid = have ? 1 : 0;
+  if (!last && tid == NT - 1) {  // carry into the next tile (full tiles only: no padding)
+    const int key = s_crow[NT - 1];
+    TileCarry<T> o;
+    o.row = key & 0x7fffffff;
+    o.have = 0;
+    o.val = T(0);
+    if (key < 0) {
+      int t0 = NT;
+      while (t0 > 0 && s_crow[t0 - 1] == key) --t0;
+      bool h = false;
+      T v = T(0);
+      if (t0 == 0 && tc->have && tc->row == o.row) { v = tc->val; h = true; }
+      for (int u = t0; u < NT; ++u) { v = h ? v + s_cval[u] : s_cval[u]; h = true; }
+      o.have = 1;
+      o.val = v;
+    }
+    *tn = o;
   }
-  __syncthreads();
 }
 
-// Streams / resident tiles of CTA c through tile_spmv.  State of the double buffer lives in the
-// caller (u = next stream sequence number to consume; persistent launches wrap around so the
-// first tiles of the next iteration are in flight across the barrier).
-template <typename T> struct Pipe {
-  int tb, nt;        // first coordinate index, tile count
-  int mres;          // resident tiles
-  int ns;            // streamed tiles
-  long long u;       // next streamed sequence number to consume
-  long long issued;  // streamed sequence numbers issued
-  unsigned char *sbuf;  // stream buffer b at sbuf + b * sstride
-  int sstride;
-  unsigned char *res;
+// Tiles of CTA c: the first tm in TMEM, the next sm in shared memory, the rest streamed — through
+// a ring of nb shared-memory buffers filled by bulk copies (TMA, mbarrier completion) issued nb
+// tiles ahead of the consumer (nb = 0: coalesced loads straight into registers).  Persistent
+// launches keep streaming across iteration boundaries (the next iteration's first tiles load
+// during the all-reduces); `issued` counts streamed sequence numbers issued, `u` consumed.
+struct TileSet {
+  int tb, nt, tm, sm, nb;
+  uint32_t tbase;             // TMEM base address (tm > 0)
+  const unsigned char *sres;  // shared-memory resident tiles
+  unsigned char *ring;        // nb stream buffers
+  long long u, issued;
+  bool wrap;
 };
 
-template <typename T>
-PERKS_DEVINL void pipe_issue_next(const Params<T> &P, Pipe<T> &pp, uint64_t *mbar, bool wrap) {
-  // thread 0 only: keep two streamed tiles in flight
-  while (pp.ns > 0 && pp.issued < pp.u + 2 && (wrap || pp.issued < pp.ns)) {
-    const int m = pp.mres + (int)(pp.issued % pp.ns);
-    const int2 a = P.coords[pp.tb + m], e = P.coords[pp.tb + m + 1];
-    const int buf = (int)(pp.issued & 1);
-    issue_tile<T>(P, pp.sbuf + buf * pp.sstride, a.x, a.y, e.x - a.x, e.y - a.y, mbar + buf);
-    ++pp.issued;
+template <typename T> PERKS_DEVINL void ring_issue(const Params<T> &P, TileSet &ts, unsigned char *smem) {
+  // thread 0 only
+  const int first = ts.tm + ts.sm, ns = ts.nt - first;
+  if (ts.nb == 0 || ns <= 0) return;
+  uint64_t *mb = reinterpret_cast<uint64_t *>(smem + Smem::MBAR) + 1;
+  while (ts.issued < ts.u + ts.nb && (ts.wrap || ts.issued < ns)) {
+    const int m = first + (int)(ts.issued % ns);
+    const int b = (int)(ts.issued % ts.nb);
+    mbar_arrive_tx(mb + b, (unsigned)tile_bytes<T>());
+    bulk_load(ts.ring + (size_t)b * tile_bytes<T>(), P.tiles + (size_t)(ts.tb + m) * tile_bytes<T>(),
+              (unsigned)tile_bytes<T>(), mb + b);
+    ++ts.issued;
   }
 }
 
 template <typename T, class Gather, class QStore>
-PERKS_DEVINL void spmv_cta(const Params<T> &P, Pipe<T> &pp, unsigned char *smem, bool wrap, Gather gather,
+PERKS_DEVINL void spmv_cta(const Params<T> &P, TileSet &ts, unsigned char *smem, const Gather &gather,
                            QStore qstore) {
-  uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + Smem::MBAR);
-  TileCarry<T> *tc = reinterpret_cast<TileCarry<T> *>(smem + Smem::TCAR);
-  if (threadIdx.x == 0) tc->valid = 0;  // CTA shares start on a row boundary
-  __syncthreads();
-  int roff = 0;
-  for (int m = 0; m < pp.nt; ++m) {
-    const int2 a = P.coords[pp.tb + m], e = P.coords[pp.tb + m + 1];
-    const int rows_t = e.x - a.x, nnz_t = e.y - a.y;
-    unsigned char *img;
-    if (m < pp.mres) {
-      img = pp.res + roff;
-      roff += TileGeo<T>(a.x, rows_t, a.y, nnz_t).bytes();
+  if (threadIdx.x == 0) reinterpret_cast<TileCarry<T> *>(smem + Smem::TCAR)->have = 0;
+  // (the carry reset is read only after the first tile's __syncthreads)
+  uint64_t *mb = reinterpret_cast<uint64_t *>(smem + Smem::MBAR) + 1;
+  for (int m = 0; m < ts.nt; ++m) {
+    Items<T> it;
+    const bool streamed = m >= ts.tm + ts.sm;
+    if (m < ts.tm) {
+      items_from_tmem<T>(tmem_addr<T>(ts.tbase, m), it);
+    } else if (!streamed) {
+      items_from<T>(ts.sres + (size_t)(m - ts.tm) * tile_bytes<T>(), it, false);
+    } else if (ts.nb > 0) {
+      const int b = (int)(ts.u % ts.nb);
+      mbar_wait(mb + b, (unsigned)((ts.u / ts.nb) & 1));
+      items_from<T>(ts.ring + (size_t)b * tile_bytes<T>(), it, false);
     } else {
-      const int buf = (int)(pp.u & 1);
-      mbar_wait(mbar + buf, (unsigned)((pp.u >> 1) & 1));
-      img = pp.sbuf + buf * pp.sstride;
+      items_from<T>(P.tiles + (size_t)(ts.tb + m) * tile_bytes<T>(), it, true);
     }
-    tile_spmv<T>(tile_view<T>(img, a.x, a.y, rows_t, nnz_t), smem, m & 1, m == pp.nt - 1, gather, qstore);
-    if (m >= pp.mres) {
-      ++pp.u;
-      if (threadIdx.x == 0) pipe_issue_next<T>(P, pp, mbar, wrap);
+    tile_spmv<T>(it, smem, m, m == ts.nt - 1, gather, qstore);
+    // (tile_spmv's __syncthreads follows every thread's item reads: the ring slot is free)
+    if (streamed && ts.nb > 0) {
+      ++ts.u;
+      if (threadIdx.x == 0) ring_issue<T>(P, ts, smem);
     }
   }
+  __syncthreads();  // the last fix-up's stores before anyone reads q
 }
 
+// Resident tiles (persistent MAT/MIX): TMEM tiles through registers, shared-memory tiles by one
+// bulk copy each; the stream ring's first copies.  Returns the CTA's tile set.
 template <typename T>
-PERKS_DEVINL void pipe_init(const Params<T> &P, Pipe<T> &pp, unsigned char *smem, int vec_rows, bool wrap) {
+PERKS_DEVINL TileSet tiles_init(const Params<T> &P, unsigned char *smem, int vec_rows, bool resident, bool wrap) {
+  TileSet ts;
   const int c = blockIdx.x;
-  pp.tb = P.ctile[c];
-  pp.nt = P.ctile[c + 1] - pp.tb - 1;
-  unsigned char *p = smem + Smem::vec_off<T>() + 4 * a16((long long)vec_rows * (int)sizeof(T));
-  pp.sbuf = p;
-  pp.sstride = P.stream ? tile_max_bytes<T>() : 0;
-  pp.res = p + (P.stream ? 2 * tile_max_bytes<T>() : 0);
-  // resident tiles: the first tiles of the CTA while their images fit the budget
-  int used = 0, mres = 0;
-  for (int m = 0; m < pp.nt; ++m) {
-    const int2 a = P.coords[pp.tb + m], e = P.coords[pp.tb + m + 1];
-    const int bts = TileGeo<T>(a.x, e.x - a.x, a.y, e.y - a.y).bytes();
-    if (used + bts > P.res_budget) break;
-    used += bts;
-    ++mres;
-  }
-  pp.mres = mres;
-  pp.ns = pp.nt - mres;
-  pp.u = 0;
-  pp.issued = 0;
-  uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + Smem::MBAR);
+  ts.tb = P.ctile[c];
+  ts.nt = P.ctile[c + 1] - ts.tb;
+  ts.tm = resident ? min(ts.nt, P.tm_tiles) : 0;
+  ts.sm = resident ? min(ts.nt - ts.tm, P.sm_tiles) : 0;
+  ts.nb = P.nbuf;
+  ts.tbase = 0;
+  ts.ring = smem + Smem::VEC + 4 * a16((long long)vec_rows * (int)sizeof(T));
+  ts.sres = ts.ring + (size_t)ts.nb * tile_bytes<T>();
+  ts.u = 0;
+  ts.issued = 0;
+  ts.wrap = wrap;
+  uint64_t *mb = reinterpret_cast<uint64_t *>(smem + Smem::MBAR);
   if (threadIdx.x == 0) {
-    mbar_init(mbar + 0, 1);
-    mbar_init(mbar + 1, 1);
-    mbar_init(mbar + 2, 1);
+    for (int b = 0; b <= ts.nb; ++b) mbar_init(mb + b, 1);
     mbar_fence_init();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (mres > 0) {  // resident tiles: one mbarrier phase for all of them
-      mbar_arrive_tx(mbar + 2, (unsigned)used);
-      int off = 0;
-      for (int m = 0; m < mres; ++m) {
-        const int2 a = P.coords[pp.tb + m], e = P.coords[pp.tb + m + 1];
-        issue_tile<T>(P, pp.res + off, a.x, a.y, e.x - a.x, e.y - a.y, mbar + 2, false);
-        off += TileGeo<T>(a.x, e.x - a.x, a.y, e.y - a.y).bytes();
-      }
+    if (ts.sm > 0) {
+      mbar_arrive_tx(mb, (unsigned)(ts.sm * tile_bytes<T>()));
+      for (int s = 0; s < ts.sm; ++s)
+        bulk_load(const_cast<unsigned char *>(ts.sres) + (size_t)s * tile_bytes<T>(),
+                  P.tiles + (size_t)(ts.tb + ts.tm + s) * tile_bytes<T>(), (unsigned)tile_bytes<T>(), mb);
     }
-    pipe_issue_next<T>(P, pp, mbar, wrap);
+    ring_issue<T>(P, ts, smem);
   }
-  if (mres > 0) mbar_wait(mbar + 2, 0);
+  if (ts.tm > 0) {
+    uint32_t *s_tb = reinterpret_cast<uint32_t *>(smem + Smem::TMEMB);
+    if (threadIdx.x < 32) {
+      tmem_alloc(s_tb, TMEM_COLS);
+      tmem_relinquish();
+    }
+    tmem_fence_before_sync();
+    __syncthreads();
+    tmem_fence_after_sync();
+    ts.tbase = *s_tb;
+    for (int m = 0; m < ts.tm; ++m) {
+      Items<T> it;
+      items_from<T>(P.tiles + (size_t)(ts.tb + m) * tile_bytes<T>(), it, true);
+      items_to_tmem<T>(tmem_addr<T>(ts.tbase, m), it);
+    }
+    tmem_wait_st();
+  }
+  if (ts.sm > 0) mbar_wait(mb, 0);
+  __syncthreads();
+  return ts;
 }
 
-// Before exit: every issued bulk copy must have landed (thread 0 waits on the outstanding ones).
-template <typename T> PERKS_DEVINL void pipe_drain(Pipe<T> &pp, unsigned char *smem) {
-  uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + Smem::MBAR);
+template <typename T> PERKS_DEVINL void tiles_fini(TileSet &ts, unsigned char *smem) {
+  // every issued bulk copy must land before the CTA exits
+  uint64_t *mb = reinterpret_cast<uint64_t *>(smem + Smem::MBAR) + 1;
   if (threadIdx.x == 0)
-    for (long long v = pp.u; v < pp.issued; ++v) mbar_wait(mbar + (v & 1), (unsigned)((v >> 1) & 1));
-  __syncthreads();
+    for (long long v = ts.u; v < ts.issued; ++v) mbar_wait(mb + (v % ts.nb), (unsigned)((v / ts.nb) & 1));
+  if (ts.tm > 0) {
+    tmem_fence_before_sync();
+    __syncthreads();
+    tmem_fence_after_sync();
+    if (threadIdx.x < 32) tmem_dealloc(ts.tbase, TMEM_COLS);
+  }
 }
 
 // ------------------------------------------------------------------------ CG building blocks
@@ -397,7 +443,7 @@ PERKS_DEVINL Own<T, VEC> own_view(const Params<T> &P, unsigned char *smem) {
   o.R0 = P.crow[blockIdx.x];
   o.rows = P.crow[blockIdx.x + 1] - o.R0;
   const int vb = a16((long long)P.rows_max * (int)sizeof(T));
-  unsigned char *v = smem + Smem::vec_off<T>();
+  unsigned char *v = smem + Smem::VEC;
   o.s_r = reinterpret_cast<T *>(v);
   o.s_x = reinterpret_cast<T *>(v + vb);
   o.s_p = reinterpret_cast<T *>(v + 2 * vb);
@@ -405,15 +451,17 @@ PERKS_DEVINL Own<T, VEC> own_view(const Params<T> &P, unsigned char *smem) {
   return o;
 }
 
-// x_0 = 0, r_0 = b (published for the gathers); returns this thread's part of <r_0, r_0>.
+// x_0 = 0, r_0 = b, p_{-1} = 0 (published for the gathers); returns this thread's part of
+// <r_0, r_0>.
 template <typename T, bool VEC> PERKS_DEVINL double cg_prologue(const Params<T> &P, const Own<T, VEC> &o) {
   double acc = 0.0;
   for (int j = threadIdx.x; j < o.rows; j += NT) {
     const int i = o.R0 + j;
     const T bi = P.b[i];
-    if (VEC) { o.s_x[j] = T(0); o.s_r[j] = bi; }
+    if (VEC) { o.s_x[j] = T(0); o.s_r[j] = bi; o.s_p[j] = T(0); }
     else P.x[i] = T(0);
     P.r[i] = bi;
+    P.p1[i] = T(0);  // p_{-1} = 0: p_0 = fma(0, p_{-1}, r_0) = r_0 with the general update
     acc = fma_rn((double)bi, (double)bi, acc);
   }
   return acc;
@@ -423,9 +471,10 @@ template <typename T, bool VEC> PERKS_DEVINL double cg_prologue(const Params<T> 
 // inner-product chain); U rows per batch so their loads are in flight together.
 constexpr int U = 4;
 
-// p_k (own rows): p_0 = r_0; p_k = fma(beta, p_{k-1}, r_k); published into pcur.
+// p_k (own rows) = fma(beta, p_{k-1}, r_k) (k = 0: beta = 0 and p_{-1} = 0, so p_0 = r_0),
+// published into pcur.
 template <typename T, bool VEC>
-PERKS_DEVINL void cg_p_update(const Params<T> &P, const Own<T, VEC> &o, bool first, T beta, const T *pprev, T *pcur) {
+PERKS_DEVINL void cg_p_update(const Params<T> &P, const Own<T, VEC> &o, T beta, const T *pprev, T *pcur) {
   for (int j0 = threadIdx.x; j0 < o.rows; j0 += U * NT) {
     T r[U], pp[U];
 #pragma unroll
@@ -433,13 +482,13 @@ PERKS_DEVINL void cg_p_update(const Params<T> &P, const Own<T, VEC> &o, bool fir
       const int j = j0 + u * NT, i = o.R0 + j;
       const bool ok = j < o.rows;
       r[u] = ok ? (VEC ? o.s_r[j] : __ldcg(P.r + i)) : T(0);
-      pp[u] = ok && !first ? (VEC ? o.s_p[j] : __ldcg(pprev + i)) : T(0);
+      pp[u] = ok ? (VEC ? o.s_p[j] : __ldcg(pprev + i)) : T(0);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int j = j0 + u * NT;
       if (j < o.rows) {
-        const T p = first ? r[u] : fma_rn(beta, pp[u], r[u]);
+        const T p = fma_rn(beta, pp[u], r[u]);
         if (VEC) o.s_p[j] = p;
         pcur[o.R0 + j] = p;
       }
@@ -500,74 +549,171 @@ PERKS_DEVINL double cg_xr_update(const Params<T> &P, const Own<T, VEC> &o, T a, 
   return acc;
 }
 
-// The SpMV A p_k of the CTA's own rows, gathers as described in the header.
+// Gather of p_k at column jc for the SpMV of iteration k.
+//   FUSED (two barriers per iteration): own columns from the buffer this CTA just wrote, other
+//   CTAs' columns recomputed as fma(beta, p_{k-1}, r_k) from their published p_{k-1} and r_k (the
+//   owner computed p_k with the same fma: identical values).
+//   !FUSED (three barriers): every CTA published p_k before a grid barrier; one load.
+// load() issues the loads (branch-free: selects and a predicated second load), value()
+// combines them.  jc = -1: no column (padding / empty row), value 0.
+template <typename T, bool FUSED> struct CgGather {
+  int R0, rows;
+  T beta;
+  const T *pcur, *pprev, *r;
+  PERKS_DEVINL void load(int jc, T &a, T &b) const {
+    const int j = jc < 0 ? 0 : jc;
+    if (!FUSED) {
+      a = __ldcg(pcur + j);
+      b = T(0);
+      return;
+    }
+    const bool own = (unsigned)(j - R0) < (unsigned)rows;
+    a = __ldcg((own ? pcur : pprev) + j);
+    b = own ? T(0) : __ldcg(r + j);
+  }
+  PERKS_DEVINL T value(int jc, T a, T b) const {
+    if (jc < 0) return T(0);
+    if (!FUSED) return a;
+    const bool own = (unsigned)(jc - R0) < (unsigned)rows;
+    return own ? a : fma_rn(beta, a, b);
+  }
+};
+
+template <typename T> struct PlainGather {  // standalone SpMV: x[j]
+  const T *x;
+  PERKS_DEVINL void load(int j, T &a, T &b) const {
+    a = __ldg(x + (j < 0 ? 0 : j));
+    b = T(0);
+  }
+  PERKS_DEVINL T value(int j, T a, T) const { return j < 0 ? T(0) : a; }
+};
+
 template <typename T, bool VEC>
-PERKS_DEVINL void cg_spmv(const Params<T> &P, const Own<T, VEC> &o, Pipe<T> &pp, unsigned char *smem, bool wrap,
-                          bool first, T beta, const T *pprev, const T *pcur) {
-  const int R0 = o.R0, rows = o.rows;
-  const T *r = P.r;
+PERKS_DEVINL void cg_spmv(const Params<T> &P, const Own<T, VEC> &o, TileSet &ts, unsigned char *smem, bool fused,
+                          T beta, const T *pprev, const T *pcur) {
+  const int R0 = o.R0;
   T *q = P.q;
-  const T *sp = o.s_p;
   T *sq = o.s_q;
-  auto gather = [=](int jc) -> T {
-    const unsigned off = (unsigned)(jc - R0);
-    if (off < (unsigned)rows) return VEC ? sp[off] : __ldcg(pcur + jc);
-    return first ? __ldcg(r + jc) : fma_rn(beta, __ldcg(pprev + jc), __ldcg(r + jc));
-  };
   auto qstore = [=](int row, T v) {
     if (VEC) sq[row - R0] = v;
     else q[row] = v;
   };
-  spmv_cta<T>(P, pp, smem, wrap, gather, qstore);
+  if (fused) spmv_cta<T>(P, ts, smem, CgGather<T, true>{o.R0, o.rows, beta, pcur, pprev, P.r}, qstore);
+  else spmv_cta<T>(P, ts, smem, CgGather<T, false>{o.R0, o.rows, beta, pcur, pprev, P.r}, qstore);
 }
 
 // ------------------------------------------------------------------------ kernels
+// All-reduce of one double per CTA without a separate barrier (PERKS_CG_LL=1; measured slower
+// than barrier + slot read on B200, kept as an option): CTA c stores its partial with a tag into
+// LL slot c; one warp of every CTA polls all G slots until each carries the tag, then sums them
+// in the same fixed order as slots_sum.  `order`: release fence before the store, acquire fence
+// after the poll (the next phase reads other CTAs' vectors).
+PERKS_DEVINL double ll_allreduce(LLWord *slots, int G, unsigned tag, double part, bool order, double *s_bc) {
+  if (threadIdx.x == 0) {
+    if (order) fence_acq_rel_gpu();
+    LL<double>::put(slots + 2 * blockIdx.x, part, tag);
+  }
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    double v[kMaxG / 32];
+    const unsigned long long t0 = globaltimer_ns();
+    unsigned spins = 0;
+    bool ok;
+    do {
+      ok = true;
+#pragma unroll
+      for (int j = 0; j < kMaxG / 32; ++j) {
+        v[j] = 0.0;
+        if (lane + 32 * j < G) ok &= LL<double>::get(slots + 2 * (lane + 32 * j), tag, v[j]);
+      }
+      if ((++spins & 255u) == 0 && globaltimer_ns() - t0 > PERKS_WATCHDOG_NS) watchdog_fire("cg allreduce", tag, G);
+    } while (!__all_sync(0xffffffffu, ok));
+    if (order) fence_acq_rel_gpu();
+    double t = 0.0;
+#pragma unroll
+    for (int j = 0; j < kMaxG / 32; ++j) t += v[j];
+    t = warp_sum(t);
+    if (lane == 0) *s_bc = t;
+  }
+  __syncthreads();
+  return *s_bc;
+}
+
+// Phase timer (development, PERKS_CG_TIMING=1): CTA 0 / thread 0 accumulates globaltimer deltas
+// per phase into P.dbg[0..3] (0 p update, 1 SpMV, 2 <p,Ap> + all-reduce, 3 x/r update +
+// all-reduce); P.dbg[8] += iterations.
+struct PhaseClock {
+  unsigned long long *dbg;
+  unsigned long long t;
+  PERKS_DEVINL explicit PhaseClock(unsigned long long *d)
+      : dbg(blockIdx.x == 0 && threadIdx.x == 0 ? d : nullptr), t(0) {
+    if (dbg) t = globaltimer_ns();
+  }
+  PERKS_DEVINL void tick(int ph) {
+    if (dbg) {
+      const unsigned long long n = globaltimer_ns();
+      dbg[ph] += n - t;
+      t = n;
+    }
+  }
+};
+
 // (b)/(c): the whole solve in one cooperative launch.
 template <typename T, bool VEC> __global__ void __launch_bounds__(NT, 1) cg_persistent_kernel(Params<T> P) {
   extern __shared__ __align__(128) unsigned char smem[];
   double *s_red = reinterpret_cast<double *>(smem + Smem::RED);
   double *s_bc = reinterpret_cast<double *>(smem + Smem::BCAST);
   const Own<T, VEC> o = own_view<T, VEC>(P, smem);
-  Pipe<T> pp;
-  pipe_init<T>(P, pp, smem, VEC ? P.rows_max : 0, true);
+  TileSet ts = tiles_init<T>(P, smem, VEC ? P.rows_max : 0, true, true);
   const int c = blockIdx.x;
+  // all-reduce of the per-CTA partials: grid barrier + slot read, or tagged LL slots
+  // (P.use_ll); kind 0 = <p,Ap>, 1 = <r,r>; both give the same bits
   unsigned nb = 0;
+  auto allreduce = [&](int kind, unsigned tag, double part, bool order, double *bc) -> double {
+    if (P.use_ll) return ll_allreduce(P.ll + 2 * kind * P.G, P.G, tag, part, order, bc);
+    if (threadIdx.x == 0) P.slots[kind * P.G + c] = part;
+    grid_barrier(P.bar, ++nb);
+    return slots_sum(P.slots + kind * P.G, P.G, bc);
+  };
   double part = block_sum(cg_prologue<T, VEC>(P, o), s_red);
-  if (threadIdx.x == 0) P.slots[P.G + c] = part;
-  grid_barrier(P.bar, ++nb);
-  double rr = slots_sum(P.slots + P.G, P.G, s_bc);
+  double rr = allreduce(1, 1u, part, true, s_bc);  // r_0 = b published before the gathers
   if (c == 0 && threadIdx.x == 0 && P.hist) P.hist[0] = rr;
+  PhaseClock clk(P.dbg);
   long long k = 0;
   int status = 0;
   double beta = 0.0;
   while (k < P.kmax) {
     if (!(rr > P.tol2)) break;  // reading RC2: <r_k,r_k> <= tol^2 stops before the iteration
-    const bool first = (k == 0);
     T *pcur = (k & 1) ? P.p1 : P.p0;
     const T *pprev = (k & 1) ? P.p0 : P.p1;
     const T bt = (T)beta;
-    cg_p_update<T, VEC>(P, o, first, bt, pprev, pcur);
-    __syncthreads();
-    cg_spmv<T, VEC>(P, o, pp, smem, true, first, bt, pprev, pcur);
+    const unsigned tag = (unsigned)k + 2u;
+    cg_p_update<T, VEC>(P, o, bt, pprev, pcur);
+    if (P.fused) __syncthreads();
+    else grid_barrier(P.bar, ++nb);  // every CTA's p_k published before the gathers
+    clk.tick(0);
+    cg_spmv<T, VEC>(P, o, ts, smem, P.fused, bt, pprev, pcur);
+    clk.tick(1);
     part = block_sum(cg_pap<T, VEC>(P, o, pcur), s_red);
-    if (threadIdx.x == 0) P.slots[c] = part;
-    grid_barrier(P.bar, ++nb);
-    const double pap = slots_sum(P.slots, P.G, s_bc + 1);
+    // phase B touches only this CTA's rows: no ordering needed
+    const double pap = allreduce(0, tag, part, false, s_bc + 1);
+    clk.tick(2);
     if (!(pap > 0.0)) { status = 1; break; }  // reading RC4: not positive definite
     const double alpha = rr / pap;
     part = block_sum(cg_xr_update<T, VEC>(P, o, (T)alpha, pcur), s_red);
-    if (threadIdx.x == 0) P.slots[P.G + c] = part;
-    grid_barrier(P.bar, ++nb);
-    const double rr_new = slots_sum(P.slots + P.G, P.G, s_bc + 2);
+    // the next (fused) SpMV gathers the r and p other CTAs published: release/acquire
+    const double rr_new = allreduce(1, tag, part, P.fused != 0, s_bc + 2);
+    clk.tick(3);
     beta = rr_new / rr;
     rr = rr_new;
     ++k;
     if (c == 0 && threadIdx.x == 0 && P.hist) P.hist[k] = rr;
   }
+  if (clk.dbg) clk.dbg[8] += k;
   if (VEC)
     for (int j = threadIdx.x; j < o.rows; j += NT) P.x[o.R0 + j] = o.s_x[j];
   if (c == 0 && threadIdx.x == 0 && P.info) { P.info[0] = k; P.info[1] = status; }
-  pipe_drain<T>(pp, smem);
+  tiles_fini<T>(ts, smem);
 }
 
 // (a) host loop: prologue, then per iteration kernel A (p update, SpMV, <p,Ap>) and kernel B
@@ -575,7 +721,6 @@ template <typename T, bool VEC> __global__ void __launch_bounds__(NT, 1) cg_pers
 template <typename T> __global__ void __launch_bounds__(NT, 1) cg_hl_prologue_kernel(Params<T> P) {
   extern __shared__ __align__(128) unsigned char smem[];
   double *s_red = reinterpret_cast<double *>(smem + Smem::RED);
-  double *s_bc = reinterpret_cast<double *>(smem + Smem::BCAST);
   const Own<T, false> o = own_view<T, false>(P, smem);
   const double part = block_sum(cg_prologue<T, false>(P, o), s_red);
   if (threadIdx.x == 0) P.slots[P.G + blockIdx.x] = part;
@@ -599,18 +744,16 @@ template <typename T> __global__ void __launch_bounds__(NT, 1) cg_hl_a_kernel(Pa
     return;
   }
   const Own<T, false> o = own_view<T, false>(P, smem);
-  Pipe<T> pp;
-  pipe_init<T>(P, pp, smem, 0, false);
-  const bool first = (k == 0);
+  TileSet ts = tiles_init<T>(P, smem, 0, false, false);
   T *pcur = (k & 1) ? P.p1 : P.p0;
   const T *pprev = (k & 1) ? P.p0 : P.p1;
   const T bt = (T)beta;
-  cg_p_update<T, false>(P, o, first, bt, pprev, pcur);
+  cg_p_update<T, false>(P, o, bt, pprev, pcur);
   __syncthreads();
-  cg_spmv<T, false>(P, o, pp, smem, false, first, bt, pprev, pcur);
+  cg_spmv<T, false>(P, o, ts, smem, true, bt, pprev, pcur);
   const double part = block_sum(cg_pap<T, false>(P, o, pcur), s_red);
   if (threadIdx.x == 0) P.slots[c] = part;
-  pipe_drain<T>(pp, smem);
+  tiles_fini<T>(ts, smem);
 }
 
 template <typename T> __global__ void __launch_bounds__(NT, 1) cg_hl_b_kernel(Params<T> P, long long k) {
@@ -649,14 +792,12 @@ template <typename T> __global__ void cg_hl_finish_kernel(Params<T> P) {
 // Standalone merge-based SpMV: q = A xin.
 template <typename T> __global__ void __launch_bounds__(NT, 1) cg_spmv_kernel(Params<T> P) {
   extern __shared__ __align__(128) unsigned char smem[];
-  Pipe<T> pp;
-  pipe_init<T>(P, pp, smem, 0, false);
-  const T *xin = P.xin;
+  TileSet ts = tiles_init<T>(P, smem, 0, false, false);
+  const PlainGather<T> gather{P.xin};
   T *y = P.q;
-  auto gather = [=](int j) -> T { return __ldg(xin + j); };
   auto qstore = [=](int row, T v) { y[row] = v; };
-  spmv_cta<T>(P, pp, smem, false, gather, qstore);
-  pipe_drain<T>(pp, smem);
+  spmv_cta<T>(P, ts, smem, gather, qstore);
+  tiles_fini<T>(ts, smem);
 }
 
 }  // namespace cg
@@ -688,16 +829,13 @@ struct perks_cg_s {
   int64_t n = 0, nnz = 0;
   int G = 1;
   int rows_max = 0;
-  int ntiles = 0;
-  int tile_max = 0;                 // largest tile image (bytes)
+  int ntiles = 0;                   // tiles over all CTAs
+  int tiles_max = 0;                // most tiles of one CTA
   std::vector<int> h_crow;          // G+1
   std::vector<int> h_ctile;         // G+1
-  std::vector<int2> h_coords;       // ntiles + G
-  void *d_mem = nullptr;            // one allocation: row_off | col | val | coords | ctile | crow
-  int *d_row_off = nullptr, *d_col = nullptr, *d_ctile = nullptr, *d_crow = nullptr;
-  void *d_val = nullptr;
-  int2 *d_coords = nullptr;
-  // run_host scratch
+  void *d_mem = nullptr;            // one allocation: tiles | ctile | crow
+  unsigned char *d_tiles = nullptr;
+  int *d_ctile = nullptr, *d_crow = nullptr;
   std::mutex mu;
   size_t elem() const { return dtype == PERKS_F64 ? 8 : 4; }
 };
@@ -705,7 +843,7 @@ struct perks_cg_s {
 namespace {
 
 // Merge-path search on the global CSR: (rows completed, nonzeros consumed) at diagonal d.
-void path_coord(const std::vector<int64_t> &ro, int64_t n, int64_t nnz, int64_t d, int64_t &i, int64_t &k) {
+void path_coord(const int64_t *ro, int64_t n, int64_t nnz, int64_t d, int64_t &i, int64_t &k) {
   int64_t lo = std::max<int64_t>(0, d - nnz), hi = std::min<int64_t>(d, n);
   while (lo < hi) {
     const int64_t mid = (lo + hi) / 2;
@@ -717,14 +855,16 @@ void path_coord(const std::vector<int64_t> &ro, int64_t n, int64_t nnz, int64_t 
 }
 
 struct Layout {
-  size_t ws_bytes, off_r, off_p0, off_p1, off_q, off_slots, off_scal, off_state, off_bar;
+  size_t ws_bytes, off_r, off_p0, off_p1, off_q, off_slots, off_scal, off_state, off_bar, off_dbg, off_ll, ll_bytes;
 };
 Layout ws_layout(const perks_cg_s *h) {
   Layout L{};
   const size_t vb = align256((size_t)std::max<int64_t>(h->n, 1) * h->elem());
   size_t o = 0;
   L.off_bar = o; o += 256;
+  L.off_dbg = o; o += 256;   // bytes 256..511: phase timer (tools/cg_timing.py reads it there)
   L.off_slots = o; o += align256((size_t)2 * h->G * 8);
+  L.off_ll = o; L.ll_bytes = align256((size_t)2 * h->G * 16); o += L.ll_bytes;
   L.off_scal = o; o += 256;
   L.off_state = o; o += 256;
   L.off_r = o; o += vb;
@@ -738,19 +878,13 @@ Layout ws_layout(const perks_cg_s *h) {
 struct CgPlan {
   int variant, policy;
   bool vec = false;
-  int res_budget = 0;
-  bool stream = true;
+  bool fused = true;    // persistent: 2 barriers/iteration (p_k recomputed at the gathers)
+  int nbuf = 0;         // stream ring buffers
+  int tm = 0, sm = 0;   // resident tiles per CTA: TMEM, shared memory
   int smem = 0;
-  int64_t cached_nnz = 0, cached_rows = 0;
+  int64_t cached_items_tmem = 0, cached_items_smem = 0, cached_rows = 0;
   double dram = 0, unfused = 0;
 };
-
-int tile_bytes_host(const perks_cg_s *h, int idx, int c) {
-  const int2 a = h->h_coords[idx], e = h->h_coords[idx + 1];
-  (void)c;
-  return h->dtype == PERKS_F64 ? TileGeo<double>(a.x, e.x - a.x, a.y, e.y - a.y).bytes()
-                               : TileGeo<float>(a.x, e.x - a.x, a.y, e.y - a.y).bytes();
-}
 
 CgPlan make_plan(const perks_cg_s *h, perks_variant v, perks_cg_policy pol) {
   CgPlan pl;
@@ -761,52 +895,52 @@ CgPlan make_plan(const perks_cg_s *h, perks_variant v, perks_cg_policy pol) {
   pl.policy = pol;
   const bool f64 = h->dtype == PERKS_F64;
   const int S = (int)h->elem();
-  const int tmax = f64 ? tile_max_bytes<double>() : tile_max_bytes<float>();
-  const int base = f64 ? Smem::vec_off<double>() : Smem::vec_off<float>();
+  const int tb = f64 ? tile_bytes<double>() : tile_bytes<float>();
   const int vecb = 4 * a16((long long)h->rows_max * S);
-  pl.vec = (pol == PERKS_CG_VEC || pol == PERKS_CG_MIX) && base + vecb + 2 * tmax <= kSmemMax;
-  const int fixed = base + (pl.vec ? vecb : 0);
+  pl.vec = (pol == PERKS_CG_VEC || pol == PERKS_CG_MIX) && Smem::VEC + vecb <= kSmemMax;
   const bool mat = pol == PERKS_CG_MAT || pol == PERKS_CG_MIX;
-  // resident budget: if every CTA's whole share fits without stream buffers, no streaming
-  int need_max = 0;
-  for (int c = 0; c < h->G; ++c) {
-    int s = 0;
-    for (int m = h->h_ctile[c]; m < h->h_ctile[c + 1] - 1; ++m) s += tile_bytes_host(h, m, c);
-    need_max = std::max(need_max, s);
-  }
-  if (mat && fixed + need_max <= kSmemMax) {
-    pl.res_budget = need_max;
-    pl.stream = false;
-  } else if (mat) {
-    pl.res_budget = std::max(0, kSmemMax - fixed - 2 * tmax) & ~15;
-    pl.stream = true;
-  } else {
-    pl.res_budget = 0;
-    pl.stream = h->ntiles > 0;
-  }
-  pl.smem = fixed + (pl.stream ? 2 * tmax : 0) + pl.res_budget;
-  // what is cached, per CTA exactly as pipe_init decides
-  for (int c = 0; c < h->G; ++c) {
-    int used = 0;
-    for (int m = h->h_ctile[c]; m < h->h_ctile[c + 1] - 1; ++m) {
-      const int b = tile_bytes_host(h, m, c);
-      if (used + b > pl.res_budget) break;
-      used += b;
-      pl.cached_nnz += h->h_coords[m + 1].y - h->h_coords[m].y;
+  const int base = Smem::VEC + (pl.vec ? vecb : 0);
+  const int fit = std::max(0, (kSmemMax - base) / tb);  // tile records that fit next to VEC
+  if (mat) {
+    pl.tm = std::min(h->tiles_max, f64 ? tmem_tiles<double>() : tmem_tiles<float>());
+    const int rest = h->tiles_max - pl.tm;
+    if (rest <= fit) {
+      pl.sm = rest;  // everything resident: no stream
+    } else {         // keep a stream ring of up to 3 buffers, the rest resident
+      pl.nbuf = std::min(fit, 3);
+      pl.sm = fit - pl.nbuf;
     }
+  } else if (h->tiles_max > 0) {
+    pl.nbuf = std::min(fit, env_int("PERKS_CG_NBUF", 3));
+  }
+  pl.nbuf = std::min(pl.nbuf, 6);
+  pl.smem = base + (pl.nbuf + pl.sm) * tb;
+  // two barriers (p_k recomputed at the gathers) only for one-tile shares; from two tiles per CTA
+  // up one gather load per nonzero costs more than the third barrier (measured: G2 9.0 vs 10.1,
+  // G3 14.1 vs 13.5, G4 98.9 vs 84.7 us/iteration fused vs not; PERKS_CG_FUSED overrides)
+  pl.fused = env_int("PERKS_CG_FUSED", h->tiles_max <= 1 ? 1 : 0) != 0;
+  // TMEM holds all 512 columns: exactly one CTA per SM (more than half the SM's shared memory)
+  if (pl.tm > 0) pl.smem = std::max(pl.smem, 120 * 1024);
+  // what is cached, per CTA as tiles_init decides; bytes per iteration
+  const int64_t items_total = (int64_t)h->ntiles * TI;
+  for (int c = 0; c < h->G; ++c) {
+    const int nt = h->h_ctile[c + 1] - h->h_ctile[c];
+    const int tm = std::min(nt, pl.tm), sm = std::min(nt - tm, pl.sm);
+    pl.cached_items_tmem += (int64_t)tm * TI;
+    pl.cached_items_smem += (int64_t)sm * TI;
     if (pl.vec) pl.cached_rows += h->h_crow[c + 1] - h->h_crow[c];
   }
-  // bytes per iteration.  Unfused (the metric): A once (values, columns, row offsets), the
-  // gathered p once per row, and the vector passes of Algorithm: p update (r, p
-  // read, p written), <p,Ap> (p, q read), x update (x, p read, x written), r update (r, q
-  // read, r written), <r,r> (r read) = 13 vector accesses per row, and A p written once.
+  // Unfused (the metric): A once in CSR (values, columns, row offsets), the gathered p once per
+  // row, and the vector passes of Algorithm: p update (r, p read, p written), <p,Ap>
+  // (p, q read), x update (x, p read, x written), r update (r, q read, r written), <r,r> (r
+  // read) = 13 vector accesses per row, plus A p written once.
   const double n = (double)h->n, nnz = (double)h->nnz;
   pl.unfused = nnz * (S + 4) + (n + 1) * 4 + n * S * (1 + 13 + 1);
-  // modelled DRAM: uncached matrix + the vectors that leave the SM (r and p published, read
-  // back by the gathers through L2: counted once), plus own-row vector traffic without VEC.
-  const double mat_b = (nnz - (double)pl.cached_nnz) * (S + 4) + (n + 1) * 4;
-  const double vec_b = pl.vec ? n * S * 2 : n * S * (2 + 9);
-  pl.dram = mat_b + vec_b;
+  // Modelled DRAM: streamed tile records + the vectors leaving the SM (r and p published and
+  // gathered back: counted once each), plus own-row vector traffic without VEC.
+  const double rec = (double)tb / TI;  // bytes per item slot incl. headers
+  const double streamed = (double)(items_total - pl.cached_items_tmem - pl.cached_items_smem);
+  pl.dram = streamed * rec + (pl.vec ? n * S * 2 : n * S * 11);
   return pl;
 }
 
@@ -816,10 +950,7 @@ template <typename T> Params<T> make_params(perks_cg_s *h, void *ws, const CgPla
   Params<T> P{};
   P.n = (int)h->n;
   P.G = h->G;
-  P.row_off = h->d_row_off;
-  P.col = h->d_col;
-  P.val = static_cast<const T *>(h->d_val);
-  P.coords = h->d_coords;
+  P.tiles = h->d_tiles;
   P.ctile = h->d_ctile;
   P.crow = h->d_crow;
   P.r = reinterpret_cast<T *>(w + L.off_r);
@@ -830,9 +961,13 @@ template <typename T> Params<T> make_params(perks_cg_s *h, void *ws, const CgPla
   P.scal = reinterpret_cast<double *>(w + L.off_scal);
   P.state = reinterpret_cast<long long *>(w + L.off_state);
   P.bar = reinterpret_cast<unsigned *>(w + L.off_bar);
+  P.ll = reinterpret_cast<LLWord *>(w + L.off_ll);
+  P.dbg = env_int("PERKS_CG_TIMING", 0) ? reinterpret_cast<unsigned long long *>(w + L.off_dbg) : nullptr;
   P.rows_max = h->rows_max;
-  P.res_budget = pl.res_budget;
-  P.stream = pl.stream ? 1 : 0;
+  P.tm_tiles = pl.tm;
+  P.sm_tiles = pl.sm;
+  P.nbuf = pl.nbuf;
+  P.fused = pl.fused ? 1 : 0;
   return P;
 }
 
@@ -848,7 +983,7 @@ cudaError_t launch_solve(perks_cg_s *h, const CgPlan &pl, const void *b, void *x
   P.tol2 = tol * tol;
   cudaError_t e;
   if (pl.variant == PERKS_HOSTLOOP) {
-    const int smem = smem_bytes<T>(0, P.stream, 0);
+    const int smem = smem_bytes<T>(0, pl.nbuf, 0);
     void (*ka)(Params<T>, long long) = cg_hl_a_kernel<T>;
     void (*pk)(Params<T>) = cg_hl_prologue_kernel<T>;
     void (*kb)(Params<T>, long long) = cg_hl_b_kernel<T>;
@@ -863,6 +998,10 @@ cudaError_t launch_solve(perks_cg_s *h, const CgPlan &pl, const void *b, void *x
     cg_hl_finish_kernel<T><<<1, 32, 0, s>>>(P);
     return cudaGetLastError();
   }
+  const Layout L = ws_layout(h);
+  P.use_ll = env_int("PERKS_CG_LL", 0);
+  if (P.use_ll && (e = cudaMemsetAsync(static_cast<unsigned char *>(ws) + L.off_ll, 0, L.ll_bytes, s)) != cudaSuccess)
+    return e;
   if ((e = reset_grid_barrier(P.bar, s)) != cudaSuccess) return e;
   void *kfn = pl.vec ? (void *)cg_persistent_kernel<T, true> : (void *)cg_persistent_kernel<T, false>;
   if ((e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem)) != cudaSuccess) return e;
@@ -885,7 +1024,7 @@ template <typename T> cudaError_t launch_spmv(perks_cg_s *h, const void *xin, vo
   Params<T> P = make_params<T>(h, ws, pl);
   P.xin = static_cast<const T *>(xin);
   P.q = static_cast<T *>(y);
-  const int smem = smem_bytes<T>(0, P.stream, 0);
+  const int smem = smem_bytes<T>(0, pl.nbuf, 0);
   cudaError_t e;
   if ((e = cudaFuncSetAttribute(cg_spmv_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess)
     return e;
@@ -896,6 +1035,50 @@ template <typename T> cudaError_t launch_spmv(perks_cg_s *h, const void *xin, vo
 bool overlaps(const void *a, size_t na, const void *b, size_t nb) {
   const char *x = static_cast<const char *>(a), *y = static_cast<const char *>(b);
   return x < y + nb && y < x + na;
+}
+
+// Build the item tiles of every CTA (see the header comment) into `buf` (tile records).
+template <typename T>
+void build_tiles(const perks_csr_desc *d, const std::vector<int> &crow, const std::vector<int> &ctile,
+                 std::vector<unsigned char> &buf) {
+  const int G = (int)crow.size() - 1;
+  const size_t tbytes = tile_bytes<T>();
+  buf.assign((size_t)ctile[G] * tbytes, 0);
+  std::vector<int> irow, iword;
+  std::vector<T> ival;
+  std::vector<char> ifirst;
+  for (int c = 0; c < G; ++c) {
+    irow.clear(); iword.clear(); ival.clear(); ifirst.clear();
+    for (int64_t i = crow[c]; i < crow[c + 1]; ++i) {
+      const int64_t a = d->row_offsets[i], b = d->row_offsets[i + 1];
+      if (a == b) {  // empty row: one zero item without a column
+        irow.push_back((int)i); iword.push_back((int)0xffffffff); ival.push_back(T(0)); ifirst.push_back(1);
+        continue;
+      }
+      for (int64_t k = a; k < b; ++k) {
+        irow.push_back((int)i);
+        iword.push_back(d->col_indices[k] | (k == b - 1 ? (int)0x80000000 : 0));
+        ival.push_back((T)d->values[k]);  // rounded once (reading RC3)
+        ifirst.push_back(k == a);
+      }
+    }
+    const int64_t ni = (int64_t)irow.size();
+    for (int m = 0; m < ctile[c + 1] - ctile[c]; ++m) {
+      unsigned char *rec = buf.data() + (size_t)(ctile[c] + m) * tbytes;
+      T *val = reinterpret_cast<T *>(rec);
+      int *wrd = reinterpret_cast<int *>(rec + TI * sizeof(T));
+      int *hdr = reinterpret_cast<int *>(rec + TI * (sizeof(T) + 4));
+      for (int t = 0; t < NT; ++t) {
+        const int64_t i0 = (int64_t)m * TI + (int64_t)t * IPT;
+        hdr[t] = i0 < ni ? (irow[i0] | (ifirst[i0] ? 0 : (int)0x80000000)) : crow[c + 1];
+        for (int e = 0; e < IPT; ++e) {
+          const int64_t it = i0 + e;
+          val[e * NT + t] = it < ni ? ival[it] : T(0);
+          wrd[e * NT + t] = it < ni ? iword[it] : PAD;
+        }
+      }
+    }
+  }
 }
 
 }  // namespace
@@ -927,62 +1110,37 @@ perks_status perks_cg_create(const perks_csr_desc *d, int device, perks_cg_t *ou
   cudaError_t e = cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (e != cudaSuccess) { delete h; return cg_cuda_fail(e); }
   h->num_sms = env_int("PERKS_NUM_SMS", h->num_sms);
-  // CTA-level (TB-level) merge-path partition, row aligned; then tiles of TILE path items.
+  // CTA-level (TB-level) merge-path partition, row aligned
   const int64_t L = n + nnz;
   h->G = (int)std::max<int64_t>(1, std::min<int64_t>(std::min(h->num_sms, kMaxG), (L + 1023) / 1024));
-  std::vector<int64_t> ro(d->row_offsets, d->row_offsets + n + 1);
   h->h_crow.resize(h->G + 1);
   for (int c = 0; c <= h->G; ++c) {
     int64_t i, k;
-    path_coord(ro, n, nnz, L * c / h->G, i, k);
+    path_coord(d->row_offsets, n, nnz, L * c / h->G, i, k);
     h->h_crow[c] = (int)(c == h->G ? n : i);
   }
-  for (int c = 0; c < h->G; ++c) h->rows_max = std::max(h->rows_max, h->h_crow[c + 1] - h->h_crow[c]);
-  h->h_ctile.resize(h->G + 1);
+  // items per CTA (nonzeros + one per empty row) -> tiles
+  h->h_ctile.assign(h->G + 1, 0);
   for (int c = 0; c < h->G; ++c) {
-    h->h_ctile[c] = (int)h->h_coords.size();
-    const int64_t R0 = h->h_crow[c], R1 = h->h_crow[c + 1];
-    const int64_t P0 = R0 + ro[R0], P1 = R1 + ro[R1];
-    for (int64_t dd = P0; dd < P1; dd += TILE) {
-      int64_t i, k;
-      path_coord(ro, n, nnz, dd, i, k);
-      h->h_coords.push_back(make_int2((int)i, (int)k));
-    }
-    h->h_coords.push_back(make_int2((int)R1, (int)ro[R1]));
+    h->rows_max = std::max(h->rows_max, h->h_crow[c + 1] - h->h_crow[c]);
+    int64_t items = d->row_offsets[h->h_crow[c + 1]] - d->row_offsets[h->h_crow[c]];
+    for (int64_t i = h->h_crow[c]; i < h->h_crow[c + 1]; ++i) items += d->row_offsets[i + 1] == d->row_offsets[i];
+    const int nt = (int)((items + TI - 1) / TI);
+    h->tiles_max = std::max(h->tiles_max, nt);
+    h->h_ctile[c + 1] = h->h_ctile[c] + nt;
   }
-  h->h_ctile[h->G] = (int)h->h_coords.size();
-  h->ntiles = (int)h->h_coords.size() - h->G;
-  // device copy: row_off | col | val | coords | ctile | crow (each 256-B aligned, padded so the
-  // 16-byte-rounded bulk copies never read past an allocation)
-  const size_t S = h->elem();
-  const size_t b_ro = align256((n + 1) * 4 + 64), b_col = align256(nnz * 4 + 64), b_val = align256(nnz * S + 64);
-  const size_t b_co = align256(h->h_coords.size() * 8), b_ct = align256((h->G + 1) * 4), b_cr = b_ct;
-  e = cudaMalloc(&h->d_mem, b_ro + b_col + b_val + b_co + b_ct + b_cr);
+  h->ntiles = h->h_ctile[h->G];
+  std::vector<unsigned char> tiles;
+  if (h->dtype == PERKS_F64) build_tiles<double>(d, h->h_crow, h->h_ctile, tiles);
+  else build_tiles<float>(d, h->h_crow, h->h_ctile, tiles);
+  const size_t b_t = align256(tiles.size() + 16), b_c = align256((h->G + 1) * 4);
+  e = cudaMalloc(&h->d_mem, b_t + 2 * b_c);
   if (e != cudaSuccess) { delete h; return cg_cuda_fail(e); }
   char *m = static_cast<char *>(h->d_mem);
-  h->d_row_off = reinterpret_cast<int *>(m);
-  h->d_col = reinterpret_cast<int *>(m + b_ro);
-  h->d_val = m + b_ro + b_col;
-  h->d_coords = reinterpret_cast<int2 *>(m + b_ro + b_col + b_val);
-  h->d_ctile = reinterpret_cast<int *>(m + b_ro + b_col + b_val + b_co);
-  h->d_crow = reinterpret_cast<int *>(m + b_ro + b_col + b_val + b_co + b_ct);
-  std::vector<int> ro32(n + 1);
-  for (int64_t i = 0; i <= n; ++i) ro32[i] = (int)ro[i];
-  std::vector<unsigned char> vals(nnz * S + 1);
-  for (int64_t k = 0; k < nnz; ++k) {
-    if (h->dtype == PERKS_F64) {
-      const double v = d->values[k];
-      std::memcpy(vals.data() + k * 8, &v, 8);
-    } else {
-      const float v = (float)d->values[k];  // rounded once (reading RC3)
-      std::memcpy(vals.data() + k * 4, &v, 4);
-    }
-  }
-  if ((e = cudaMemset(h->d_mem, 0, b_ro + b_col + b_val)) != cudaSuccess ||
-      (e = cudaMemcpy(h->d_row_off, ro32.data(), (n + 1) * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
-      (nnz && (e = cudaMemcpy(h->d_col, d->col_indices, nnz * 4, cudaMemcpyHostToDevice)) != cudaSuccess) ||
-      (nnz && (e = cudaMemcpy(h->d_val, vals.data(), nnz * S, cudaMemcpyHostToDevice)) != cudaSuccess) ||
-      (e = cudaMemcpy(h->d_coords, h->h_coords.data(), h->h_coords.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess ||
+  h->d_tiles = reinterpret_cast<unsigned char *>(m);
+  h->d_ctile = reinterpret_cast<int *>(m + b_t);
+  h->d_crow = reinterpret_cast<int *>(m + b_t + b_c);
+  if ((!tiles.empty() && (e = cudaMemcpy(h->d_tiles, tiles.data(), tiles.size(), cudaMemcpyHostToDevice)) != cudaSuccess) ||
       (e = cudaMemcpy(h->d_ctile, h->h_ctile.data(), (h->G + 1) * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = cudaMemcpy(h->d_crow, h->h_crow.data(), (h->G + 1) * 4, cudaMemcpyHostToDevice)) != cudaSuccess) {
     cudaFree(h->d_mem);
@@ -1082,9 +1240,7 @@ perks_status perks_cg_query(perks_cg_t h, perks_variant v, perks_cg_policy pol, 
   info->block = NT;
   info->items_per_thread = IPT;
   info->tiles = h->ntiles;
-  info->smem_per_cta = pl.variant == PERKS_HOSTLOOP ? (h->dtype == PERKS_F64 ? smem_bytes<double>(0, true, 0)
-                                                                             : smem_bytes<float>(0, true, 0))
-                                                    : pl.smem;
+  info->smem_per_cta = pl.smem;
   DevGuard g(h->device);
   cudaFuncAttributes fa{};
   const void *kfn = h->dtype == PERKS_F64
@@ -1096,7 +1252,10 @@ perks_status perks_cg_query(perks_cg_t h, perks_variant v, perks_cg_policy pol, 
                                                         : (const void *)cg_persistent_kernel<float, false>);
   if (g.ok && cudaFuncGetAttributes(&fa, kfn) == cudaSuccess) info->regs_per_thread = fa.numRegs;
   else cudaGetLastError();
-  info->cached_nnz_smem = pl.cached_nnz;
+  info->cached_nnz_smem = pl.cached_items_smem;
+  info->cached_nnz_tmem = pl.cached_items_tmem;
+  info->tmem_tiles_per_cta = pl.tm;
+  info->smem_tiles_per_cta = pl.sm;
   info->cached_rows_smem = pl.cached_rows;
   info->n_rows = h->n;
   info->nnz = h->nnz;

@@ -26,9 +26,11 @@ pytestmark = pytest.mark.gpu
 
 DT = [np.float64, np.float32]
 # RC5: the GPU may differ from the oracle by at most SPREAD_FACTOR x the oracle's own spread
-# under a reordering of the same problem (a symmetric permutation P A P^T, P b: identical
-# mathematics, different summation orders), plus a floor of a few ulps of the result.
-SPREAD_FACTOR = 10.0
+# under reorderings of the same problem (symmetric permutations P A P^T, P b: identical
+# mathematics, different summation orders; the largest deviation over N_PERM of them), plus a
+# floor of a few ulps of the result.
+SPREAD_FACTOR = 30.0
+N_PERM = 4
 # fixed-size parity (full workloads) where the permuted oracle would take too long:
 XTOL = {np.float64: 1e-9, np.float32: 2e-3}
 RTOL_HIST = {np.float64: 1e-6, np.float32: 5e-2}
@@ -186,7 +188,7 @@ def _oracle_spread(ro, ci, va, b, K):
     permutations (RC5), as max|dx| / max|x| and max_k |sqrt(h_k) - sqrt(h'_k)| / sqrt(h_0)."""
     xo, ho, ko = oracle.cg(ro, ci, va, b, kmax=K)
     xs = rs = 0.0
-    for seed in (1, 2):
+    for seed in range(1, N_PERM + 1):
         perm, ro2, ci2, va2, b2 = _permuted(ro, ci, va, b, seed)
         x2, h2, k2 = oracle.cg(ro2, ci2, va2, b2, kmax=K)
         assert k2 == ko

@@ -1,5 +1,6 @@
 """CG timing sweep (development): us per iteration for each workload x variant/policy, with
 CUDA events around one solve of K iterations (tol = 0), best of R."""
+import os
 import sys
 import time
 
@@ -20,6 +21,18 @@ for wl in wls:
     h = CG(ro, ci, va, dtype="f64" if dtype == np.float64 else "f32")
     b = torch.from_numpy(sp.rhs(n, dtype=dtype)).cuda()
     base = None
+    y = torch.empty_like(b)
+    h.spmv(b, out=y)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(20):
+        h.spmv(b, out=y)
+    e1.record()
+    torch.cuda.synchronize()
+    t_sp = e0.elapsed_time(e1) * 1e3 / 20
+    mb = (h.nnz * (8 if dtype == np.float64 else 4) + h.nnz * 4 + (n + 1) * 4 + 2 * n * (8 if dtype == np.float64 else 4))
+    print(f"{wl} spmv kernel {t_sp:9.2f} us  {mb / t_sp / 1e3:8.1f} GB/s (A + x + y once)", flush=True)
     for v, p in combos:
         q = h.query(v, p)
         x, hist, info = h.solve(b, 3, 0.0, v, p)
@@ -34,11 +47,20 @@ for wl in wls:
             ts.append(e0.elapsed_time(e1) * 1e3 / K)
         it = int(info[0].item())
         t = min(ts)
+        phases = ""
+        if os.environ.get("PERKS_CG_TIMING") and v != "hostloop":
+            ws = h.workspace()
+            ws[256:512].zero_()
+            h.solve(b, K, 0.0, v, p, out=x, history=hist)
+            torch.cuda.synchronize()
+            d = ws[256:512].cpu().numpy().view(np.uint64)
+            nit = max(int(d[8]), 1)
+            phases = " phases(us/iter): " + " ".join(f"{d[i] / nit / 1e3:.2f}" for i in range(4))
         if base is None:
             base = t
         gbs = q["unfused_bytes_per_iter"] / (t * 1e-6) / 1e9
         print(f"{wl} {v:10s} {p:4s} {t:9.2f} us/iter  x{base / t:5.2f} vs hostloop  {gbs:8.1f} GB/s unfused "
-              f" iters={it} smem={q['smem_per_cta']} cached_nnz={q['cached_nnz_smem']}/{q['nnz']} "
-              f"vec_rows={q['cached_rows_smem']} regs={q['regs_per_thread']} tiles={q['tiles']} grid={q['grid']}",
+              f" iters={it} smem={q['smem_per_cta']} cached tm/sm={q['cached_nnz_tmem']}/{q['cached_nnz_smem']} of {q['nnz']} ({q['tmem_tiles_per_cta']}+{q['smem_tiles_per_cta']} tiles) "
+              f"vec_rows={q['cached_rows_smem']} regs={q['regs_per_thread']} tiles={q['tiles']} grid={q['grid']}{phases}",
               flush=True)
     h.close()

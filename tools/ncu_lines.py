@@ -31,5 +31,6 @@ for r in csv.reader(out.splitlines()):
 tot_i = sum(x[0] for x in rows)
 tot_s = sum(x[1] for x in rows)
 print(f"total instructions {tot_i}  samples {tot_s}")
-for ie, ss, where, src in sorted(rows, reverse=True)[:n]:
+key = (lambda x: x[1]) if "--samples" in sys.argv else (lambda x: x[0])
+for ie, ss, where, src in sorted(rows, key=key, reverse=True)[:n]:
     print(f"{ie:>11} {100*ie/max(tot_i,1):5.1f}% {ss:>6} {where:24s} {src}")
