@@ -52,17 +52,34 @@ namespace perks {
 namespace cg {
 
 #ifndef PERKS_CG_IPT
-#define PERKS_CG_IPT 8
+#define PERKS_CG_IPT 12
 #endif
-constexpr int NT = 512;             // threads per CTA (16 warps; one CTA per SM)
+#ifndef PERKS_CG_NT
+#define PERKS_CG_NT 512
+#endif
+#ifndef PERKS_CG_CPS
+#define PERKS_CG_CPS 1
+#endif
+// One CTA of 512 threads per SM.  Two CTAs of 256 per SM (the paper's TB/SM knob)
+// would overlap one CTA's per-tile barrier with the other's work, but a kernel containing
+// tcgen05.alloc is limited to one CTA per SM by the occupancy calculator (measured:
+// cudaOccupancyMaxActiveBlocksPerMultiprocessor = 1 at any register/shared-memory footprint),
+// so the TMEM tier and CPS > 1 exclude each other in a cooperative launch.
+#ifndef PERKS_CG_MAXREG  // two 256-thread CTAs per SM need <= 120 registers (measured occupancy)
+#define PERKS_CG_MAXREG (PERKS_CG_CPS > 1 ? 120 : 128)
+#endif
+constexpr int NT = PERKS_CG_NT;     // threads per CTA
+constexpr int CPS = PERKS_CG_CPS;   // co-resident CTAs per SM
 constexpr int IPT = PERKS_CG_IPT;   // items per thread per tile
 constexpr int TI = NT * IPT;        // items per tile
-constexpr int kSmemMax = 227 * 1024;
-constexpr int kMaxG = 256;
+constexpr int kSmemMax = 227 * 1024 / PERKS_CG_CPS - (PERKS_CG_CPS > 1 ? 1024 : 0);
+constexpr int kMaxG = 512;
 constexpr int PAD = 0x7fffffff;     // an empty item slot (after the CTA's last item)
 constexpr int COLMASK = 0x7fffffff; // column bits of an item word; 0x7fffffff = no column
-constexpr int TMEM_COLS = 512;      // one CTA per SM allocates all of TMEM
-constexpr int TMEM_COLS_PER_THREAD = TMEM_COLS / 4;  // 4 warps share each lane quarter
+constexpr int TMEM_COLS = 512 / CPS;  // the CTAs of an SM split its 512 TMEM columns
+// warps w, w+4, ... share lane quarter w%4: each thread gets its share of the CTA's columns
+constexpr int TMEM_COLS_PER_THREAD = TMEM_COLS / (NT / 128);
+static_assert(NT % 128 == 0 && TMEM_COLS >= 32, "TMEM geometry");
 
 // Bytes of one tile record (global and shared memory): values [TI] | item words [TI] | headers [NT].
 template <typename T> constexpr int tile_bytes() { return TI * ((int)sizeof(T) + 4) + NT * 4; }
@@ -83,7 +100,6 @@ template <typename T> struct Params {
   double *scal;                // host loop: <r,r> by iteration parity [2]
   long long *state;            // host loop: [0] done, [1] iterations, [2] status
   unsigned *bar;               // grid barrier words
-  LLWord *ll;                  // persistent (PERKS_CG_LL=1): 2*G tagged all-reduce slots
   unsigned long long *dbg;     // nullable: phase timer (PERKS_CG_TIMING)
   double *hist;                // nullable, kmax+1
   long long *info;             // nullable, 2
@@ -94,7 +110,6 @@ template <typename T> struct Params {
   int sm_tiles;                // tiles per CTA resident in shared memory (MAT)
   int nbuf;                    // stream ring buffers (0: direct loads)
   int fused;                   // persistent: 2 barriers/iteration (p recomputed at the gather)
-  int use_ll;
 };
 
 // Dynamic shared memory layout.
@@ -136,12 +151,17 @@ PERKS_DEVINL double block_sum(double v, double *s_red) {
 PERKS_DEVINL double slots_sum(const double *slots, int G, double *s_bc) {
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
-    double v[kMaxG / 32];
-#pragma unroll
-    for (int j = 0; j < kMaxG / 32; ++j) v[j] = lane + 32 * j < G ? __ldcg(slots + lane + 32 * j) : 0.0;
     double t = 0.0;
+    for (int j0 = 0; j0 < G; j0 += 4 * 32) {  // 4 loads in flight, summed in order
+      double v[4];
 #pragma unroll
-    for (int j = 0; j < kMaxG / 32; ++j) t += v[j];
+      for (int j = 0; j < 4; ++j) {
+        const int c = j0 + 32 * j + lane;
+        v[j] = c < G ? __ldcg(slots + c) : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) t += v[j];
+    }
     t = warp_sum(t);
     if (lane == 0) *s_bc = t;
   }
@@ -467,6 +487,13 @@ template <typename T, bool VEC> PERKS_DEVINL double cg_prologue(const Params<T> 
   return acc;
 }
 
+// Vector loads (p, r, x, A p).  Plain, L1-cacheable loads: every value another CTA wrote is
+// read only after a grid barrier whose acquire (thread 0) and __syncthreads order it before the
+// load (and the acquire invalidates the SM's L1), and the own CTA's writes go through L1.  The
+// gathers reuse p[j] across neighbouring rows, so L1 hits matter: with L2-only (.cg) loads every
+// CTA but the first ran 1.5x slower on the stencil-like matrices (profiles/r02_cg_*).
+template <typename T> PERKS_DEVINL T ldv(const T *p) { return *p; }
+
 // Own-row passes visit rows j = tid, tid+NT, ... in that order (the order of every per-thread
 // inner-product chain); U rows per batch so their loads are in flight together.
 constexpr int U = 4;
@@ -481,8 +508,8 @@ PERKS_DEVINL void cg_p_update(const Params<T> &P, const Own<T, VEC> &o, T beta, 
     for (int u = 0; u < U; ++u) {
       const int j = j0 + u * NT, i = o.R0 + j;
       const bool ok = j < o.rows;
-      r[u] = ok ? (VEC ? o.s_r[j] : __ldcg(P.r + i)) : T(0);
-      pp[u] = ok ? (VEC ? o.s_p[j] : __ldcg(pprev + i)) : T(0);
+      r[u] = ok ? (VEC ? o.s_r[j] : ldv(P.r + i)) : T(0);
+      pp[u] = ok ? (VEC ? o.s_p[j] : ldv(pprev + i)) : T(0);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -505,8 +532,8 @@ template <typename T, bool VEC> PERKS_DEVINL double cg_pap(const Params<T> &P, c
     for (int u = 0; u < U; ++u) {
       const int j = j0 + u * NT, i = o.R0 + j;
       const bool ok = j < o.rows;
-      p[u] = ok ? (VEC ? o.s_p[j] : __ldcg(pcur + i)) : T(0);
-      q[u] = ok ? (VEC ? o.s_q[j] : __ldcg(P.q + i)) : T(0);
+      p[u] = ok ? (VEC ? o.s_p[j] : ldv(pcur + i)) : T(0);
+      q[u] = ok ? (VEC ? o.s_q[j] : ldv(P.q + i)) : T(0);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
@@ -529,8 +556,8 @@ PERKS_DEVINL double cg_xr_update(const Params<T> &P, const Own<T, VEC> &o, T a, 
         p[u] = ok ? o.s_p[j] : T(0); q[u] = ok ? o.s_q[j] : T(0);
         x[u] = ok ? o.s_x[j] : T(0); r[u] = ok ? o.s_r[j] : T(0);
       } else {
-        p[u] = ok ? __ldcg(pcur + i) : T(0); q[u] = ok ? __ldcg(P.q + i) : T(0);
-        x[u] = ok ? __ldcg(P.x + i) : T(0); r[u] = ok ? __ldcg(P.r + i) : T(0);
+        p[u] = ok ? ldv(pcur + i) : T(0); q[u] = ok ? ldv(P.q + i) : T(0);
+        x[u] = ok ? ldv(P.x + i) : T(0); r[u] = ok ? ldv(P.r + i) : T(0);
       }
     }
 #pragma unroll
@@ -563,13 +590,13 @@ template <typename T, bool FUSED> struct CgGather {
   PERKS_DEVINL void load(int jc, T &a, T &b) const {
     const int j = jc < 0 ? 0 : jc;
     if (!FUSED) {
-      a = __ldcg(pcur + j);
+      a = ldv(pcur + j);
       b = T(0);
       return;
     }
     const bool own = (unsigned)(j - R0) < (unsigned)rows;
-    a = __ldcg((own ? pcur : pprev) + j);
-    b = own ? T(0) : __ldcg(r + j);
+    a = ldv((own ? pcur : pprev) + j);
+    b = own ? T(0) : ldv(r + j);
   }
   PERKS_DEVINL T value(int jc, T a, T b) const {
     if (jc < 0) return T(0);
@@ -603,80 +630,51 @@ PERKS_DEVINL void cg_spmv(const Params<T> &P, const Own<T, VEC> &o, TileSet &ts,
 }
 
 // ------------------------------------------------------------------------ kernels
-// All-reduce of one double per CTA without a separate barrier (PERKS_CG_LL=1; measured slower
-// than barrier + slot read on B200, kept as an option): CTA c stores its partial with a tag into
-// LL slot c; one warp of every CTA polls all G slots until each carries the tag, then sums them
-// in the same fixed order as slots_sum.  `order`: release fence before the store, acquire fence
-// after the poll (the next phase reads other CTAs' vectors).
-PERKS_DEVINL double ll_allreduce(LLWord *slots, int G, unsigned tag, double part, bool order, double *s_bc) {
-  if (threadIdx.x == 0) {
-    if (order) fence_acq_rel_gpu();
-    LL<double>::put(slots + 2 * blockIdx.x, part, tag);
-  }
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    double v[kMaxG / 32];
-    const unsigned long long t0 = globaltimer_ns();
-    unsigned spins = 0;
-    bool ok;
-    do {
-      ok = true;
-#pragma unroll
-      for (int j = 0; j < kMaxG / 32; ++j) {
-        v[j] = 0.0;
-        if (lane + 32 * j < G) ok &= LL<double>::get(slots + 2 * (lane + 32 * j), tag, v[j]);
-      }
-      if ((++spins & 255u) == 0 && globaltimer_ns() - t0 > PERKS_WATCHDOG_NS) watchdog_fire("cg allreduce", tag, G);
-    } while (!__all_sync(0xffffffffu, ok));
-    if (order) fence_acq_rel_gpu();
-    double t = 0.0;
-#pragma unroll
-    for (int j = 0; j < kMaxG / 32; ++j) t += v[j];
-    t = warp_sum(t);
-    if (lane == 0) *s_bc = t;
-  }
-  __syncthreads();
-  return *s_bc;
-}
-
 // Phase timer (development, PERKS_CG_TIMING=1): CTA 0 / thread 0 accumulates globaltimer deltas
 // per phase into P.dbg[0..3] (0 p update, 1 SpMV, 2 <p,Ap> + all-reduce, 3 x/r update +
 // all-reduce); P.dbg[8] += iterations.
+// Every CTA's thread 0 also adds its own SpMV time to P.dbg[16 + c] (load balance).
 struct PhaseClock {
   unsigned long long *dbg;
   unsigned long long t;
-  PERKS_DEVINL explicit PhaseClock(unsigned long long *d)
-      : dbg(blockIdx.x == 0 && threadIdx.x == 0 ? d : nullptr), t(0) {
-    if (dbg) t = globaltimer_ns();
+  PERKS_DEVINL explicit PhaseClock(unsigned long long *d) : dbg(threadIdx.x == 0 ? d : nullptr), t(0) {
+    if (dbg) {
+      t = globaltimer_ns();
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      dbg[16 + kMaxG + blockIdx.x] = smid;
+    }
   }
   PERKS_DEVINL void tick(int ph) {
     if (dbg) {
       const unsigned long long n = globaltimer_ns();
-      dbg[ph] += n - t;
+      if (blockIdx.x == 0) dbg[ph] += n - t;
+      if (ph == 1) dbg[16 + blockIdx.x] += n - t;
       t = n;
     }
   }
 };
 
 // (b)/(c): the whole solve in one cooperative launch.
-template <typename T, bool VEC> __global__ void __launch_bounds__(NT, 1) cg_persistent_kernel(Params<T> P) {
+template <typename T, bool VEC> __global__ void __maxnreg__(PERKS_CG_MAXREG) cg_persistent_kernel(Params<T> P) {
   extern __shared__ __align__(128) unsigned char smem[];
   double *s_red = reinterpret_cast<double *>(smem + Smem::RED);
   double *s_bc = reinterpret_cast<double *>(smem + Smem::BCAST);
   const Own<T, VEC> o = own_view<T, VEC>(P, smem);
   TileSet ts = tiles_init<T>(P, smem, VEC ? P.rows_max : 0, true, true);
   const int c = blockIdx.x;
-  // all-reduce of the per-CTA partials: grid barrier + slot read, or tagged LL slots
-  // (P.use_ll); kind 0 = <p,Ap>, 1 = <r,r>; both give the same bits
+  // all-reduce of the per-CTA partials: slot write, grid barrier, slot read in a fixed order
+  // (kind 0 = <p,Ap>, 1 = <r,r>).  A barrier-free variant with tagged (LL) slots polled by every
+  // CTA was measured slower on B200 (G2 12.9 vs 9.6 us/iteration: 148 pollers on one set of L2
+  // lines) and removed.
   unsigned nb = 0;
-  auto allreduce = [&](int kind, unsigned tag, double part, bool order, double *bc) -> double {
-    if (P.use_ll) return ll_allreduce(P.ll + 2 * kind * P.G, P.G, tag, part, order, bc);
+  auto allreduce = [&](int kind, double part, double *bc) -> double {
     if (threadIdx.x == 0) P.slots[kind * P.G + c] = part;
     grid_barrier(P.bar, ++nb);
     return slots_sum(P.slots + kind * P.G, P.G, bc);
   };
   double part = block_sum(cg_prologue<T, VEC>(P, o), s_red);
-  double rr = allreduce(1, 1u, part, true, s_bc);  // r_0 = b published before the gathers
+  double rr = allreduce(1, part, s_bc);  // (the barrier also publishes r_0 = b, p_{-1} = 0)
   if (c == 0 && threadIdx.x == 0 && P.hist) P.hist[0] = rr;
   PhaseClock clk(P.dbg);
   long long k = 0;
@@ -687,7 +685,6 @@ template <typename T, bool VEC> __global__ void __launch_bounds__(NT, 1) cg_pers
     T *pcur = (k & 1) ? P.p1 : P.p0;
     const T *pprev = (k & 1) ? P.p0 : P.p1;
     const T bt = (T)beta;
-    const unsigned tag = (unsigned)k + 2u;
     cg_p_update<T, VEC>(P, o, bt, pprev, pcur);
     if (P.fused) __syncthreads();
     else grid_barrier(P.bar, ++nb);  // every CTA's p_k published before the gathers
@@ -695,21 +692,19 @@ template <typename T, bool VEC> __global__ void __launch_bounds__(NT, 1) cg_pers
     cg_spmv<T, VEC>(P, o, ts, smem, P.fused, bt, pprev, pcur);
     clk.tick(1);
     part = block_sum(cg_pap<T, VEC>(P, o, pcur), s_red);
-    // phase B touches only this CTA's rows: no ordering needed
-    const double pap = allreduce(0, tag, part, false, s_bc + 1);
+    const double pap = allreduce(0, part, s_bc + 1);
     clk.tick(2);
     if (!(pap > 0.0)) { status = 1; break; }  // reading RC4: not positive definite
     const double alpha = rr / pap;
     part = block_sum(cg_xr_update<T, VEC>(P, o, (T)alpha, pcur), s_red);
-    // the next (fused) SpMV gathers the r and p other CTAs published: release/acquire
-    const double rr_new = allreduce(1, tag, part, P.fused != 0, s_bc + 2);
+    const double rr_new = allreduce(1, part, s_bc + 2);  // (publishes r_{k+1} for fused gathers)
     clk.tick(3);
     beta = rr_new / rr;
     rr = rr_new;
     ++k;
     if (c == 0 && threadIdx.x == 0 && P.hist) P.hist[k] = rr;
   }
-  if (clk.dbg) clk.dbg[8] += k;
+  if (clk.dbg && c == 0) clk.dbg[8] += k;
   if (VEC)
     for (int j = threadIdx.x; j < o.rows; j += NT) P.x[o.R0 + j] = o.s_x[j];
   if (c == 0 && threadIdx.x == 0 && P.info) { P.info[0] = k; P.info[1] = status; }
@@ -855,16 +850,15 @@ void path_coord(const int64_t *ro, int64_t n, int64_t nnz, int64_t d, int64_t &i
 }
 
 struct Layout {
-  size_t ws_bytes, off_r, off_p0, off_p1, off_q, off_slots, off_scal, off_state, off_bar, off_dbg, off_ll, ll_bytes;
+  size_t ws_bytes, off_r, off_p0, off_p1, off_q, off_slots, off_scal, off_state, off_bar, off_dbg;
 };
 Layout ws_layout(const perks_cg_s *h) {
   Layout L{};
   const size_t vb = align256((size_t)std::max<int64_t>(h->n, 1) * h->elem());
   size_t o = 0;
   L.off_bar = o; o += 256;
-  L.off_dbg = o; o += 256;   // bytes 256..511: phase timer (tools/cg_timing.py reads it there)
+  L.off_dbg = o; o += 256 + 16 * kMaxG;  // bytes 256..: phase timer (tools/cg_timing.py reads it there)
   L.off_slots = o; o += align256((size_t)2 * h->G * 8);
-  L.off_ll = o; L.ll_bytes = align256((size_t)2 * h->G * 16); o += L.ll_bytes;
   L.off_scal = o; o += 256;
   L.off_state = o; o += 256;
   L.off_r = o; o += vb;
@@ -897,12 +891,17 @@ CgPlan make_plan(const perks_cg_s *h, perks_variant v, perks_cg_policy pol) {
   const int S = (int)h->elem();
   const int tb = f64 ? tile_bytes<double>() : tile_bytes<float>();
   const int vecb = 4 * a16((long long)h->rows_max * S);
-  pl.vec = (pol == PERKS_CG_VEC || pol == PERKS_CG_MIX) && Smem::VEC + vecb <= kSmemMax;
   const bool mat = pol == PERKS_CG_MAT || pol == PERKS_CG_MIX;
+  const int tmem_t = mat ? std::min(h->tiles_max, f64 ? tmem_tiles<double>() : tmem_tiles<float>()) : 0;
+  const bool streams = h->tiles_max > tmem_t;
+  // VEC only where it leaves room for a stream ring of two buffers (when the SpMV streams):
+  // a one-deep ring costs more than the vector caching saves (G4: 67.5 vs 56.1 us/iteration)
+  pl.vec = (pol == PERKS_CG_VEC || pol == PERKS_CG_MIX) &&
+           Smem::VEC + vecb + (streams ? 2 * tb : 0) <= kSmemMax;
   const int base = Smem::VEC + (pl.vec ? vecb : 0);
   const int fit = std::max(0, (kSmemMax - base) / tb);  // tile records that fit next to VEC
   if (mat) {
-    pl.tm = std::min(h->tiles_max, f64 ? tmem_tiles<double>() : tmem_tiles<float>());
+    pl.tm = tmem_t;
     const int rest = h->tiles_max - pl.tm;
     if (rest <= fit) {
       pl.sm = rest;  // everything resident: no stream
@@ -919,8 +918,8 @@ CgPlan make_plan(const perks_cg_s *h, perks_variant v, perks_cg_policy pol) {
   // up one gather load per nonzero costs more than the third barrier (measured: G2 9.0 vs 10.1,
   // G3 14.1 vs 13.5, G4 98.9 vs 84.7 us/iteration fused vs not; PERKS_CG_FUSED overrides)
   pl.fused = env_int("PERKS_CG_FUSED", h->tiles_max <= 1 ? 1 : 0) != 0;
-  // TMEM holds all 512 columns: exactly one CTA per SM (more than half the SM's shared memory)
-  if (pl.tm > 0) pl.smem = std::max(pl.smem, 120 * 1024);
+  // each CTA allocates 512/CPS TMEM columns: at most CPS CTAs per SM (shared memory > 1/(CPS+1))
+  if (pl.tm > 0) pl.smem = std::max(pl.smem, 228 * 1024 / (CPS + 1) + 1024);
   // what is cached, per CTA as tiles_init decides; bytes per iteration
   const int64_t items_total = (int64_t)h->ntiles * TI;
   for (int c = 0; c < h->G; ++c) {
@@ -961,7 +960,6 @@ template <typename T> Params<T> make_params(perks_cg_s *h, void *ws, const CgPla
   P.scal = reinterpret_cast<double *>(w + L.off_scal);
   P.state = reinterpret_cast<long long *>(w + L.off_state);
   P.bar = reinterpret_cast<unsigned *>(w + L.off_bar);
-  P.ll = reinterpret_cast<LLWord *>(w + L.off_ll);
   P.dbg = env_int("PERKS_CG_TIMING", 0) ? reinterpret_cast<unsigned long long *>(w + L.off_dbg) : nullptr;
   P.rows_max = h->rows_max;
   P.tm_tiles = pl.tm;
@@ -998,13 +996,12 @@ cudaError_t launch_solve(perks_cg_s *h, const CgPlan &pl, const void *b, void *x
     cg_hl_finish_kernel<T><<<1, 32, 0, s>>>(P);
     return cudaGetLastError();
   }
-  const Layout L = ws_layout(h);
-  P.use_ll = env_int("PERKS_CG_LL", 0);
-  if (P.use_ll && (e = cudaMemsetAsync(static_cast<unsigned char *>(ws) + L.off_ll, 0, L.ll_bytes, s)) != cudaSuccess)
-    return e;
   if ((e = reset_grid_barrier(P.bar, s)) != cudaSuccess) return e;
   void *kfn = pl.vec ? (void *)cg_persistent_kernel<T, true> : (void *)cg_persistent_kernel<T, false>;
   if ((e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem)) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared)) !=
+      cudaSuccess)
+    return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(h->G);
   cfg.blockDim = dim3(NT);
@@ -1016,6 +1013,11 @@ cudaError_t launch_solve(perks_cg_s *h, const CgPlan &pl, const void *b, void *x
   cfg.attrs = at;
   cfg.numAttrs = 1;
   void *args[] = {&P};
+  int occ = 0;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, NT, (size_t)pl.smem)) != cudaSuccess) return e;
+  if (occ * h->num_sms < h->G) {
+    return cudaErrorCooperativeLaunchTooLarge;
+  }
   return cudaLaunchKernelExC(&cfg, kfn, args);
 }
 
@@ -1112,7 +1114,7 @@ perks_status perks_cg_create(const perks_csr_desc *d, int device, perks_cg_t *ou
   h->num_sms = env_int("PERKS_NUM_SMS", h->num_sms);
   // CTA-level (TB-level) merge-path partition, row aligned
   const int64_t L = n + nnz;
-  h->G = (int)std::max<int64_t>(1, std::min<int64_t>(std::min(h->num_sms, kMaxG), (L + 1023) / 1024));
+  h->G = (int)std::max<int64_t>(1, std::min<int64_t>(std::min(CPS * h->num_sms, kMaxG), (L + 1023) / 1024));
   h->h_crow.resize(h->G + 1);
   for (int c = 0; c <= h->G; ++c) {
     int64_t i, k;

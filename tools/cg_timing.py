@@ -50,12 +50,16 @@ for wl in wls:
         phases = ""
         if os.environ.get("PERKS_CG_TIMING") and v != "hostloop":
             ws = h.workspace()
-            ws[256:512].zero_()
+            ws[256:256 + 8 * 528].zero_()
             h.solve(b, K, 0.0, v, p, out=x, history=hist)
             torch.cuda.synchronize()
-            d = ws[256:512].cpu().numpy().view(np.uint64)
+            d = ws[256:256 + 8 * 528].cpu().numpy().view(np.uint64)
             nit = max(int(d[8]), 1)
-            phases = " phases(us/iter): " + " ".join(f"{d[i] / nit / 1e3:.2f}" for i in range(4))
+            g = q["grid"]
+            per = d[16:16 + g] / nit / 1e3
+            phases = (" phases(us/iter): " + " ".join(f"{d[i] / nit / 1e3:.2f}" for i in range(4)) +
+                      f" spmv/CTA min {per.min():.2f} med {np.median(per):.2f} max {per.max():.2f}"
+                      f" argmax {int(per.argmax())}")
         if base is None:
             base = t
         gbs = q["unfused_bytes_per_iter"] / (t * 1e-6) / 1e9
