@@ -7,7 +7,11 @@ largest configuration that fits one GPU (C5 is the multi-GPU slab workload; C1-C
 selectable with --config and are parity-test cases, not the headline).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mine|reference]
-                    [--config C1..C5] [--variant perks|persistent|hostloop|auto]
+                    [--config C1..C5|G1..G5] [--variant perks|persistent|hostloop|auto]
+                    [--policy auto|imp|vec|mat|mix]
+
+--config G1..G5 benches the PERKS conjugate-gradient workloads with the
+paper's CG metric, sustained GB/s; see run_cg.
 
 Prints ONE JSON line on rank 0.  `value` = whole-job GCell-updates/s (cells x T x K x N / max
 over ranks of the device-timed region).  `--impl reference` times the CPU oracle (the only other
@@ -419,14 +423,209 @@ def run_mine(args):
     return 0
 
 
+# ----------------------------------------------------------------------------- CG (NEXT-3)
+# --config G1..G5: the PERKS conjugate-gradient workloads (seeded_inputs/sparse.py CG_WORKLOADS,
+# the Table V size classes).  One bench step = one solve of K iterations (tol = 0) from x0 = 0.
+# Metric: the paper's CG figure of merit, sustained memory bandwidth: unfused-equivalent
+# bytes per iteration (matrix in CSR once + the 15 vector accesses per row of Algorithm P:244-258,
+# perks_cg_info.unfused_bytes_per_iter) x iterations / time.
+CG_METRIC = "CG sustained GB/s (unfused-equivalent bytes per iteration, P:465); speedup over host-loop"
+
+
+def _cg_setup(name):
+    import seeded_inputs.sparse as sp
+
+    kind, size, dtype, iters, desc = sp.CG_WORKLOADS[name]
+    ro, ci, va = sp.matrix(kind, size)
+    return sp, kind, size, dtype, iters, desc, ro, ci, va
+
+
+def _cg_oracle_rate(ro, ci, va, b, iters, unfused, budget_s, nthreads):
+    import oracle
+
+    oracle.cg(ro, ci, va, b, kmax=1, nthreads=nthreads)  # warm (thread pool, library load)
+    t0 = time.perf_counter()
+    oracle.cg(ro, ci, va, b, kmax=1, nthreads=nthreads)
+    t1 = max(time.perf_counter() - t0, 1e-6)
+    k = int(max(1, min(iters, budget_s / t1)))
+    t0 = time.perf_counter()
+    _, _, kk = oracle.cg(ro, ci, va, b, kmax=k, nthreads=nthreads)
+    dt = time.perf_counter() - t0
+    return unfused * kk / dt / 1e9, kk, dt
+
+
+def run_cg_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    sp, kind, size, dtype, iters, desc, ro, ci, va = _cg_setup(args.config)
+    n, nnz = len(ro) - 1, len(ci)
+    S = 8 if dtype == np.float64 else 4
+    unfused = nnz * (S + 4) + (n + 1) * 4 + n * S * 15
+    b = sp.rhs(n, dtype=dtype)
+    cores = os.cpu_count() or 1
+    times, ks = [], []
+    for i in range(args.warmup + args.steps):
+        v, kk, dt = _cg_oracle_rate(ro, ci, va, b, iters, unfused, 2.0, cores)
+        if i >= args.warmup:
+            times.append(dt)
+            ks.append(kk)
+    value = unfused * sum(ks) / sum(times) / 1e9
+    line = {
+        "impl": "reference", "metric": CG_METRIC, "value": value, "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(times) / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64" if dtype == np.float64 else "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {desc}", "sample_iterations": ks[0]},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{ks[0]} of {iters} CG iterations per bench step, {cores} OpenMP threads "
+                                   "(SpMV rows in parallel, inner products sequential)"},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_cg(args):
+    import torch
+
+    ws, rank, local = _dist()
+    dist = ws > 1
+    if dist:
+        import torch.distributed as tdist
+
+        tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    from paper_2204_02064_b200 import CG
+
+    sp, kind, size, dtype, iters, desc, ro, ci, va = _cg_setup(args.config)
+    K = args.T or iters
+    n, nnz = len(ro) - 1, len(ci)
+    h = CG(ro, ci, va, dtype="f64" if dtype == np.float64 else "f32", device=local)
+    b = torch.from_numpy(sp.rhs(n, dtype=dtype)).to(dev)
+    x = torch.empty_like(b)
+    hist = torch.empty(K + 1, dtype=torch.float64, device=dev)
+    info = torch.zeros(2, dtype=torch.int64, device=dev)
+    variant = args.variant if args.variant != "auto" else "perks"
+    policy = args.policy
+    q = h.query(variant, policy)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def one(v, p):
+        h.solve(b, K, 0.0, v, p, out=x, history=hist, info=info)
+
+    for _ in range(args.warmup):
+        one(variant, policy)
+    torch.cuda.synchronize()
+    if dist:
+        tdist.barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    ev = []
+    for _ in range(args.steps):
+        flush.fill_(1)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        one(variant, policy)
+        e1.record(stream)
+        ev.append((e0, e1))
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    done = int(info[0].item())
+    per = [a.elapsed_time(c) for a, c in ev]
+    tot_ms = sum(per)
+    if dist:
+        t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    ms_per = tot_ms / args.steps
+    unfused = q["unfused_bytes_per_iter"]
+    value = unfused * done * args.steps * ws / (tot_ms * 1e-3) / 1e9
+    hl = None
+    if variant != "hostloop" and not args.no_hostloop:
+        one("hostloop", "imp")
+        torch.cuda.synchronize()
+        hts = []
+        for _ in range(max(1, min(args.steps, 3))):
+            flush.fill_(1)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            one("hostloop", "imp")
+            e1.record(stream)
+            torch.cuda.synchronize()
+            hts.append(e0.elapsed_time(e1))
+        hl = statistics.mean(hts)
+    e2e = None
+    if not args.no_e2e:
+        bh = sp.rhs(n, dtype=dtype)
+        h.solve_host(bh, K, 0.0, variant, policy)
+        n_e2e = max(1, min(args.steps, 3))
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            _, _, kk, _ = h.solve_host(bh, K, 0.0, variant, policy)
+        dt = time.perf_counter() - t0
+        S = 8 if dtype == np.float64 else 4
+        e2e = {"value": unfused * kk * n_e2e * ws / dt / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": n * S, "d2h_bytes_per_step": n * S + (K + 1) * 8 + 16,
+               "timing": "host wall clock around perks_cg_solve_host (b in, x + history + info out)"}
+    peaks = _peaks()
+    launches = 1 if variant != "hostloop" else 2 * K + 2
+    kern_ms = ms_per / launches
+    alg = q["dram_bytes_per_iter"] * done / launches
+    achieved = alg / (kern_ms * 1e-3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": achieved / peaks["hbm_gbs"], "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+            "traffic": None, "kernel": q["kernel_name"],
+            "algorithmic_bytes": "modelled DRAM bytes per iteration (uncached matrix tiles + vectors "
+                                 "leaving the SM), perks_cg_info.dram_bytes_per_iter"}
+    line = {
+        "metric": CG_METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64" if dtype == np.float64 else "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {desc}", "iterations_per_bench_step": done,
+                   "variant": q["variant"], "policy": q["policy"], "kernel": q["kernel_name"],
+                   "grid": q["grid"], "block": q["block"], "n_rows": n, "nnz": nnz,
+                   "cached_items_tmem": q["cached_nnz_tmem"], "cached_items_smem": q["cached_nnz_smem"],
+                   "parallelism": f"replicas{ws}" if ws > 1 else "single",
+                   "l2": "flushed between timed steps (256 MiB device write outside the events)"},
+        "us_per_iteration": 1e3 * ms_per / max(done, 1),
+        "hostloop_ms_per_step": hl, "speedup_vs_hostloop": (hl / ms_per) if hl else None,
+        "ms_per_step_best": min(per), "ms_per_step_median": statistics.median(per),
+        "roofline": roof, "gpu_launches": launches * args.steps, "clocks": clocks, "e2e": e2e,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        bh = sp.rhs(n, dtype=dtype)
+        cores = os.cpu_count() or 1
+        v, kk, dt = _cg_oracle_rate(ro, ci, va, bh, K, unfused, 8.0, cores)
+        v1, kk1, dt1 = _cg_oracle_rate(ro, ci, va, bh, K, unfused, 4.0, 1)
+        line["cpu_baseline"] = {"value": v, "unit": "GB/s", "cores": cores, "kind": "oracle",
+                                "sample": f"{kk} of {K} iterations, {cores} OpenMP threads, {dt:.1f} s",
+                                "single_thread": {"value": v1, "unit": "GB/s", "cores": 1,
+                                                  "sample": f"{kk1} of {K} iterations, 1 thread, {dt1:.1f} s"}}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    h.close()
+    if dist:
+        tdist.barrier()
+        tdist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
-    ap.add_argument("--config", default="C4", choices=sorted(si.CONFIGS),
-                    help="C5 = the slab-decomposed multi-GPU workload (N>1 under torchrun)")
+    ap.add_argument("--config", default="C4", choices=sorted(si.CONFIGS) + ["G1", "G2", "G3", "G4", "G5"],
+                    help="C5 = the slab-decomposed multi-GPU workload (N>1 under torchrun); "
+                         "G1..G5 = the PERKS CG workloads (NEXT-3)")
+    ap.add_argument("--policy", default="auto", choices=["auto", "imp", "vec", "mat", "mix"],
+                    help="CG cache policy (G configs)")
     ap.add_argument("--variant", default="perks",
                     choices=["perks", "persistent", "hostloop", "auto"])
     ap.add_argument("--T", type=int, default=0, help="override time steps (dev only)")
@@ -434,6 +633,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-hostloop", action="store_true")
     args = ap.parse_args()
+    if args.config.startswith("G"):
+        return run_cg_reference(args) if args.impl == "reference" else run_cg(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_mine(args)
