@@ -222,6 +222,87 @@ def _traffic_from_profiles(kernel_prefix, config):
     return None
 
 
+def run_nccl_slab(args):
+    """SURVEY §8(e)(a) baseline: C5 z-slabs, face planes exchanged every step by NCCL send/recv
+    (torch.distributed batch_isend_irecv), one host-loop step per time step through the C ABI
+    (paper_2204_02064_b200/nccl_slab.py).  Same metric/config as the in-kernel exchange path."""
+    import torch
+    import torch.distributed as tdist
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    if ws > 1:
+        tdist.init_process_group("nccl", device_id=dev)
+    from paper_2204_02064_b200 import Stencil
+    from paper_2204_02064_b200.nccl_slab import NcclSlabHostLoop
+
+    c = _cfg(args.config)
+    offs, w = si.preset(c["stencil"])
+    T = args.T or c["steps"]
+    nz, ny, nx = c["shape"]
+    nzg = nz * ws
+    radius = max(max(abs(v) for v in o) for o in offs)
+    holder = {}
+
+    def empty(shape):
+        return torch.empty(shape, dtype=torch.float64 if c["dtype"] == "f64" else torch.float32, device=dev)
+
+    def step(src, dst):
+        st = holder.get("st")
+        if st is None:
+            st = holder["st"] = Stencil(tuple(src.shape), offs, w, dtype=c["np_dtype"], device=local)
+            holder["ws"] = st.workspace("hostloop")
+        st.run(src, 1, "hostloop", out=dst, workspace=holder["ws"])
+
+    sl = NcclSlabHostLoop(nzg, ny, nx, radius, rank, ws, step, empty)
+    sl.load(si.field_torch((sl.nz, ny, nx), c["np_dtype"], dev, index_offset=sl.z0 * ny * nx))
+    sl.run(1)
+    for _ in range(args.warmup):
+        sl.run(T)
+    torch.cuda.synchronize()
+    if ws > 1:
+        tdist.barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    stream = torch.cuda.current_stream(dev)
+    per = []
+    for _ in range(args.steps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        sl.run(T)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        per.append(e0.elapsed_time(e1))
+    clocks = sampler.stop()
+    tot_ms = sum(per)
+    if ws > 1:
+        t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    cells = nz * ny * nx
+    value = cells * T * args.steps * ws / (tot_ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": c["dtype"], "data": "synthetic",
+        "config": {"workload": f"{args.config}: {CONFIG_DESC[args.config]}, global z = {nz} x {ws}",
+                   "parallelism": f"slab{ws}", "variant": "nccl-hostloop",
+                   "exchange": "per step: ncclSend/ncclRecv of the face planes (torch.distributed "
+                               "batch_isend_irecv), then one host-loop kernel on the halo-extended slab",
+                   "time_steps_per_bench_step": T},
+        "us_per_time_step": 1e3 * tot_ms / args.steps / T,
+        "gpu_launches": T * args.steps, "clocks": clocks, "e2e": None,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        tdist.barrier()
+        tdist.destroy_process_group()
+    return 0
+
+
 def run_mine(args):
     import torch
 
@@ -627,7 +708,8 @@ def main():
     ap.add_argument("--policy", default="auto", choices=["auto", "imp", "vec", "mat", "mix"],
                     help="CG cache policy (G configs)")
     ap.add_argument("--variant", default="perks",
-                    choices=["perks", "persistent", "hostloop", "auto"])
+                    choices=["perks", "persistent", "hostloop", "auto", "nccl"],
+                    help="nccl = the NCCL host-loop slab baseline (C5, SURVEY §8(e)(a))")
     ap.add_argument("--T", type=int, default=0, help="override time steps (dev only)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -637,6 +719,8 @@ def main():
         return run_cg_reference(args) if args.impl == "reference" else run_cg(args)
     if args.impl == "reference":
         return run_reference(args)
+    if args.variant == "nccl":
+        return run_nccl_slab(args)
     return run_mine(args)
 
 

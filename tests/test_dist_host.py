@@ -58,3 +58,64 @@ def test_neighbour_blob_exchange_gloo(world):
         lo, hi = res[r]
         assert lo == (bytes([r - 1]) * 128 if r > 0 else None)
         assert hi == (bytes([r + 1]) * 128 if r < world - 1 else None)
+
+
+# ---------------------------------------------------------------- NCCL host-loop slab baseline
+# per-step halo send/recv + one host-loop step per time step.  The exchange logic
+# runs here on CPU with gloo and the CPU oracle as the step; the gathered slabs must equal the
+# oracle on the global domain bit-exactly (reading R12) — on GPU the same class drives NCCL and
+# the CUDA library (bench.py --variant nccl).
+
+def _nccl_slab_worker(rank, world, port, q, name, shape, steps):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    import seeded_inputs as si
+    from paper_2204_02064_b200.nccl_slab import NcclSlabHostLoop
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    offs, w = si.preset(name)
+    r = max(max(abs(v) for v in o) for o in offs)
+    nz, ny, nx = shape
+    u0 = si.field(shape, dtype=np.float64)
+
+    def step(src, dst):
+        dst.copy_(torch.from_numpy(oracle.run(src.numpy(), offs, w, 1)))
+
+    sl = NcclSlabHostLoop(nz, ny, nx, r, rank, world, step, lambda s: torch.zeros(s, dtype=torch.float64))
+    sl.load(torch.from_numpy(u0[sl.z0:sl.z1]))
+    out = sl.run(steps).numpy().copy()
+    q.put((rank, sl.z0, sl.z1, out))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,name,shape,steps", [(2, "3d7pt", (9, 6, 7), 5), (3, "3d27pt", (11, 5, 6), 4),
+                                                     (2, "3d13pt", (12, 7, 7), 3)])
+def test_nccl_slab_hostloop_matches_global_oracle(world, name, shape, steps):
+    import numpy as np
+    import torch.multiprocessing as mp
+
+    import oracle
+    import seeded_inputs as si
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_nccl_slab_worker, args=(r, world, port, q, name, shape, steps)) for r in range(world)]
+    for p in ps:
+        p.start()
+    parts = [q.get(timeout=120) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    offs, w = si.preset(name)
+    ref = oracle.run(si.field(shape, dtype=np.float64), offs, w, steps)
+    got = np.empty_like(ref)
+    for _, z0, z1, out in parts:
+        got[z0:z1] = out
+    assert np.array_equal(got, ref)
