@@ -18,8 +18,13 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "stream3d.cuh"
 
 namespace perks {
+
+// TMA descriptors (k3d_stream.cu)
+bool tma_available();
+bool encode_map3(CUtensorMap *m, const Problem &p, const void *base, int bx, int by);
 
 constexpr int KW3_TX = 32, KW3_TY = 16, KW3_THREADS = KW3_TX * KW3_TY, KW3_ZC = 32, KW3_MAXR = 3;
 // planes in flight ahead of the one being waited for (one-plane lookahead ran 3d13pt fp64 256^3 at
@@ -218,6 +223,207 @@ __global__ void __launch_bounds__(KW3_THREADS) wide3_persistent_kernel(const T *
   }
 }
 
+// ------------------------------------------------------------------ TMA column kernel (3d13pt)
+// The Table II 3d13pt preset (PS 1: every out-of-plane point on the cell's own z column) on a
+// B200-style pipeline instead of per-element cp.async: one thread issues ONE tensor-box copy per
+// input plane (the (TX+2r) x (TY+2r) window, out-of-domain cells zero-filled by the TMA unit) into
+// a ring of NSL shared-memory slots, completing on the slot's mbarrier; a thread owns V cells in x
+// (16 bytes) x RY rows, keeps its cells' values of planes o-r .. o+r in registers (the z terms)
+// and reads only the in-plane neighbours of output plane o from the slot.  Per output plane and
+// cell: 9 in-plane values shared across the thread's V x RY cells (row segments loaded once)
+// instead of 13 scalar loads, no address arithmetic for the loads, one CTA barrier per plane.
+// Same chain order (reading R5) as every other kernel: bit-identical results.
+#ifndef PERKS_W3T_MINB
+#define PERKS_W3T_MINB 2
+#endif
+constexpr int KT3_NW = 8, KT3_RY = 2, KT3_NT = 32 * KT3_NW, KT3_TY = KT3_NW * KT3_RY, KT3_LA = 3;
+template <typename T> struct KT3 {
+  static constexpr int V = 16 / (int)sizeof(T), TX = 32 * V;
+  static constexpr int R = WideSet3<1>::R;
+  // the box starts PX = R rounded up to 16 bytes left of the tile: the tensor copy's innermost
+  // start must be 16-byte aligned (an fp32 box starting 8 bytes off faults as an illegal
+  // instruction on B200)
+  static constexpr int PX = (R * (int)sizeof(T) + 15) / 16 * 16 / (int)sizeof(T);
+  static constexpr int BX = TX + 2 * PX;  // box width (a 16-byte multiple)
+  static constexpr int BY = KT3_TY + 2 * R;
+  static constexpr int SLOT = (BX * BY * (int)sizeof(T) + 127) / 128 * 128 / (int)sizeof(T);
+  static constexpr int NSL = R + 1 + KT3_LA;  // plane o's window + planes up to o+r+LA in flight
+  static constexpr size_t SMEM = (size_t)NSL * SLOT * sizeof(T) + 128;  // + mbarriers
+};
+
+struct WideMaps3 {
+  CUtensorMap m[3];  // in, out, tmp: box {BX, BY, 1}
+};
+
+// One unit: tile (x0, y0), output planes [z0, z1) of one step, src -> dst.  Arrivals q = z0-R ..
+// z1+R-1 (input planes); plane q's own cells enter the column window when it lands; output
+// o = q - R is computed when plane q is resident (its in-plane window is plane o's slot).
+// `k` = running arrival counter (slot = k % NSL, mbarrier parity = (k / NSL) & 1).
+template <typename T>
+__device__ void unit3t(const CUtensorMap *map, T *__restrict__ dst, int nx, int ny, int nz, int x0, int y0, int z0,
+                       int z1, const WideCoef3<T> &c, T *ring, uint64_t *bars, unsigned &k) {
+  using K = KT3<T>;
+  using WS = WideSet3<1>;
+  constexpr int R = K::R, V = K::V, NSL = K::NSL;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int xl = lane * V, yl = w * KT3_RY;  // tile-local first cell
+  const int q0 = z0 - R, q1 = z1 + R;        // arrivals [q0, q1)
+  // prologue: the first min(NSL, arrivals) planes (planes outside [0, nz) are not loaded)
+  if (threadIdx.x == 0)
+    for (int i = 0; i < NSL && q0 + i < q1; i++) {
+      const int q = q0 + i;
+      const unsigned kk = k + i;
+      if (q >= 0 && q < nz) {
+        mbar_arrive_tx(bars + kk % NSL, (unsigned)(K::BX * K::BY * sizeof(T)));
+        tma_load_3d(ring + (size_t)(kk % NSL) * K::SLOT, map, x0 - K::PX, y0 - R, q, bars + kk % NSL);
+      } else {
+        mbar_arrive(bars + kk % NSL);  // empty plane: complete the phase without data
+      }
+    }
+  T col[2 * R + 1][KT3_RY][V];  // own cells of planes o-R .. o+R (index 2R = newest)
+#pragma unroll
+  for (int a = 0; a < 2 * R + 1; a++)
+#pragma unroll
+    for (int ry = 0; ry < KT3_RY; ry++)
+#pragma unroll
+      for (int v = 0; v < V; v++) col[a][ry][v] = T(0);
+  for (int q = q0; q < q1; q++, k++) {
+    const unsigned sl = k % NSL;
+    mbar_wait(bars + sl, (k / NSL) & 1);
+    const T *pq = ring + (size_t)sl * K::SLOT;
+    // shift the column window and append plane q's own cells (zero outside the domain's z range)
+#pragma unroll
+    for (int a = 0; a < 2 * R; a++)
+#pragma unroll
+      for (int ry = 0; ry < KT3_RY; ry++)
+#pragma unroll
+        for (int v = 0; v < V; v++) col[a][ry][v] = col[a + 1][ry][v];
+    const bool qin = q >= 0 && q < nz;
+#pragma unroll
+    for (int ry = 0; ry < KT3_RY; ry++) {
+      T own[V];
+      const T *src = pq + (size_t)(yl + ry + R) * K::BX + xl + K::PX;
+      if constexpr ((K::PX * sizeof(T)) % 16 == 0) vload<T, V>(own, src);
+      else
+#pragma unroll
+        for (int v = 0; v < V; v++) own[v] = src[v];
+#pragma unroll
+      for (int v = 0; v < V; v++) col[2 * R][ry][v] = qin ? own[v] : T(0);
+    }
+    const int o = q - R;
+    if (o >= z0) {  // output plane o: in-plane window = the slot of arrival k - R
+      const T *po = ring + (size_t)((k - R) % NSL) * K::SLOT;
+      const bool zin = o >= R && o < nz - R;
+#pragma unroll
+      for (int ry = 0; ry < KT3_RY; ry++) {
+        const int y = y0 + yl + ry;
+        // row segments: centre row x-R .. x+V+R-1, rows y+dy (dy != 0) at x .. x+V-1
+        T seg[2 * R + 1][V + 2 * R];
+#pragma unroll
+        for (int dy = -R; dy <= R; dy++) {
+          const T *row = po + (size_t)(yl + ry + R + dy) * K::BX + xl + K::PX - R;
+          if (dy == 0) {
+#pragma unroll
+            for (int i = 0; i < V + 2 * R; i++) seg[dy + R][i] = row[i];
+          } else {
+#pragma unroll
+            for (int i = 0; i < V; i++) seg[dy + R][i + R] = row[i + R];
+          }
+        }
+        T out[V];
+#pragma unroll
+        for (int v = 0; v < V; v++) {
+          const int x = x0 + xl + v;
+          auto at = [&](int p) -> T {
+            if (WS::dz(p) != 0 || (WS::dx(p) == 0 && WS::dy(p) == 0)) return col[WS::dz(p) + R][ry][v];
+            return seg[WS::dy(p) + R][v + R + WS::dx(p)];
+          };
+          T a = mul_rn(c.w[0], at(0));
+#pragma unroll
+          for (int p = 1; p < WS::N; p++) a = fma_rn(c.w[p], at(p), a);
+          const bool inner = zin && x >= R && x < nx - R && y >= R && y < ny - R;
+          out[v] = inner ? a : col[R][ry][v];  // frame (reading R1): the input value
+        }
+        if (y < ny) {
+          T *d = dst + ((size_t)o * ny + y) * nx + x0 + xl;
+          if (x0 + xl + V <= nx) vstore<T, V>(d, out);
+          else
+#pragma unroll
+            for (int v = 0; v < V; v++)
+              if (x0 + xl + v < nx) d[v] = out[v];
+        }
+      }
+    }
+    // every warp is done with the slot of arrival k - R (plane o's window) after this barrier:
+    // refill it with arrival k - R + NSL
+    __syncthreads();
+    if (threadIdx.x == 0 && o >= z0 - R) {
+      const unsigned kn = k - R + NSL;  // arrival index of plane q - R + NSL
+      const int qn = q - R + NSL;
+      if (qn < q1) {
+        if (qn >= 0 && qn < nz) {
+          mbar_arrive_tx(bars + kn % NSL, (unsigned)(K::BX * K::BY * sizeof(T)));
+          tma_load_3d(ring + (size_t)(kn % NSL) * K::SLOT, map, x0 - K::PX, y0 - R, qn, bars + kn % NSL);
+        } else {
+          mbar_arrive(bars + kn % NSL);
+        }
+      }
+    }
+  }
+}
+
+template <typename T>
+PERKS_DEVINL void kt3_init(T *&ring, uint64_t *&bars) {
+  extern __shared__ __align__(128) unsigned char kt3_smem[];
+  ring = reinterpret_cast<T *>(kt3_smem);
+  bars = reinterpret_cast<uint64_t *>(kt3_smem + (size_t)KT3<T>::NSL * KT3<T>::SLOT * sizeof(T));
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < KT3<T>::NSL; i++) mbar_init(bars + i, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(KT3_NT, PERKS_W3T_MINB) wide3t_hostloop_kernel(const __grid_constant__ WideMaps3 maps, int src_idx,
+                                                                T *__restrict__ dst, int nx, int ny, int nz, Blocks3 b,
+                                                                int zc, const __grid_constant__ WideCoef3<T> c) {
+  T *ring;
+  uint64_t *bars;
+  kt3_init<T>(ring, bars);
+  const int id = blockIdx.x, z0 = (id / (b.bx * b.by)) * zc;
+  unsigned k = 0;
+  unit3t<T>(&maps.m[src_idx], dst, nx, ny, nz, (id % b.bx) * KT3<T>::TX, ((id / b.bx) % b.by) * KT3_TY, z0,
+            min(z0 + zc, nz), c, ring, bars, k);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(KT3_NT, PERKS_W3T_MINB) wide3t_persistent_kernel(const __grid_constant__ WideMaps3 maps, T *out,
+                                                                  T *tmp, int nx, int ny, int nz, Blocks3 b, int zc,
+                                                                  int64_t steps, unsigned *bar,
+                                                                  const __grid_constant__ WideCoef3<T> c) {
+  T *ring;
+  uint64_t *bars;
+  kt3_init<T>(ring, bars);
+  const int nb = b.bx * b.by * b.bz;
+  unsigned k = 0;
+  for (int64_t t = 0; t < steps; t++) {
+    const int si = t == 0 ? 0 : ((((steps - t) & 1) == 0) ? 1 : 2);
+    T *dst = (((steps - 1 - t) & 1) == 0) ? out : tmp;
+    for (int i = blockIdx.x; i < nb; i += gridDim.x) {  // odd steps in reverse order (zig-zag)
+      const int id = (t & 1) ? nb - 1 - i : i;
+      const int z0 = (id / (b.bx * b.by)) * zc;
+      unit3t<T>(&maps.m[si], dst, nx, ny, nz, (id % b.bx) * KT3<T>::TX, ((id / b.bx) % b.by) * KT3_TY, z0,
+                min(z0 + zc, nz), c, ring, bars, k);
+    }
+    if (t + 1 < steps) {
+      grid_barrier(bar, (unsigned)(t + 1));
+      // the step's outputs were written through the generic proxy; the next step reads them with TMA
+      asm volatile("fence.proxy.async.global;\n" ::: "memory");
+    }
+  }
+}
+
 // ------------------------------------------------------------------ host side
 namespace {
 int radius3d(const Problem &p) {
@@ -244,6 +450,9 @@ template <typename T> WideCoef3<T> make_coef3(const Problem &p) {
   }
   return c;
 }
+template <typename T> void *wk3t(bool hostloop) {
+  return hostloop ? (void *)wide3t_hostloop_kernel<T> : (void *)wide3t_persistent_kernel<T>;
+}
 template <typename T> void *wk3(bool hostloop, int ps) {
   if (hostloop) return ps == 1 ? (void *)wide3_hostloop_kernel<T, 1> : (void *)wide3_hostloop_kernel<T, 0>;
   return ps == 1 ? (void *)wide3_persistent_kernel<T, 1> : (void *)wide3_persistent_kernel<T, 0>;
@@ -263,8 +472,14 @@ Plan plan_wide3d(const Problem &p, perks_variant v) {
   }
   const bool f32 = p.dtype == PERKS_F32, hostloop = v == PERKS_HOSTLOOP;
   const int ps = wide3_preset(p);
-  void *k = f32 ? wk3<float>(hostloop, ps) : wk3<double>(hostloop, ps);
-  const size_t smem = smem3(r, p.elem());
+  // the TMA column kernel for the 3d13pt preset (16-byte aligned rows for the tensor map)
+  const bool tk = ps == 1 && (p.nx * (int64_t)p.elem()) % 16 == 0 && p.nx >= 8 && tma_available() &&
+                  env_int("PERKS_W3_TMA", 1) != 0;
+  void *k = tk ? (f32 ? wk3t<float>(hostloop) : wk3t<double>(hostloop))
+               : (f32 ? wk3<float>(hostloop, ps) : wk3<double>(hostloop, ps));
+  const size_t smem = tk ? (f32 ? KT3<float>::SMEM : KT3<double>::SMEM) : smem3(r, p.elem());
+  const int threads = tk ? KT3_NT : KW3_THREADS;
+  const int TXu = tk ? (f32 ? KT3<float>::TX : KT3<double>::TX) : KW3_TX, TYu = tk ? KT3_TY : KW3_TY;
   if (smem > (size_t)p.max_smem_optin) { pl.why = "wide3d: block does not fit shared memory"; return pl; }
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
     cudaGetLastError();
@@ -274,9 +489,9 @@ Plan plan_wide3d(const Problem &p, perks_variant v) {
   cudaFuncAttributes fa;
   if (cudaFuncGetAttributes(&fa, k) != cudaSuccess) { pl.why = "cudaFuncGetAttributes"; return pl; }
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, KW3_THREADS, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, threads, smem);
   if (occ < 1) { pl.why = "wide3d: not resident"; return pl; }
-  const int bx = (int)((p.nx + KW3_TX - 1) / KW3_TX), by = (int)((p.ny + KW3_TY - 1) / KW3_TY);
+  const int bx = (int)((p.nx + TXu - 1) / TXu), by = (int)((p.ny + TYu - 1) / TYu);
   // z-chunk length: balance the units over the resident CTAs (whole waves) against the 2r-plane
   // re-read per chunk
   const int64_t G = (int64_t)occ * p.num_sms;
@@ -292,20 +507,20 @@ Plan plan_wide3d(const Problem &p, perks_variant v) {
   pl.units = blocks;
   // persistent: every resident CTA, each with an equal share of the planes
   pl.grid = hostloop ? (int)blocks : (int)std::min<int64_t>(blocks, G);
-  pl.block = KW3_THREADS;
+  pl.block = threads;
   pl.ctas_per_sm = occ;
-  pl.tile[0] = KW3_TX; pl.tile[1] = KW3_TY; pl.tile[2] = zc;
+  pl.tile[0] = TXu; pl.tile[1] = TYu; pl.tile[2] = zc;
   pl.regs = fa.numRegs;
   pl.smem = (int)smem;
-  pl.cfg = ps;
+  pl.cfg = tk ? 2 : ps;
   pl.family = 5;  // (wide 3D)
   const double S = (double)p.elem();
   pl.dram_bytes_step = 2.0 * S * (double)p.cells();
   pl.halo_bytes_step = S * (double)blocks *  // window re-reads per unit (L2)
-                       ((double)(KW3_TX + 2 * r) * (KW3_TY + 2 * r) * (zc + 2 * r) - (double)KW3_TX * KW3_TY * zc);
+                       ((double)(TXu + 2 * r) * (TYu + 2 * r) * (zc + 2 * r) - (double)TXu * TYu * zc);
   pl.ws_bytes = align256((size_t)p.cells() * p.elem()) + (hostloop ? 0 : 256);
-  snprintf(pl.name, sizeof(pl.name), "%s3d_wide_r%d_%dpt%s_%s%s", v == PERKS_PERKS ? "perks" : hostloop ? "hostloop" : "persistent",
-           r, p.npts, ps ? "" : "_any", f32 ? "f32" : "f64", v == PERKS_PERKS ? "_c0" : "");
+  snprintf(pl.name, sizeof(pl.name), "%s3d_wide_r%d_%dpt%s_%s%s%s", v == PERKS_PERKS ? "perks" : hostloop ? "hostloop" : "persistent",
+           r, p.npts, ps ? "" : "_any", f32 ? "f32" : "f64", tk ? "_tma" : "", v == PERKS_PERKS ? "_c0" : "");
   pl.ok = true;
   return pl;
 }
@@ -318,8 +533,42 @@ cudaError_t run_wide3_t(const Problem &p, const Plan &pl, const T *in, T *out, v
   int r = radius3d(p);
   int nx = (int)p.nx, ny = (int)p.ny, nz = (int)p.nz;
   int zc = pl.tile[2];
-  Blocks3 b{(nx + KW3_TX - 1) / KW3_TX, (ny + KW3_TY - 1) / KW3_TY, (nz + zc - 1) / zc};
+  Blocks3 b{(nx + pl.tile[0] - 1) / pl.tile[0], (ny + pl.tile[1] - 1) / pl.tile[1], (nz + zc - 1) / zc};
   T *tmp = (T *)ws;
+  if (pl.cfg == 2) {  // TMA column kernel
+    WideMaps3 maps;
+    const void *bs[3] = {in, out, tmp};
+    for (int i = 0; i < 3; i++)
+      if (!encode_map3(&maps.m[i], p, bs[i], KT3<T>::BX, KT3<T>::BY)) return cudaErrorInvalidValue;
+    void *k = wk3t<T>(pl.variant == PERKS_HOSTLOOP);
+    if (pl.variant == PERKS_HOSTLOOP) {
+      for (int64_t t = 0; t < steps; t++) {
+        int si = t == 0 ? 0 : ((((steps - t) & 1) == 0) ? 1 : 2);
+        T *dst = (((steps - 1 - t) & 1) == 0) ? out : tmp;
+        void *args[] = {(void *)&maps, (void *)&si, (void *)&dst, (void *)&nx, (void *)&ny, (void *)&nz, (void *)&b,
+                        (void *)&zc, (void *)&c};
+        cudaError_t e = cudaLaunchKernel(k, dim3(pl.grid), dim3(KT3_NT), args, pl.smem, s);
+        if (e != cudaSuccess) return e;
+      }
+      return cudaSuccess;
+    }
+    unsigned *bar = (unsigned *)((char *)ws + align256((size_t)p.cells() * p.elem()));
+    cudaError_t e = reset_grid_barrier(bar, s);
+    if (e != cudaSuccess) return e;
+    void *args[] = {(void *)&maps, (void *)&out, (void *)&tmp, (void *)&nx, (void *)&ny, (void *)&nz, (void *)&b,
+                    (void *)&zc, (void *)&steps, (void *)&bar, (void *)&c};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(pl.grid);
+    cfg.blockDim = dim3(KT3_NT);
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelExC(&cfg, k, args);
+  }
   void *k = wk3<T>(pl.variant == PERKS_HOSTLOOP, pl.cfg);
   if (pl.variant == PERKS_HOSTLOOP) {
     for (int64_t t = 0; t < steps; t++) {

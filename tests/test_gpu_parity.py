@@ -366,6 +366,25 @@ def test_parity_wide_3d(variant, dtype, shape):
             _check(_run_gpu_offs(u0, offs, w, T, variant), ref, u0, dtype)
 
 
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("dtype,shape", [(np.float64, (30, 40, 130)), (np.float32, (33, 50, 136)),
+                                         (np.float64, (70, 20, 64)), (np.float32, (9, 17, 256))])
+def test_parity_3d13pt_tma_column_kernel(variant, dtype, shape):
+    """The TMA column kernel for Table II 3d13pt (k3d_wide.cu unit3t: tensor-box plane loads,
+    column registers for the z terms): several tiles and z chunks, ragged x/y tiles, bit-exact vs
+    the oracle for every variant (16-byte aligned rows select it)."""
+    _need_gpu()
+    from paper_2204_02064_b200 import Stencil
+    offs, w = si.preset("3d13pt")
+    st = Stencil(shape, offs, w, dtype=dtype)
+    assert "_tma" in st.query(variant)["kernel"]
+    st.close()
+    u0 = si.field(shape, dtype=dtype, seed=1313)
+    for T in (1, 5):
+        ref = oracle.run(u0, offs, w, T, nthreads=8)
+        _check(_run_gpu(u0, "3d13pt", w, T, variant), ref, u0, dtype)
+
+
 @pytest.mark.parametrize("name,shape,dtype,variant", [
     ("2d9pt", (300, 520), np.float32, "persistent"),
     ("3d7pt", (24, 40, 64), np.float64, "persistent"),
