@@ -255,121 +255,128 @@ struct WideMaps3 {
   CUtensorMap m[3];  // in, out, tmp: box {BX, BY, 1}
 };
 
-// One unit: tile (x0, y0), output planes [z0, z1) of one step, src -> dst.  Arrivals q = z0-R ..
-// z1+R-1 (input planes); plane q's own cells enter the column window when it lands; output
-// o = q - R is computed when plane q is resident (its in-plane window is plane o's slot).
-// `k` = running arrival counter (slot = k % NSL, mbarrier parity = (k / NSL) & 1).
-template <typename T>
-__device__ void unit3t(const CUtensorMap *map, T *__restrict__ dst, int nx, int ny, int nz, int x0, int y0, int z0,
-                       int z1, const WideCoef3<T> &c, T *ring, uint64_t *bars, unsigned &k) {
+// The units a CTA runs in one step, as one stream of plane arrivals: unit j (id(j)) = tile
+// (x0, y0), output planes [z0, z1); its arrivals are input planes z0-R .. z1+R-1.  Plane q's own
+// cells enter the column window when it lands; output o = q - R is computed while plane q is
+// resident (its in-plane window is the slot of arrival k - R).  The TMA producer (thread 0) runs
+// NSL arrivals ahead of the consumers ACROSS unit boundaries, so a CTA's next unit is already
+// loading while it finishes the current one (no ring drain/refill per unit).  `k` = running
+// arrival counter over the whole launch (slot = k % NSL, mbarrier parity = (k / NSL) & 1).
+struct Unit3t {
+  int x0, y0, z0, z1;
+};
+template <typename T, class Units>
+__device__ void stream3t(const CUtensorMap *map, T *__restrict__ dst, int nx, int ny, int nz, const Units &units,
+                         int nu, const WideCoef3<T> &c, T *ring, uint64_t *bars, unsigned &k) {
   using K = KT3<T>;
   using WS = WideSet3<1>;
   constexpr int R = K::R, V = K::V, NSL = K::NSL;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int xl = lane * V, yl = w * KT3_RY;  // tile-local first cell
-  const int q0 = z0 - R, q1 = z1 + R;        // arrivals [q0, q1)
-  // prologue: the first min(NSL, arrivals) planes (planes outside [0, nz) are not loaded)
-  if (threadIdx.x == 0)
-    for (int i = 0; i < NSL && q0 + i < q1; i++) {
-      const int q = q0 + i;
-      const unsigned kk = k + i;
-      if (q >= 0 && q < nz) {
-        mbar_arrive_tx(bars + kk % NSL, (unsigned)(K::BX * K::BY * sizeof(T)));
-        tma_load_3d(ring + (size_t)(kk % NSL) * K::SLOT, map, x0 - K::PX, y0 - R, q, bars + kk % NSL);
-      } else {
-        mbar_arrive(bars + kk % NSL);  // empty plane: complete the phase without data
-      }
+  if (nu <= 0) return;
+  // producer cursor (thread 0 only): unit jp, next plane qp
+  int jp = 0, qp = 0;
+  Unit3t up = units(0);
+  qp = up.z0 - R;
+  auto issue_one = [&](unsigned kk) {  // issue the producer cursor's arrival as arrival kk
+    if (jp >= nu) return;
+    if (qp >= 0 && qp < nz) {
+      mbar_arrive_tx(bars + kk % NSL, (unsigned)(K::BX * K::BY * sizeof(T)));
+      tma_load_3d(ring + (size_t)(kk % NSL) * K::SLOT, map, up.x0 - K::PX, up.y0 - R, qp, bars + kk % NSL);
+    } else {
+      mbar_arrive(bars + kk % NSL);  // outside the domain: complete the phase without data
     }
+    if (++qp == up.z1 + R && ++jp < nu) {
+      up = units(jp);
+      qp = up.z0 - R;
+    }
+  };
+  if (threadIdx.x == 0)
+    for (int i = 0; i < NSL; i++) issue_one(k + i);
   T col[2 * R + 1][KT3_RY][V];  // own cells of planes o-R .. o+R (index 2R = newest)
+  unsigned kstart = k;           // first arrival of the current unit
+  for (int j = 0; j < nu; j++) {
+    const Unit3t u = units(j);
+    const int q0 = u.z0 - R, q1 = u.z1 + R;
 #pragma unroll
-  for (int a = 0; a < 2 * R + 1; a++)
-#pragma unroll
-    for (int ry = 0; ry < KT3_RY; ry++)
-#pragma unroll
-      for (int v = 0; v < V; v++) col[a][ry][v] = T(0);
-  for (int q = q0; q < q1; q++, k++) {
-    const unsigned sl = k % NSL;
-    mbar_wait(bars + sl, (k / NSL) & 1);
-    const T *pq = ring + (size_t)sl * K::SLOT;
-    // shift the column window and append plane q's own cells (zero outside the domain's z range)
-#pragma unroll
-    for (int a = 0; a < 2 * R; a++)
+    for (int a = 0; a < 2 * R + 1; a++)
 #pragma unroll
       for (int ry = 0; ry < KT3_RY; ry++)
 #pragma unroll
-        for (int v = 0; v < V; v++) col[a][ry][v] = col[a + 1][ry][v];
-    const bool qin = q >= 0 && q < nz;
+        for (int v = 0; v < V; v++) col[a][ry][v] = T(0);
+    for (int q = q0; q < q1; q++, k++) {
+      const unsigned sl = k % NSL;
+      mbar_wait(bars + sl, (k / NSL) & 1);
+      const T *pq = ring + (size_t)sl * K::SLOT;
 #pragma unroll
-    for (int ry = 0; ry < KT3_RY; ry++) {
-      T own[V];
-      const T *src = pq + (size_t)(yl + ry + R) * K::BX + xl + K::PX;
-      if constexpr ((K::PX * sizeof(T)) % 16 == 0) vload<T, V>(own, src);
-      else
+      for (int a = 0; a < 2 * R; a++)
 #pragma unroll
-        for (int v = 0; v < V; v++) own[v] = src[v];
+        for (int ry = 0; ry < KT3_RY; ry++)
 #pragma unroll
-      for (int v = 0; v < V; v++) col[2 * R][ry][v] = qin ? own[v] : T(0);
-    }
-    const int o = q - R;
-    if (o >= z0) {  // output plane o: in-plane window = the slot of arrival k - R
-      const T *po = ring + (size_t)((k - R) % NSL) * K::SLOT;
-      const bool zin = o >= R && o < nz - R;
+          for (int v = 0; v < V; v++) col[a][ry][v] = col[a + 1][ry][v];
+      const bool qin = q >= 0 && q < nz;
 #pragma unroll
       for (int ry = 0; ry < KT3_RY; ry++) {
-        const int y = y0 + yl + ry;
-        // row segments: centre row x-R .. x+V+R-1, rows y+dy (dy != 0) at x .. x+V-1
-        T seg[2 * R + 1][V + 2 * R];
+        T own[V];
+        const T *src = pq + (size_t)(yl + ry + R) * K::BX + xl + K::PX;
+        if constexpr ((K::PX * sizeof(T)) % 16 == 0) vload<T, V>(own, src);
+        else
 #pragma unroll
-        for (int dy = -R; dy <= R; dy++) {
-          const T *row = po + (size_t)(yl + ry + R + dy) * K::BX + xl + K::PX - R;
-          if (dy == 0) {
+          for (int v = 0; v < V; v++) own[v] = src[v];
 #pragma unroll
-            for (int i = 0; i < V + 2 * R; i++) seg[dy + R][i] = row[i];
-          } else {
+        for (int v = 0; v < V; v++) col[2 * R][ry][v] = qin ? own[v] : T(0);
+      }
+      const int o = q - R;
+      if (o >= u.z0) {  // output plane o: in-plane window = the slot of arrival k - R
+        const T *po = ring + (size_t)((k - R) % NSL) * K::SLOT;
+        const bool zin = o >= R && o < nz - R;
 #pragma unroll
-            for (int i = 0; i < V; i++) seg[dy + R][i + R] = row[i + R];
+        for (int ry = 0; ry < KT3_RY; ry++) {
+          const int y = u.y0 + yl + ry;
+          // row segments: centre row x-R .. x+V+R-1, rows y+dy (dy != 0) at x .. x+V-1
+          T seg[2 * R + 1][V + 2 * R];
+#pragma unroll
+          for (int dy = -R; dy <= R; dy++) {
+            const T *row = po + (size_t)(yl + ry + R + dy) * K::BX + xl + K::PX - R;
+            if (dy == 0) {
+#pragma unroll
+              for (int i = 0; i < V + 2 * R; i++) seg[dy + R][i] = row[i];
+            } else {
+#pragma unroll
+              for (int i = 0; i < V; i++) seg[dy + R][i + R] = row[i + R];
+            }
+          }
+          T out[V];
+#pragma unroll
+          for (int v = 0; v < V; v++) {
+            const int x = u.x0 + xl + v;
+            auto at = [&](int p) -> T {
+              if (WS::dz(p) != 0 || (WS::dx(p) == 0 && WS::dy(p) == 0)) return col[WS::dz(p) + R][ry][v];
+              return seg[WS::dy(p) + R][v + R + WS::dx(p)];
+            };
+            T a = mul_rn(c.w[0], at(0));
+#pragma unroll
+            for (int p = 1; p < WS::N; p++) a = fma_rn(c.w[p], at(p), a);
+            const bool inner = zin && x >= R && x < nx - R && y >= R && y < ny - R;
+            out[v] = inner ? a : col[R][ry][v];  // frame (reading R1): the input value
+          }
+          if (y < ny) {
+            T *d = dst + ((size_t)o * ny + y) * nx + u.x0 + xl;
+            if (u.x0 + xl + V <= nx) vstore<T, V>(d, out);
+            else
+#pragma unroll
+              for (int v = 0; v < V; v++)
+                if (u.x0 + xl + v < nx) d[v] = out[v];
           }
         }
-        T out[V];
-#pragma unroll
-        for (int v = 0; v < V; v++) {
-          const int x = x0 + xl + v;
-          auto at = [&](int p) -> T {
-            if (WS::dz(p) != 0 || (WS::dx(p) == 0 && WS::dy(p) == 0)) return col[WS::dz(p) + R][ry][v];
-            return seg[WS::dy(p) + R][v + R + WS::dx(p)];
-          };
-          T a = mul_rn(c.w[0], at(0));
-#pragma unroll
-          for (int p = 1; p < WS::N; p++) a = fma_rn(c.w[p], at(p), a);
-          const bool inner = zin && x >= R && x < nx - R && y >= R && y < ny - R;
-          out[v] = inner ? a : col[R][ry][v];  // frame (reading R1): the input value
-        }
-        if (y < ny) {
-          T *d = dst + ((size_t)o * ny + y) * nx + x0 + xl;
-          if (x0 + xl + V <= nx) vstore<T, V>(d, out);
-          else
-#pragma unroll
-            for (int v = 0; v < V; v++)
-              if (x0 + xl + v < nx) d[v] = out[v];
-        }
       }
-    }
-    // every warp is done with the slot of arrival k - R (plane o's window) after this barrier:
-    // refill it with arrival k - R + NSL
-    __syncthreads();
-    if (threadIdx.x == 0 && o >= z0 - R) {
-      const unsigned kn = k - R + NSL;  // arrival index of plane q - R + NSL
-      const int qn = q - R + NSL;
-      if (qn < q1) {
-        if (qn >= 0 && qn < nz) {
-          mbar_arrive_tx(bars + kn % NSL, (unsigned)(K::BX * K::BY * sizeof(T)));
-          tma_load_3d(ring + (size_t)(kn % NSL) * K::SLOT, map, x0 - K::PX, y0 - R, qn, bars + kn % NSL);
-        } else {
-          mbar_arrive(bars + kn % NSL);
-        }
-      }
+      // every warp is done with the slot of arrival k - R after this barrier (the window of output
+      // o, or a plane no output of its unit reads): the producer refills it with the next arrival
+      __syncthreads();
+      if (threadIdx.x == 0 && k >= kstart + R) issue_one(k - R + NSL);
     }
   }
+  (void)kstart;
 }
 
 template <typename T>
@@ -392,9 +399,9 @@ __global__ void __launch_bounds__(KT3_NT, PERKS_W3T_MINB) wide3t_hostloop_kernel
   uint64_t *bars;
   kt3_init<T>(ring, bars);
   const int id = blockIdx.x, z0 = (id / (b.bx * b.by)) * zc;
+  const Unit3t u1{(id % b.bx) * KT3<T>::TX, ((id / b.bx) % b.by) * KT3_TY, z0, min(z0 + zc, nz)};
   unsigned k = 0;
-  unit3t<T>(&maps.m[src_idx], dst, nx, ny, nz, (id % b.bx) * KT3<T>::TX, ((id / b.bx) % b.by) * KT3_TY, z0,
-            min(z0 + zc, nz), c, ring, bars, k);
+  stream3t<T>(&maps.m[src_idx], dst, nx, ny, nz, [&](int) { return u1; }, 1, c, ring, bars, k);
 }
 
 template <typename T>
@@ -410,12 +417,15 @@ __global__ void __launch_bounds__(KT3_NT, PERKS_W3T_MINB) wide3t_persistent_kern
   for (int64_t t = 0; t < steps; t++) {
     const int si = t == 0 ? 0 : ((((steps - t) & 1) == 0) ? 1 : 2);
     T *dst = (((steps - 1 - t) & 1) == 0) ? out : tmp;
-    for (int i = blockIdx.x; i < nb; i += gridDim.x) {  // odd steps in reverse order (zig-zag)
+    // this CTA's units blockIdx.x, +gridDim.x, ...; odd steps in reverse order (zig-zag)
+    const int nu = blockIdx.x < nb ? (nb - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    auto unit = [&](int j) -> Unit3t {
+      const int i = (int)blockIdx.x + j * (int)gridDim.x;
       const int id = (t & 1) ? nb - 1 - i : i;
       const int z0 = (id / (b.bx * b.by)) * zc;
-      unit3t<T>(&maps.m[si], dst, nx, ny, nz, (id % b.bx) * KT3<T>::TX, ((id / b.bx) % b.by) * KT3_TY, z0,
-                min(z0 + zc, nz), c, ring, bars, k);
-    }
+      return Unit3t{(id % b.bx) * KT3<T>::TX, ((id / b.bx) % b.by) * KT3_TY, z0, min(z0 + zc, nz)};
+    };
+    stream3t<T>(&maps.m[si], dst, nx, ny, nz, unit, nu, c, ring, bars, k);
     if (t + 1 < steps) {
       grid_barrier(bar, (unsigned)(t + 1));
       // the step's outputs were written through the generic proxy; the next step reads them with TMA
