@@ -116,8 +116,10 @@ perks_status perks_cg_solve(perks_cg_t h, perks_variant variant, perks_cg_policy
                             double *d_rr_history, int64_t *d_info, void *d_workspace,
                             size_t workspace_bytes, void *stream);
 
-/* End-to-end: host b in, host x (and nullable host history / info) out; allocates device
- * buffers, copies, solves, copies back, synchronises.  Blocking. */
+/* End-to-end: host b in, host x (and nullable host history / info) out: copies b to device
+ * scratch, solves, copies back, synchronises.  Blocking.  The device scratch and a private stream
+ * are kept in the handle across calls (grown on demand, freed by destroy); calls on one handle
+ * are serialised. */
 perks_status perks_cg_solve_host(perks_cg_t h, perks_variant variant, perks_cg_policy policy,
                                  const void *h_b, void *h_x, int64_t k_max, double tol,
                                  double *h_rr_history, int64_t *h_info);

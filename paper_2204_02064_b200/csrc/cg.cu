@@ -832,6 +832,10 @@ struct perks_cg_s {
   unsigned char *d_tiles = nullptr;
   int *d_ctile = nullptr, *d_crow = nullptr;
   std::mutex mu;
+  // solve_host scratch (device buffers + stream), kept across calls, grown on demand
+  char *hbuf = nullptr;
+  size_t hbuf_bytes = 0;
+  cudaStream_t hstream = nullptr;
   size_t elem() const { return dtype == PERKS_F64 ? 8 : 4; }
 };
 
@@ -1205,14 +1209,21 @@ perks_status perks_cg_solve_host(perks_cg_t h, perks_variant v, perks_cg_policy 
   const size_t vb = (size_t)std::max<int64_t>(h->n, 1) * h->elem();
   const size_t wsb = ws_layout(h).ws_bytes;
   const size_t hb = (size_t)(kmax + 1) * 8;
-  char *buf = nullptr;
   const size_t ob_b = 0, ob_x = align256(vb), ob_h = 2 * align256(vb), ob_i = ob_h + align256(hb),
                ob_w = ob_i + 256, total = ob_w + wsb;
-  cudaError_t e = cudaMalloc(&buf, total);
-  if (e != cudaSuccess) return cg_cuda_fail(e);
-  cudaStream_t s = nullptr;
+  cudaError_t e = cudaSuccess;
+  if (h->hbuf_bytes < total) {  // grow the cached device scratch
+    if (h->hbuf) cudaFree(h->hbuf);
+    h->hbuf = nullptr;
+    h->hbuf_bytes = 0;
+    if ((e = cudaMalloc(&h->hbuf, total)) != cudaSuccess) return cg_cuda_fail(e);
+    h->hbuf_bytes = total;
+  }
+  if (!h->hstream && (e = cudaStreamCreateWithFlags(&h->hstream, cudaStreamNonBlocking)) != cudaSuccess)
+    return cg_cuda_fail(e);
+  char *buf = h->hbuf;
+  cudaStream_t s = h->hstream;
   perks_status st = PERKS_OK;
-  if ((e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) != cudaSuccess) { cudaFree(buf); return cg_cuda_fail(e); }
   if (h->n > 0) e = cudaMemcpyAsync(buf + ob_b, h_b, h->n * h->elem(), cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) {
     st = perks_cg_solve(h, v, pol, buf + ob_b, buf + ob_x, kmax, tol, reinterpret_cast<double *>(buf + ob_h),
@@ -1221,12 +1232,11 @@ perks_status perks_cg_solve_host(perks_cg_t h, perks_variant v, perks_cg_policy 
       if (h->n > 0) e = cudaMemcpyAsync(h_x, buf + ob_x, h->n * h->elem(), cudaMemcpyDeviceToHost, s);
       if (e == cudaSuccess && h_hist) e = cudaMemcpyAsync(h_hist, buf + ob_h, hb, cudaMemcpyDeviceToHost, s);
       if (e == cudaSuccess && h_info) e = cudaMemcpyAsync(h_info, buf + ob_i, 16, cudaMemcpyDeviceToHost, s);
-      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     }
   }
-  cudaStreamDestroy(s);
-  cudaFree(buf);
+  const cudaError_t es = cudaStreamSynchronize(s);
   if (st != PERKS_OK) return st;
+  if (e == cudaSuccess) e = es;
   return e == cudaSuccess ? PERKS_OK : cg_cuda_fail(e);
 }
 
@@ -1282,6 +1292,8 @@ perks_status perks_cg_destroy(perks_cg_t h) {
   {
     DevGuard g(h->device);
     cudaFree(h->d_mem);
+    if (h->hbuf) cudaFree(h->hbuf);
+    if (h->hstream) cudaStreamDestroy(h->hstream);
   }
   delete h;
   return PERKS_OK;
