@@ -102,8 +102,11 @@ class CG:
             history = torch.full((int(kmax) + 1,), float("nan"), dtype=torch.float64, device=dev)
         if info is None:
             info = torch.zeros(2, dtype=torch.int64, device=dev)
-        if history.numel() < kmax + 1 or history.dtype != torch.float64 or info.dtype != torch.int64:
-            raise ValueError("history must hold kmax+1 float64, info 2 int64")
+        if (history.numel() < kmax + 1 or history.dtype != torch.float64 or not history.is_contiguous()
+                or history.device != torch.device(dev)):
+            raise ValueError(f"history must be a contiguous float64 tensor of >= kmax+1 values on {dev}")
+        if info.numel() < 2 or info.dtype != torch.int64 or not info.is_contiguous() or info.device != torch.device(dev):
+            raise ValueError(f"info must be a contiguous int64 tensor of >= 2 values on {dev}")
         ws = self.workspace()
         s = torch.cuda.current_stream(self.device).cuda_stream
         check(lib.perks_cg_solve(self._h, _variant(variant), _policy(policy), ctypes.c_void_p(b.data_ptr()),
