@@ -51,7 +51,9 @@ typedef enum { PERKS_F32 = 0, PERKS_F64 = 1 } perks_dtype;
 
 typedef enum {
   PERKS_BC_FRAME = 0,    /* Dirichlet frame of width r (hot path)                               */
-  PERKS_BC_PERIODIC = 1  /* wrap-around; accepted by create, UNSUPPORTED by the GPU variants    */
+  PERKS_BC_PERIODIC = 1  /* wrap-around (R1): single GPU, the general kernels (2D radius
+                            <= 6, 3D radius <= 3); PERKS runs the persistent body with an empty
+                            cache split; UNSUPPORTED for multi-GPU slabs                        */
 } perks_bc;
 
 typedef enum {

@@ -251,8 +251,11 @@ static perks_status create_impl(const perks_stencil_desc *d, int device, int ran
     if (d->extent[a] < 2 * r + 1) return PERKS_ERR_INVALID_DOMAIN;
   for (int a = 0; a < 3; a++)
     if (d->extent[a] > (int64_t)1 << 30) return PERKS_ERR_UNSUPPORTED;
-  if (d->bc != PERKS_BC_FRAME) return PERKS_ERR_UNSUPPORTED;  // GPU kernels: FRAME only
-  int shape = find_shape(d->ndim, d->offsets, d->npoints);
+  // PERIODIC (reading R1's alternative): single GPU, the general kernels of k2d_wide.cu /
+  // k3d_wide.cu (wrapped tile and plane loads); slabs keep the FRAME boundary
+  const bool periodic = d->bc == PERKS_BC_PERIODIC;
+  if (periodic && nranks > 1) return PERKS_ERR_UNSUPPORTED;
+  int shape = periodic ? -1 : find_shape(d->ndim, d->offsets, d->npoints);
   // 2D point sets without a specialised kernel (radius > 1, or another order / set): the general
   // kernels of k2d_wide.cu (radius <= 6)
   if (shape < 0 && d->ndim == 2 && r <= 6) shape = SHAPE_G2D;

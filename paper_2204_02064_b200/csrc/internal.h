@@ -52,6 +52,7 @@ struct Plan {
   int nc = 0;                 // 3D PERKS: shared-memory plane slots per CTA
   int ntm = 0, tcols = 0;     // 3D PERKS: TMEM planes per CTA, TMEM columns allocated per CTA
   int wsg = 0;                // 3D persistent: warp-specialised geometry (k3d_stream.cu)
+  bool persistent_body = false;  // a PERKS plan that runs the persistent kernel (empty cache split)
   int64_t cached_reg = 0, cached_smem = 0, cached_tmem = 0;
   double dram_bytes_step = 0, halo_bytes_step = 0;
   size_t ws_bytes = 0;

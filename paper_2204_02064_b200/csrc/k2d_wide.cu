@@ -30,6 +30,7 @@ constexpr int KW_MAXR = 6;
 
 template <typename T> struct WideCoef {
   int n;
+  int per;  // PERKS_BC_PERIODIC: indices wrap, every cell is updated (reading R1's alternative)
   int8_t dx[kMaxPoints2D], dy[kMaxPoints2D];
   T w[kMaxPoints2D];
 };
@@ -60,14 +61,18 @@ template <typename T> struct WideGeo {
 };
 
 // Load the tile at (x0, y0) with its r-wide ring from src into s (pitch P = TX + 2r); cells
-// outside the domain read as 0 (they only feed frame cells).
+// outside the domain read as 0 (they only feed frame cells), or wrap around (PERIODIC).
 template <typename T>
 __device__ void load_tile(const T *__restrict__ src, int nx, int ny, int x0, int y0, int TX, int TY, int r,
-                          T *s) {
+                          T *s, bool per) {
   const int P = TX + 2 * r, H = TY + 2 * r;
   for (int i = threadIdx.x; i < P * H; i += blockDim.x) {
     const int ly = i / P, lx = i % P;
-    const int x = x0 - r + lx, y = y0 - r + ly;
+    int x = x0 - r + lx, y = y0 - r + ly;
+    if (per) {
+      x = x < 0 ? x + nx : (x >= nx ? x - nx : x);  // r < extent: one wrap suffices
+      y = y < 0 ? y + ny : (y >= ny ? y - ny : y);
+    }
     s[i] = (x >= 0 && x < nx && y >= 0 && y < ny) ? __ldcg(src + (size_t)y * nx + x) : T(0);
   }
 }
@@ -79,7 +84,7 @@ __device__ __forceinline__ T cell_update(const T *s, int P, int r, int lx, int l
                                          const WideCoef<T> &c) {
   if constexpr (PS == 0) {
     const T *ctr = s + (ly + r) * P + (lx + r);
-    if (x < r || x >= nx - r || y < r || y >= ny - r) return *ctr;
+    if (!c.per && (x < r || x >= nx - r || y < r || y >= ny - r)) return *ctr;
     T acc = mul_rn(c.w[0], ctr[c.dy[0] * P + c.dx[0]]);
     for (int p = 1; p < c.n; p++) acc = fma_rn(c.w[p], ctr[c.dy[p] * P + c.dx[p]], acc);
     return acc;
@@ -87,7 +92,7 @@ __device__ __forceinline__ T cell_update(const T *s, int P, int r, int lx, int l
     using WS = WideSet<PS>;
     constexpr int R = WS::R, PC = TX + 2 * R;  // compile-time radius and pitch
     const T *ctr = s + (ly + R) * PC + (lx + R);
-    if (x < R || x >= nx - R || y < R || y >= ny - R) return *ctr;
+    if (!c.per && (x < R || x >= nx - R || y < R || y >= ny - R)) return *ctr;
     T acc = mul_rn(c.w[0], ctr[WS::dy(0) * PC + WS::dx(0)]);
 #pragma unroll
     for (int p = 1; p < WS::N; p++) acc = fma_rn(c.w[p], ctr[WS::dy(p) * PC + WS::dx(p)], acc);
@@ -115,7 +120,7 @@ __global__ void __launch_bounds__(KW_THREADS) wide_hostloop_kernel(const T *__re
   T *s = reinterpret_cast<T *>(kw_smem);
   constexpr int TX = WideGeo<T>::TXS, TY = WideGeo<T>::TYS;
   const int x0 = (blockIdx.x % ntx) * TX, y0 = (blockIdx.x / ntx) * TY;
-  load_tile(src, nx, ny, x0, y0, TX, TY, r, s);
+  load_tile(src, nx, ny, x0, y0, TX, TY, r, s, c.per != 0);
   __syncthreads();
   tile_step<T, PS, TX, TY>(s, dst, nx, ny, x0, y0, r, c);
 }
@@ -133,7 +138,7 @@ __global__ void __launch_bounds__(KW_THREADS) wide_persistent_kernel(const T *__
     T *dst = (((steps - 1 - t) & 1) == 0) ? out : tmp;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const int x0 = (tile % ntx) * TX, y0 = (tile / ntx) * TY;
-      load_tile(src, nx, ny, x0, y0, TX, TY, r, s);
+      load_tile(src, nx, ny, x0, y0, TX, TY, r, s, c.per != 0);
       __syncthreads();
       tile_step<T, PS, TX, TY>(s, dst, nx, ny, x0, y0, r, c);
       __syncthreads();
@@ -220,7 +225,7 @@ __global__ void __launch_bounds__(KW_THREADS_P, 1) wide_perks_kernel(const T *__
   };
 
   // ---- prologue: tile (and ring) from `in`; publish x^0's strips (tag 1, parity 0)
-  load_tile(in, nx, ny, x0, y0, TX, TY, r, buf[0]);
+  load_tile(in, nx, ny, x0, y0, TX, TY, r, buf[0], false);  // (FRAME only)
   __syncthreads();
   publish(buf[0], 0, 1u);
   int cur = 0;
@@ -257,6 +262,7 @@ int radius2d(const Problem &p) {
 }
 template <typename T> WideCoef<T> make_coef(const Problem &p) {
   WideCoef<T> c{};
+  c.per = p.bc == PERKS_BC_PERIODIC ? 1 : 0;
   c.n = p.npts;
   for (int i = 0; i < p.npts; i++) {
     c.dx[i] = (int8_t)p.off[i][0];
@@ -308,9 +314,21 @@ Plan plan_wide2d(const Problem &p, perks_variant v) {
   Plan pl;
   pl.variant = v;
   const int r = radius2d(p);
-  if (p.ndim != 2 || p.shape != SHAPE_G2D || p.bc != PERKS_BC_FRAME || r > KW_MAXR || p.npts > kMaxPoints2D) {
-    pl.why = "wide2d: 2D FRAME point sets of radius <= 6";
+  if (p.ndim != 2 || p.shape != SHAPE_G2D || r > KW_MAXR || p.npts > kMaxPoints2D) {
+    pl.why = "wide2d: 2D point sets of radius <= 6";
     return pl;
+  }
+  if (p.bc == PERKS_BC_PERIODIC && v == PERKS_PERKS) {
+    // PERIODIC: the resident-tile exchange assumes a bounded tile grid; PERKS runs the persistent
+    // body with an empty cache split (as in 3D, §7)
+    Plan q = plan_wide2d(p, PERKS_PERSISTENT);
+    if (q.ok) {
+      q.variant = PERKS_PERKS;
+      q.persistent_body = true;
+      q.cached_smem = 0;
+      snprintf(q.name, sizeof(q.name), "perks2d_wide_r%d_%dpt_%s_per_c0", r, p.npts, p.dtype == PERKS_F32 ? "f32" : "f64");
+    }
+    return q;
   }
   const bool f32 = p.dtype == PERKS_F32;
   const int ps = wide_preset(p);
@@ -366,7 +384,8 @@ template <typename T>
 cudaError_t run_wide_t(const Problem &p, const Plan &pl, const T *in, T *out, void *ws, int64_t steps, cudaStream_t s) {
   const WideCoef<T> c = make_coef<T>(p);
   const int r = radius2d(p);
-  void *k = wk<T>(pl.variant, pl.cfg);
+  const perks_variant kv = pl.persistent_body ? PERKS_PERSISTENT : pl.variant;
+  void *k = wk<T>(kv, pl.cfg);
   const int nx = (int)p.nx, ny = (int)p.ny;
   const int ntx = (nx + pl.tile[0] - 1) / pl.tile[0], nty = (ny + pl.tile[1] - 1) / pl.tile[1];
   if (pl.variant == PERKS_HOSTLOOP) {
@@ -390,7 +409,7 @@ cudaError_t run_wide_t(const Problem &p, const Plan &pl, const T *in, T *out, vo
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  if (pl.variant == PERKS_PERSISTENT) {
+  if (kv == PERKS_PERSISTENT) {
     T *tmp = (T *)ws;
     unsigned *bar = (unsigned *)((char *)ws + align256((size_t)p.cells() * p.elem()));
     cudaError_t e = reset_grid_barrier(bar, s);

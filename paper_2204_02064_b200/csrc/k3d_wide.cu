@@ -36,6 +36,7 @@ constexpr int KW3_LA = PERKS_W3_LA;
 
 template <typename T> struct WideCoef3 {
   int n;
+  int per;  // PERKS_BC_PERIODIC: indices wrap, every cell is updated (reading R1's alternative)
   int8_t dx[kMaxPoints2D], dy[kMaxPoints2D], dz[kMaxPoints2D];
   T w[kMaxPoints2D];
 };
@@ -71,22 +72,29 @@ struct PlaneCopy {
   int sidx[KW3_CPT];
   int gxy[KW3_CPT];  // -1: outside the x-y domain or beyond the window
 };
-PERKS_DEVINL PlaneCopy plane_copy(int nx, int ny, int x0, int y0, int r) {
+PERKS_DEVINL PlaneCopy plane_copy(int nx, int ny, int x0, int y0, int r, bool per) {
   const int PX = KW3_TX + 2 * r, PXY = PX * (KW3_TY + 2 * r);
   PlaneCopy pc;
 #pragma unroll
   for (int k = 0; k < KW3_CPT; k++) {
     const int i = threadIdx.x + k * KW3_THREADS;
     const int ly = i / PX, lx = i - ly * PX;
-    const int x = x0 - r + lx, y = y0 - r + ly;
+    int x = x0 - r + lx, y = y0 - r + ly;
+    if (per) {  // r < extent: one wrap suffices
+      x = x < 0 ? x + nx : (x >= nx ? x - nx : x);
+      y = y < 0 ? y + ny : (y >= ny ? y - ny : y);
+    }
     pc.sidx[k] = i;
     pc.gxy[k] = (i < PXY && x >= 0 && x < nx && y >= 0 && y < ny) ? y * nx + x : (i < PXY ? -1 : -2);
   }
   return pc;
 }
-// Issue the cp.async copies of input plane z into s (one commit group); zero outside the domain.
+// Issue the cp.async copies of input plane z into s (one commit group); zero outside the domain
+// (FRAME), or plane z mod nz (PERIODIC).
 template <typename T>
-PERKS_DEVINL void load_plane3(const T *__restrict__ src, T *s, const PlaneCopy &pc, int nx, int ny, int nz, int z) {
+PERKS_DEVINL void load_plane3(const T *__restrict__ src, T *s, const PlaneCopy &pc, int nx, int ny, int nz, int z,
+                              bool per) {
+  if (per) z = z < 0 ? z + nz : (z >= nz ? z - nz : z);
   const bool zok = z >= 0 && z < nz;
   const T *pz = src + (size_t)(zok ? z : 0) * nx * ny;
 #pragma unroll
@@ -110,11 +118,12 @@ __device__ void unit3(const T *__restrict__ src, T *__restrict__ dst, int nx, in
   const bool own = x < nx && y < ny;
   const bool inner_xy = x >= r && x < nx - r && y >= r && y < ny - r;
   const int cell = (ly + r) * PX + (lx + r);  // this thread's centre within a plane
-  const PlaneCopy pc = plane_copy(nx, ny, x0, y0, r);
+  const bool per = c.per != 0;
+  const PlaneCopy pc = plane_copy(nx, ny, x0, y0, r, per);
   // ring slot of input plane zz: (zz - (z0 - r)) mod NP; planes z0-r .. z0+r+LA-1 first (one
   // commit group each; planes past the chunk's last need are empty groups)
   for (int q = 0; q < 2 * r + KW3_LA; q++) {
-    if (z0 - r + q < z1 + r) load_plane3(src, ring + q * PXY, pc, nx, ny, nz, z0 - r + q);
+    if (z0 - r + q < z1 + r) load_plane3(src, ring + q * PXY, pc, nx, ny, nz, z0 - r + q, per);
     else cp_async_commit();
   }
   __syncthreads();  // the previous unit's last plane is read by every warp before its slots refill
@@ -138,11 +147,11 @@ __device__ void unit3(const T *__restrict__ src, T *__restrict__ dst, int nx, in
     {
       int sn = base + 2 * r + KW3_LA;  // plane z + r + LA -> the slot of plane z - r - 1
       if (sn >= NP) sn -= NP;
-      if (z + r + KW3_LA < z1 + r) load_plane3(src, ring + sn * PXY, pc, nx, ny, nz, z + r + KW3_LA);
+      if (z + r + KW3_LA < z1 + r) load_plane3(src, ring + sn * PXY, pc, nx, ny, nz, z + r + KW3_LA, per);
       else cp_async_commit();
     }
     if (own) {
-      const bool inner = inner_xy && z >= r && z < nz - r;
+      const bool inner = per || (inner_xy && z >= r && z < nz - r);
       int sc = base + r;
       if (sc >= NP) sc -= NP;
       T v;
@@ -452,6 +461,7 @@ int wide3_preset(const Problem &p) {
 template <typename T> WideCoef3<T> make_coef3(const Problem &p) {
   WideCoef3<T> c{};
   c.n = p.npts;
+  c.per = p.bc == PERKS_BC_PERIODIC ? 1 : 0;
   for (int i = 0; i < p.npts; i++) {
     c.dx[i] = (int8_t)p.off[i][0];
     c.dy[i] = (int8_t)p.off[i][1];
@@ -476,14 +486,14 @@ Plan plan_wide3d(const Problem &p, perks_variant v) {
   Plan pl;
   pl.variant = v;
   const int r = radius3d(p);
-  if (p.ndim != 3 || p.shape != SHAPE_G3D || p.bc != PERKS_BC_FRAME || r > KW3_MAXR) {
-    pl.why = "wide3d: 3D FRAME point sets of radius <= 3";
+  if (p.ndim != 3 || p.shape != SHAPE_G3D || r > KW3_MAXR) {
+    pl.why = "wide3d: 3D point sets of radius <= 3";
     return pl;
   }
   const bool f32 = p.dtype == PERKS_F32, hostloop = v == PERKS_HOSTLOOP;
   const int ps = wide3_preset(p);
   // the TMA column kernel for the 3d13pt preset (16-byte aligned rows for the tensor map)
-  const bool tk = ps == 1 && (p.nx * (int64_t)p.elem()) % 16 == 0 && p.nx >= 8 && tma_available() &&
+  const bool tk = ps == 1 && p.bc == PERKS_BC_FRAME && (p.nx * (int64_t)p.elem()) % 16 == 0 && p.nx >= 8 && tma_available() &&
                   env_int("PERKS_W3_TMA", 1) != 0;
   void *k = tk ? (f32 ? wk3t<float>(hostloop) : wk3t<double>(hostloop))
                : (f32 ? wk3<float>(hostloop, ps) : wk3<double>(hostloop, ps));
@@ -529,8 +539,9 @@ Plan plan_wide3d(const Problem &p, perks_variant v) {
   pl.halo_bytes_step = S * (double)blocks *  // window re-reads per unit (L2)
                        ((double)(TXu + 2 * r) * (TYu + 2 * r) * (zc + 2 * r) - (double)TXu * TYu * zc);
   pl.ws_bytes = align256((size_t)p.cells() * p.elem()) + (hostloop ? 0 : 256);
-  snprintf(pl.name, sizeof(pl.name), "%s3d_wide_r%d_%dpt%s_%s%s%s", v == PERKS_PERKS ? "perks" : hostloop ? "hostloop" : "persistent",
-           r, p.npts, ps ? "" : "_any", f32 ? "f32" : "f64", tk ? "_tma" : "", v == PERKS_PERKS ? "_c0" : "");
+  snprintf(pl.name, sizeof(pl.name), "%s3d_wide_r%d_%dpt%s_%s%s%s%s", v == PERKS_PERKS ? "perks" : hostloop ? "hostloop" : "persistent",
+           r, p.npts, ps ? "" : "_any", f32 ? "f32" : "f64", tk ? "_tma" : "",
+           p.bc == PERKS_BC_PERIODIC ? "_per" : "", v == PERKS_PERKS ? "_c0" : "");
   pl.ok = true;
   return pl;
 }

@@ -71,7 +71,29 @@ def test_create_validation_without_gpu():
     # k2d_wide.cu) / 3 (3D, k3d_wide.cu); beyond that they are unsupported
     assert _create(3, (12, 12, 12), [(0, 0, 4), (0, 0, 0)], [0.5, 0.5]) == "PERKS_ERR_UNSUPPORTED"  # 3D r = 4
     assert _create(2, (20, 20, 1), [(7, 0, 0), (0, 0, 0)], [0.5, 0.5]) == "PERKS_ERR_UNSUPPORTED"  # r = 7
-    assert _create(2, (8, 8, 1), o5, w5, bc=1) == "PERKS_ERR_UNSUPPORTED"      # PERIODIC on GPU
+    # PERIODIC runs on the general kernels (single GPU): the same radius limits apply
+    assert _create(2, (20, 20, 1), [(7, 0, 0), (0, 0, 0)], [0.5, 0.5], bc=1) == "PERKS_ERR_UNSUPPORTED"
+    assert _create(3, (12, 12, 12), [(0, 0, 4), (0, 0, 0)], [0.5, 0.5], bc=1) == "PERKS_ERR_UNSUPPORTED"
+    assert _create(2, (8, 8, 1), o5, w5, bc=2) == "PERKS_ERR_INVALID_ARGUMENT"  # unknown bc
+
+
+def test_periodic_slabs_unsupported_without_gpu():
+    import seeded_inputs as si
+    from paper_2204_02064_b200 import _lib
+    o7, w7 = si.preset("3d7pt")
+    offs = np.ascontiguousarray(np.asarray(o7, dtype=np.int32).reshape(-1, 3))
+    w = np.ascontiguousarray(np.asarray(w7, dtype=np.float64))
+    d = _lib.Desc()
+    d.ndim = 3
+    d.extent[:] = (16, 16, 8)
+    d.npoints = offs.shape[0]
+    d.offsets = offs.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+    d.weights = w.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    d.dtype = 0
+    d.bc = 1
+    h = ctypes.c_void_p()
+    st = _lib.lib.perks_stencil_create_dist(ctypes.byref(d), 0, 0, 2, ctypes.byref(h))
+    assert _lib.STATUS_NAMES[st] == "PERKS_ERR_UNSUPPORTED"
 
 
 def test_null_arguments():
