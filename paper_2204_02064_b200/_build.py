@@ -70,7 +70,7 @@ def spills_in_plane_loops(obj: str, func: str) -> list:
     mbarrier retry stubs follow it) that contains an mbarrier wait.  Spills of loop-invariant state in a prologue or
     in the per-step outer loop cost one access per unit/step and are tolerated; spills in the
     per-plane loop are not (P:859-860 register discipline).  Kernels without such a loop (the 2D
-    kernels) get the strict rule: every spill is reported."""
+    kernels): every spill inside the time loop (a backward branch over >= 256 instructions)."""
     r = subprocess.run(["cuobjdump", "-sass", "-fun", func, obj], capture_output=True, text=True)
     ins = []
     for ln in r.stdout.splitlines():
@@ -90,8 +90,10 @@ def spills_in_plane_loops(obj: str, func: str) -> list:
     hot = [lp for lp in loops if any(lp[0] <= w <= lp[1] for w in waits)
            and sum(1 for a, _ in ins if lp[0] <= a <= lp[1]) >= 32]
     spills = [hex(a) for a, t in ins if re.search(r"\b(LDL|STL)\b", t)]
-    if not hot:  # no mbarrier-paced loop (2D kernels): any spill counts
-        return spills
+    if not hot:  # no mbarrier-paced loop (2D kernels): any spill inside the time loop (a loop of
+        # >= 256 instructions) counts; prologue / epilogue spills run once per launch
+        big = [lp for lp in loops if sum(1 for a, _ in ins if lp[0] <= a <= lp[1]) >= 256]
+        return [a for a in spills if any(lo <= int(a, 16) <= hi for lo, hi in big)]
     inner = [lp for lp in hot if not any(o != lp and lp[0] <= o[0] and o[1] <= lp[1] for o in hot)]
     return [a for a in spills if any(lo <= int(a, 16) <= hi for lo, hi in inner)]
 

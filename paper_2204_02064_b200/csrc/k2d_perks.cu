@@ -19,6 +19,7 @@
 // The compute body is the same FMA chain as the host-loop kernel (reading R5) so results are
 // bit-identical to variants (a) and (b).
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 
 #include "common.cuh"
@@ -26,6 +27,19 @@
 #include "shapes.cuh"
 #include "tmem.cuh"
 
+// timing experiments only (wrong results): skip the halo tag waits / the per-step CTA barrier
+#ifndef PERKS_P2D_XNOWAIT
+#define PERKS_P2D_XNOWAIT 0
+#endif
+#ifndef PERKS_P2D_SUNROLL  // unroll of the shared-memory row loop (0: full; 3 = the window period)
+#define PERKS_P2D_SUNROLL 0
+#endif
+#ifndef PERKS_P2D_XNOHALO
+#define PERKS_P2D_XNOHALO 0
+#endif
+#ifndef PERKS_P2D_XNOBAR
+#define PERKS_P2D_XNOBAR 0
+#endif
 #ifndef PERKS_P2D_HPMIN  // fewest warps per CTA at which every warp takes part in the halo polls
 #define PERKS_P2D_HPMIN 8
 #endif
@@ -74,6 +88,7 @@ PERKS_DEVINL void poll_copy(const LLWord *src, int n, unsigned tag, bool exists,
     const int i = lane + 32 * e;
     if (i < n && !LL<T>::get(src + i * W, tag, val[e])) pending |= 1u << e;
   }
+  if (PERKS_P2D_XNOWAIT) pending = 0;
   if (pending) {
     const unsigned long long t0 = globaltimer_ns();
     while (pending) {
@@ -97,6 +112,27 @@ struct Tiles2 {
   int ntx, nty;
 };
 
+// Sliding-window rows of the compute body.  Scalar: x-1 .. x+V of one row.  Packed (fp32, V = 4,
+// PERKS_FFMA2): the four stride-2 pairs (w0,w2), (w1,w3), (w2,w4), (w3,w5) of w = x-1 .. x+4, so
+// the output pairs (n0,n2) and (n1,n3) take every chain operand as one register pair (an FFMA2
+// per term for two cells; neighbours dx = -1, 0, +1 of (n0,n2) are pairs 0, 1, 2, of (n1,n3)
+// pairs 1, 2, 3).  A cached row is stored in the matching order {v0, v2, v1, v3}.
+template <typename T, int V> struct SWin {
+  T w[V + 2];
+};
+struct PWin {
+  f32x2 p[4];
+};
+// storage order of a cached row <-> natural order (self-inverse)
+template <bool PK, typename T, int V> PERKS_DEVINL void perm_row(const T (&a)[V], T (&b)[V]) {
+  if constexpr (PK) {
+    b[0] = a[0]; b[1] = a[2]; b[2] = a[1]; b[3] = a[3];
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; i++) b[i] = a[i];
+  }
+}
+
 template <typename T, int S, class G>
 __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__ in,
                                                            T *__restrict__ out, LLWord *gslot,
@@ -106,6 +142,12 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
   constexpr int V = G::V, R = G::R, RR = G::RR, RT = G::RT, RS0 = G::RS0, NT = G::NT, TX = G::TX, TY = G::TY;
   constexpr int WX = G::WX, WY = G::WY, ROWW = G::ROWW, NWARP = NT / 32;
   constexpr bool BOX = has_corners<S>();
+  // fully unrolled shared-memory rows: compile-time row offsets (C2: 6.25 -> 5.89 us/step against
+  // an unroll of 3, profiles/r02_c2_ffma2.txt)
+  constexpr int SROW_UNROLL = PERKS_P2D_SUNROLL ? PERKS_P2D_SUNROLL : (G::RS > 1 ? G::RS : 1);
+  // packed-pair body (FFMA2): fp32 with 4 cells per thread-row
+  constexpr bool PK = PERKS_FFMA2 && sizeof(T) == 4 && V == 4 && RR <= 8;  // (16 register rows + pair windows spill)
+  using Win = typename std::conditional<PK, PWin, SWin<T, V>>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T *const sm = reinterpret_cast<T *>(smem_raw);
   // shared-memory map (element offsets):
@@ -234,23 +276,24 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
     for (int r = 0; r < RR; r++) {
       T v[V];
       load_row(r, v);
-#pragma unroll
-      for (int i = 0; i < V; i++) reg[r][i] = v[i];
+      perm_row<PK, T, V>(v, reg[r]);
       publish_row(0, g0, 1u, r, v);
     }
 #pragma unroll
     for (int r = RR; r < RS0; r++) {
-      T v[V];
+      T v[V], sv[V];
       load_row(r, v);
-      tmem_st_row<T, V>(trow(r), v);
+      perm_row<PK, T, V>(v, sv);
+      tmem_st_row<T, V>(trow(r), sv);
       publish_row(0, g0, 1u, r, v);
     }
     if constexpr (RT > 0) tmem_wait_st();
 #pragma unroll 1
     for (int r = RS0; r < R; r++) {
-      T v[V];
+      T v[V], sv[V];
       load_row(r, v);
-      vstore<T, V>(my_smc + (size_t)(r - RS0) * NT * V, v);
+      perm_row<PK, T, V>(v, sv);
+      vstore<T, V>(my_smc + (size_t)(r - RS0) * NT * V, sv);
       publish_row(0, g0, 1u, r, v);
     }
     flush_cols(0, g0, 1u);
@@ -278,7 +321,7 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
     // HP warps per side (all warps take part once there are >= 8): warp w reads segment w / 4 of
     // side w % 4, so the halo phase (and the CTA barrier after it) shortens with the warp count
     constexpr int HP = NWARP >= PERKS_P2D_HPMIN ? NWARP / 4 : 1;
-    for (int sw = warp; sw < 4 * HP; sw += NWARP) {
+    for (int sw = warp; sw < (PERKS_P2D_XNOHALO ? 0 : 4 * HP); sw += NWARP) {
       const int side = sw % 4, part = sw / 4;
       const int ddx = side < 2 ? 0 : (side == 2 ? -1 : 1);
       const int ddy = side < 2 ? (side == 0 ? -1 : 1) : 0;
@@ -320,130 +363,173 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
         }
       }
     }
-    __syncthreads();
+    if (!PERKS_P2D_XNOBAR) __syncthreads();
     // ---- compute x^{t+1} for the thread's V x R cells (sliding window over rows)
     LLWord *gnp = GS(tile, np);
     const unsigned tag_out = (unsigned)(t + 2);
     colL_at = o_colL + (is_l ? np * PAR_COL : 0);
     colR_at = o_colR + (is_r ? np * PAR_COL : 0);
-    T prev[V + 2], cur[V + 2], nxt[V + 2];
-    // own row (old values) + x-neighbours: shuffles inside the warp; lanes 0/31 take the
-    // neighbouring warp's / tile's edge column (broadcast reads, branch free)
-    // the warp-edge column values are loaded one row ahead (rows are widened in order 0, 1, ...,
-    // R-1), so their shared-memory latency is off the row's dependency chain; the load past the
-    // last row reads the neighbouring buffer and is never used
-    T pcl = sm[pc + o_rdL], pcr = sm[pc + o_rdR];
-    auto widen = [&](T (&w)[V + 2], const T (&v)[V], int r) {
-      const T l = __shfl_up_sync(0xffffffffu, v[V - 1], 1);
-      const T rr = __shfl_down_sync(0xffffffffu, v[0], 1);
-      const T cl = pcl, cr = pcr;
-      pcl = sm[pc + o_rdL + r + 1];
-      pcr = sm[pc + o_rdR + r + 1];
-      w[0] = is_l ? cl : l;
-      w[V + 1] = is_r ? cr : rr;
-#pragma unroll
-      for (int i = 0; i < V; i++) w[i + 1] = v[i];
-    };
-    auto halo_below = [&](T (&w)[V + 2]) {
-#pragma unroll
-      for (int i = 0; i < V + 2; i++) w[i] = sm[pr + o_below + i];
-    };
-    // FMA chain (reading R5) + frame select + publish; rotates the window
-    auto finish_row = [&](int r, T (&nv)[V], bool maybe_edge_row = true) {
-#pragma unroll
-      for (int i = 0; i < V; i++) {
-        T acc;
-#pragma unroll
-        for (int p = 0; p < Shape<S>::N; p++) {
-          const int dy = Shape<S>::dy(p), dx = Shape<S>::dx(p);
-          const T val = dy < 0 ? prev[i + 1 + dx] : (dy > 0 ? nxt[i + 1 + dx] : cur[i + 1 + dx]);
-          acc = (p == 0) ? mul_rn(c.w[0], val) : fma_rn(c.w[p], val, acc);
+    // the sweep, instantiated with and without the frame selects: a warp owns frame cells or
+    // not for the whole run, so the test is one uniform branch per step instead of one per row
+    // (which also cost register-merge moves after every row)
+    auto sweep = [&](auto frame_c) {
+      constexpr bool FR = decltype(frame_c)::value;
+      Win prev, cur, nxt;
+      // own row (old values, storage order) + x-neighbours: shuffles inside the warp; lanes 0/31
+      // take the neighbouring warp's / tile's edge column (broadcast reads, branch free)
+      // the warp-edge column values are loaded one row ahead (rows are widened in order 0, 1, ...,
+      // R-1), so their shared-memory latency is off the row's dependency chain; the load past the
+      // last row reads the neighbouring buffer and is never used
+      T pcl = sm[pc + o_rdL], pcr = sm[pc + o_rdR];
+      auto widen = [&](Win &w, const T (&v)[V], int r) {
+        T n[V];
+        perm_row<PK, T, V>(v, n);  // natural order
+        const T l = __shfl_up_sync(0xffffffffu, n[V - 1], 1);
+        const T rr = __shfl_down_sync(0xffffffffu, n[0], 1);
+        const T cl = pcl, cr = pcr;
+        pcl = sm[pc + o_rdL + r + 1];
+        pcr = sm[pc + o_rdR + r + 1];
+        const T left = is_l ? cl : l, right = is_r ? cr : rr;
+        if constexpr (PK) {
+          w.p[0] = pack2(left, n[1]);
+          w.p[1] = pack2(v[0], v[1]);  // (n0, n2): the stored pair as is
+          w.p[2] = pack2(v[2], v[3]);  // (n1, n3)
+          w.p[3] = pack2(n[2], right);
+        } else {
+          w.w[0] = left;
+          w.w[V + 1] = right;
+  #pragma unroll
+          for (int i = 0; i < V; i++) w.w[i + 1] = n[i];
         }
-        nv[i] = acc;
-      }
-      if (warp_frame) {
-        const bool rin = r >= ylo && r < yhi;
-#pragma unroll
-        for (int i = 0; i < V; i++) nv[i] = (rin && ((xmask >> i) & 1u)) ? nv[i] : cur[i + 1];
-      }
-      publish_row(np, gnp, tag_out, r, nv, maybe_edge_row);
-#pragma unroll
-      for (int i = 0; i < V + 2; i++) {
-        prev[i] = cur[i];
-        cur[i] = nxt[i];
-      }
-    };
-    {
-#pragma unroll
-      for (int i = 0; i < V + 2; i++) prev[i] = sm[pr + o_above + i];  // x = xr-1 .. xr+V
-      T v[V];
-      if (RR > 0) {
-#pragma unroll
-        for (int i = 0; i < V; i++) v[i] = opaque_copy(reg[0][i]);
-      } else if (RT > 0) {
-        tmem_ld_row<T, V>(trow(0), v);
-      } else {
-        vload<T, V>(v, my_smc);
-      }
-      widen(cur, v, 0);
-    }
-    // the first row of the next tier (TMEM, then shared memory) or the halo below
-    auto next_tier_row = [&](int rn) {
-      if (RT > 0 && rn < RS0) {
+      };
+      // a halo row (x-1 .. x+V) from a shared-memory row buffer
+      auto halo_row = [&](Win &w, int off) {
+        T h[V + 2];
+  #pragma unroll
+        for (int i = 0; i < V + 2; i++) h[i] = sm[off + i];
+        if constexpr (PK) {
+  #pragma unroll
+          for (int j = 0; j < 4; j++) w.p[j] = pack2(h[j], h[j + 2]);
+        } else {
+  #pragma unroll
+          for (int i = 0; i < V + 2; i++) w.w[i] = h[i];
+        }
+      };
+      auto halo_below = [&](Win &w) { halo_row(w, pr + o_below); };
+      // FMA chain (reading R5) + frame select + publish; rotates the window.  ns: the new row in
+      // storage order
+      auto finish_row = [&](int r, T (&ns)[V], bool maybe_edge_row = true) {
+        T nv[V], cv[V];  // natural order: new values, old values (frame cells keep them)
+        if constexpr (PK) {
+          f32x2 A = 0, B = 0;  // cells (0, 2), (1, 3)
+  #pragma unroll
+          for (int p = 0; p < Shape<S>::N; p++) {
+            const int dy = Shape<S>::dy(p), dx = Shape<S>::dx(p);
+            const Win &src = dy < 0 ? prev : (dy > 0 ? nxt : cur);
+            A = (p == 0) ? mul2_rn(c.w[0], src.p[1 + dx]) : fma2_rn(c.w[p], src.p[1 + dx], A);
+            B = (p == 0) ? mul2_rn(c.w[0], src.p[2 + dx]) : fma2_rn(c.w[p], src.p[2 + dx], B);
+          }
+          unpack2(A, nv[0], nv[2]);
+          unpack2(B, nv[1], nv[3]);
+          unpack2(cur.p[1], cv[0], cv[2]);
+          unpack2(cur.p[2], cv[1], cv[3]);
+        } else {
+  #pragma unroll
+          for (int i = 0; i < V; i++) {
+            T acc;
+  #pragma unroll
+            for (int p = 0; p < Shape<S>::N; p++) {
+              const int dy = Shape<S>::dy(p), dx = Shape<S>::dx(p);
+              const T val = dy < 0 ? prev.w[i + 1 + dx] : (dy > 0 ? nxt.w[i + 1 + dx] : cur.w[i + 1 + dx]);
+              acc = (p == 0) ? mul_rn(c.w[0], val) : fma_rn(c.w[p], val, acc);
+            }
+            nv[i] = acc;
+            cv[i] = cur.w[i + 1];
+          }
+        }
+        if constexpr (FR) {
+          const bool rin = r >= ylo && r < yhi;
+  #pragma unroll
+          for (int i = 0; i < V; i++) nv[i] = (rin && ((xmask >> i) & 1u)) ? nv[i] : cv[i];
+        }
+        publish_row(np, gnp, tag_out, r, nv, maybe_edge_row);
+        perm_row<PK, T, V>(nv, ns);
+        prev = cur;
+        cur = nxt;
+      };
+      {
+        halo_row(prev, pr + o_above);  // x = xr-1 .. xr+V
         T v[V];
-        tmem_ld_row<T, V>(trow(rn), v);
-        widen(nxt, v, rn);
-      } else if (RS0 < R) {
-        T v[V];
-        vload<T, V>(v, my_smc + (size_t)(rn - RS0) * NT * V);
-        widen(nxt, v, rn);
-      } else {
-        halo_below(nxt);
+        if (RR > 0) {
+  #pragma unroll
+          for (int i = 0; i < V; i++) v[i] = opaque_copy(reg[0][i]);
+        } else if (RT > 0) {
+          tmem_ld_row<T, V>(trow(0), v);
+        } else {
+          vload<T, V>(v, my_smc);
+        }
+        widen(cur, v, 0);
       }
-    };
-    // rows held in registers: fully unrolled so reg[][] is statically indexed
-#pragma unroll
-    for (int r = 0; r < RR; r++) {
-      if (r + 1 < RR) {
-        T v[V];
-#pragma unroll
-        for (int i = 0; i < V; i++) v[i] = opaque_copy(reg[r + 1 < RR ? r + 1 : 0][i]);
-        widen(nxt, v, r + 1);
-      } else {
-        next_tier_row(r + 1);
-      }
-      T nv[V];
-      finish_row(r, nv);
-#pragma unroll
-      for (int i = 0; i < V; i++) reg[r][i] = nv[i];
-    }
-    // rows held in TMEM: fully unrolled (compile-time column offsets); row r's old values are no
-    // longer needed once row r+1 is in the window, so its new values go straight back
-#pragma unroll
-    for (int r = RR; r < RS0; r++) {
-      next_tier_row(r + 1);
-      T nv[V];
-      finish_row(r, nv);
-      tmem_st_row<T, V>(trow(r), nv);
-    }
-    if constexpr (RT > 0) tmem_wait_st();
-    // rows held in shared memory (sm_cache); unrolled by 3 = the window period; the last row
-    // (which reads the row below the segment) is peeled so the loop body has no row tests
-    if (RS0 < R) {
-#pragma unroll 3
-      for (int r = RS0; r < R - 1; r++) {
-        T v[V];
-        vload<T, V>(v, my_smc + (size_t)(r + 1 - RS0) * NT * V);
-        widen(nxt, v, r + 1);
+      // the first row of the next tier (TMEM, then shared memory) or the halo below
+      auto next_tier_row = [&](int rn) {
+        if (RT > 0 && rn < RS0) {
+          T v[V];
+          tmem_ld_row<T, V>(trow(rn), v);
+          widen(nxt, v, rn);
+        } else if (RS0 < R) {
+          T v[V];
+          vload<T, V>(v, my_smc + (size_t)(rn - RS0) * NT * V);
+          widen(nxt, v, rn);
+        } else {
+          halo_below(nxt);
+        }
+      };
+      // rows held in registers: fully unrolled so reg[][] is statically indexed
+  #pragma unroll
+      for (int r = 0; r < RR; r++) {
+        if (r + 1 < RR) {
+          T v[V];
+  #pragma unroll
+          for (int i = 0; i < V; i++) v[i] = opaque_copy(reg[r + 1 < RR ? r + 1 : 0][i]);
+          widen(nxt, v, r + 1);
+        } else {
+          next_tier_row(r + 1);
+        }
         T nv[V];
-        finish_row(r, nv, RS0 == 0 && r == 0);
-        vstore<T, V>(my_smc + (size_t)(r - RS0) * NT * V, nv);
+        finish_row(r, nv);
+  #pragma unroll
+        for (int i = 0; i < V; i++) reg[r][i] = nv[i];
       }
-      halo_below(nxt);
-      T nv[V];
-      finish_row(R - 1, nv);
-      vstore<T, V>(my_smc + (size_t)(R - 1 - RS0) * NT * V, nv);
-    }
+      // rows held in TMEM: fully unrolled (compile-time column offsets); row r's old values are no
+      // longer needed once row r+1 is in the window, so its new values go straight back
+  #pragma unroll
+      for (int r = RR; r < RS0; r++) {
+        next_tier_row(r + 1);
+        T nv[V];
+        finish_row(r, nv);
+        tmem_st_row<T, V>(trow(r), nv);
+      }
+      if constexpr (RT > 0) tmem_wait_st();
+      // rows held in shared memory (sm_cache); unrolled (SROW_UNROLL); the last row
+      // (which reads the row below the segment) is peeled so the loop body has no row tests
+      if (RS0 < R) {
+  #pragma unroll(SROW_UNROLL)
+        for (int r = RS0; r < R - 1; r++) {
+          T v[V];
+          vload<T, V>(v, my_smc + (size_t)(r + 1 - RS0) * NT * V);
+          widen(nxt, v, r + 1);
+          T nv[V];
+          finish_row(r, nv, RS0 == 0 && r == 0);
+          vstore<T, V>(my_smc + (size_t)(r - RS0) * NT * V, nv);
+        }
+        halo_below(nxt);
+        T nv[V];
+        finish_row(R - 1, nv);
+        vstore<T, V>(my_smc + (size_t)(R - 1 - RS0) * NT * V, nv);
+      }
+    };
+    if (warp_frame) sweep(std::true_type{});
+    else sweep(std::false_type{});
     flush_cols(np, gnp, tag_out);
     // every warp signals "my part of x^{t+1}'s boundary is published": flag = (t+2)*NWARP when the
     // whole tile edge is out.  No CTA barrier here: the next step's halo phase only touches the
@@ -465,18 +551,24 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
     }
   };
 #pragma unroll
-  for (int r = 0; r < RR; r++) store_row(r, reg[r]);
+  for (int r = 0; r < RR; r++) {
+    T n[V];
+    perm_row<PK, T, V>(reg[r], n);
+    store_row(r, n);
+  }
 #pragma unroll
   for (int r = RR; r < RS0; r++) {
-    T v[V];
+    T v[V], n[V];
     tmem_ld_row<T, V>(trow(r), v);
-    store_row(r, v);
+    perm_row<PK, T, V>(v, n);
+    store_row(r, n);
   }
 #pragma unroll 1
   for (int r = RS0; r < R; r++) {
-    T v[V];
+    T v[V], n[V];
     vload<T, V>(v, my_smc + (size_t)(r - RS0) * NT * V);
-    store_row(r, v);
+    perm_row<PK, T, V>(v, n);
+    store_row(r, n);
   }
   if constexpr (RT > 0) {
     tmem_fence_before_sync();
