@@ -31,6 +31,9 @@
 #ifndef PERKS_P2D_XNOWAIT
 #define PERKS_P2D_XNOWAIT 0
 #endif
+#ifndef PERKS_P2D_TPRE  // issue each TMEM row's load one row ahead of its use
+#define PERKS_P2D_TPRE 1
+#endif
 #ifndef PERKS_P2D_SUNROLL  // unroll of the shared-memory row loop (0: full; 3 = the window period)
 #define PERKS_P2D_SUNROLL 0
 #endif
@@ -398,20 +401,20 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
         } else {
           w.w[0] = left;
           w.w[V + 1] = right;
-  #pragma unroll
+#pragma unroll
           for (int i = 0; i < V; i++) w.w[i + 1] = n[i];
         }
       };
       // a halo row (x-1 .. x+V) from a shared-memory row buffer
       auto halo_row = [&](Win &w, int off) {
         T h[V + 2];
-  #pragma unroll
+#pragma unroll
         for (int i = 0; i < V + 2; i++) h[i] = sm[off + i];
         if constexpr (PK) {
-  #pragma unroll
+#pragma unroll
           for (int j = 0; j < 4; j++) w.p[j] = pack2(h[j], h[j + 2]);
         } else {
-  #pragma unroll
+#pragma unroll
           for (int i = 0; i < V + 2; i++) w.w[i] = h[i];
         }
       };
@@ -422,7 +425,7 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
         T nv[V], cv[V];  // natural order: new values, old values (frame cells keep them)
         if constexpr (PK) {
           f32x2 A = 0, B = 0;  // cells (0, 2), (1, 3)
-  #pragma unroll
+#pragma unroll
           for (int p = 0; p < Shape<S>::N; p++) {
             const int dy = Shape<S>::dy(p), dx = Shape<S>::dx(p);
             const Win &src = dy < 0 ? prev : (dy > 0 ? nxt : cur);
@@ -434,10 +437,10 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
           unpack2(cur.p[1], cv[0], cv[2]);
           unpack2(cur.p[2], cv[1], cv[3]);
         } else {
-  #pragma unroll
+#pragma unroll
           for (int i = 0; i < V; i++) {
             T acc;
-  #pragma unroll
+#pragma unroll
             for (int p = 0; p < Shape<S>::N; p++) {
               const int dy = Shape<S>::dy(p), dx = Shape<S>::dx(p);
               const T val = dy < 0 ? prev.w[i + 1 + dx] : (dy > 0 ? nxt.w[i + 1 + dx] : cur.w[i + 1 + dx]);
@@ -449,7 +452,7 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
         }
         if constexpr (FR) {
           const bool rin = r >= ylo && r < yhi;
-  #pragma unroll
+#pragma unroll
           for (int i = 0; i < V; i++) nv[i] = (rin && ((xmask >> i) & 1u)) ? nv[i] : cv[i];
         }
         publish_row(np, gnp, tag_out, r, nv, maybe_edge_row);
@@ -457,14 +460,25 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
         prev = cur;
         cur = nxt;
       };
+      // the TMEM row in flight: row rn + 1 is issued as soon as row rn is taken (PERKS_P2D_TPRE)
+      TmemRowInFlight<T, V> tpre;
+      if constexpr (RT > 0 && PERKS_P2D_TPRE) tpre.issue(trow(RR));
+      auto tmem_row = [&](int rn, T (&v)[V]) {
+        if constexpr (PERKS_P2D_TPRE) {
+          tpre.take(v);
+          if (rn + 1 < RS0) tpre.issue(trow(rn + 1));
+        } else {
+          tmem_ld_row<T, V>(trow(rn), v);
+        }
+      };
       {
         halo_row(prev, pr + o_above);  // x = xr-1 .. xr+V
         T v[V];
         if (RR > 0) {
-  #pragma unroll
+#pragma unroll
           for (int i = 0; i < V; i++) v[i] = opaque_copy(reg[0][i]);
         } else if (RT > 0) {
-          tmem_ld_row<T, V>(trow(0), v);
+          tmem_row(0, v);
         } else {
           vload<T, V>(v, my_smc);
         }
@@ -474,7 +488,7 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
       auto next_tier_row = [&](int rn) {
         if (RT > 0 && rn < RS0) {
           T v[V];
-          tmem_ld_row<T, V>(trow(rn), v);
+          tmem_row(rn, v);
           widen(nxt, v, rn);
         } else if (RS0 < R) {
           T v[V];
@@ -485,11 +499,11 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
         }
       };
       // rows held in registers: fully unrolled so reg[][] is statically indexed
-  #pragma unroll
+#pragma unroll
       for (int r = 0; r < RR; r++) {
         if (r + 1 < RR) {
           T v[V];
-  #pragma unroll
+#pragma unroll
           for (int i = 0; i < V; i++) v[i] = opaque_copy(reg[r + 1 < RR ? r + 1 : 0][i]);
           widen(nxt, v, r + 1);
         } else {
@@ -497,12 +511,12 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
         }
         T nv[V];
         finish_row(r, nv);
-  #pragma unroll
+#pragma unroll
         for (int i = 0; i < V; i++) reg[r][i] = nv[i];
       }
       // rows held in TMEM: fully unrolled (compile-time column offsets); row r's old values are no
       // longer needed once row r+1 is in the window, so its new values go straight back
-  #pragma unroll
+#pragma unroll
       for (int r = RR; r < RS0; r++) {
         next_tier_row(r + 1);
         T nv[V];
@@ -513,7 +527,7 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
       // rows held in shared memory (sm_cache); unrolled (SROW_UNROLL); the last row
       // (which reads the row below the segment) is peeled so the loop body has no row tests
       if (RS0 < R) {
-  #pragma unroll(SROW_UNROLL)
+#pragma unroll(SROW_UNROLL)
         for (int r = RS0; r < R - 1; r++) {
           T v[V];
           vload<T, V>(v, my_smc + (size_t)(r + 1 - RS0) * NT * V);

@@ -109,6 +109,39 @@ template <typename T, int V> PERKS_DEVINL void tmem_ld_row(uint32_t taddr, T (&v
   }
 }
 
+// A row segment load split in two: issue (tcgen05.ld, no wait) and take (tcgen05.wait::ld with the
+// in-flight words as in/out operands, so nothing reads them earlier), so one row's load latency
+// overlaps the previous row's arithmetic.  At most one issued row may be outstanding (the wait
+// covers every earlier load of the thread).
+template <typename T, int V> struct TmemRowInFlight {
+  static constexpr int WPR = V * (int)sizeof(T) / 4;
+  static_assert(WPR == 4 || WPR == 8, "16- or 32-byte segments");
+  uint32_t w[WPR];
+  PERKS_DEVINL void issue(uint32_t taddr) {
+#pragma unroll
+    for (int g = 0; g < WPR / 4; g++)
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
+                   : "=r"(w[4 * g]), "=r"(w[4 * g + 1]), "=r"(w[4 * g + 2]), "=r"(w[4 * g + 3])
+                   : "r"(taddr + 4 * g));
+  }
+  PERKS_DEVINL void take(T (&v)[V]) {
+    if constexpr (WPR == 4) {
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" : "+r"(w[0]), "+r"(w[1]), "+r"(w[2]), "+r"(w[3]));
+    } else {
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+                   : "+r"(w[0]), "+r"(w[1]), "+r"(w[2]), "+r"(w[3]), "+r"(w[4]), "+r"(w[5]), "+r"(w[6]), "+r"(w[7]));
+    }
+    if constexpr (sizeof(T) == 4) {
+#pragma unroll
+      for (int i = 0; i < V; i++) v[i] = (T)__uint_as_float(w[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < V; i++)
+        v[i] = (T)__longlong_as_double((long long)((unsigned long long)w[2 * i] | ((unsigned long long)w[2 * i + 1] << 32)));
+    }
+  }
+};
+
 // tcgen05.wait::ld with the loaded registers as in/out operands (the load's destination registers
 // are undefined until the wait completes).
 PERKS_DEVINL void tmem_wait_ld_dep(uint32_t (&r)[8]) {
