@@ -255,7 +255,7 @@ def run_nccl_slab(args):
             holder["ws"] = st.workspace("hostloop")
         st.run(src, 1, "hostloop", out=dst, workspace=holder["ws"])
 
-    sl = NcclSlabHostLoop(nzg, ny, nx, radius, rank, ws, step, empty)
+    sl = NcclSlabHostLoop((nzg, ny, nx), radius, rank, ws, step, empty)
     sl.load(si.field_torch((sl.nz, ny, nx), c["np_dtype"], dev, index_offset=sl.z0 * ny * nx))
     sl.run(1)
     for _ in range(args.warmup):

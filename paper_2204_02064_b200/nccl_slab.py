@@ -1,6 +1,7 @@
-"""The multi-GPU host-loop baseline of SURVEY §8(e)(a): z-slabs, halo planes exchanged every step by
-NCCL send/recv (torch.distributed point-to-point on the "nccl" backend), one host-loop stencil
-step per time step through the C ABI.
+"""The multi-GPU host-loop baseline of SURVEY §8(e)(a): slabs along the slowest axis (z in 3D, y in
+2D, SURVEY §8(b) "global z split evenly; y for 2D"), halo planes / rows exchanged every step by NCCL
+send/recv (torch.distributed point-to-point on the "nccl" backend), one host-loop stencil step per
+time step through the C ABI.
 
 This is the baseline the in-kernel exchange of the persistent / PERKS slab path (csrc/dist.cuh,
 ``Stencil(..., rank, nranks)``) is measured against.  Layout: rank r owns global planes
@@ -25,22 +26,26 @@ from .dist import slab_bounds
 
 
 class NcclSlabHostLoop:
-    """One rank of a z-slab decomposition with per-step halo send/recv.
+    """One rank of a slab decomposition along axis 0 (z of [nz][ny][nx], y of [ny][nx]) with
+    per-step halo send/recv.
 
-    step(src, dst): advance the extended slab ``src`` by one time step into ``dst`` (same shape,
-    [nz_ext][ny][nx]); on GPU a ``Stencil(...).run(src, 1, "hostloop", out=dst)``.
+    global_shape: (nz, ny, nx) or (ny, nx).  step(src, dst): advance the extended slab ``src`` by
+    one time step into ``dst`` (same shape); on GPU a ``Stencil(...).run(src, 1, "hostloop",
+    out=dst)``.  z0/z1/nz name the slab's range along axis 0 in either case.
     """
 
-    def __init__(self, nz_global: int, ny: int, nx: int, radius: int, rank: int, nranks: int,
-                 step, empty, group=None):
+    def __init__(self, global_shape, radius: int, rank: int, nranks: int, step, empty, group=None):
+        global_shape = tuple(int(v) for v in global_shape)
+        if len(global_shape) not in (2, 3):
+            raise ValueError("global_shape must be (nz, ny, nx) or (ny, nx)")
         self.rank, self.nranks, self.h = int(rank), int(nranks), int(radius)
-        self.z0, self.z1 = slab_bounds(nz_global, nranks, rank)
+        self.z0, self.z1 = slab_bounds(global_shape[0], nranks, rank)
         self.nz = self.z1 - self.z0
         if self.nz < self.h:
             raise ValueError("slab thinner than the stencil radius")
         self.lo = self.h if rank > 0 else 0
         self.hi = self.h if rank < nranks - 1 else 0
-        self.shape = (self.lo + self.nz + self.hi, ny, nx)
+        self.shape = (self.lo + self.nz + self.hi,) + global_shape[1:]
         self.step = step
         self.group = group
         self.a = empty(self.shape)
@@ -58,8 +63,8 @@ class NcclSlabHostLoop:
     def exchange(self, buf):
         """Halo planes of ``buf`` from the neighbours: one batch of point-to-point sends and
         receives (ncclGroupStart / ncclSend / ncclRecv / ncclGroupEnd on the nccl backend).
-        Slices along z of a C-order slab are contiguous, so planes go straight from / into the
-        extended buffer."""
+        Slices along axis 0 of a C-order slab are contiguous, so planes (rows in 2D) go straight from
+        / into the extended buffer."""
         import torch.distributed as dist
 
         ops = []

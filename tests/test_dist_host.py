@@ -80,13 +80,12 @@ def _nccl_slab_worker(rank, world, port, q, name, shape, steps):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     offs, w = si.preset(name)
     r = max(max(abs(v) for v in o) for o in offs)
-    nz, ny, nx = shape
     u0 = si.field(shape, dtype=np.float64)
 
     def step(src, dst):
         dst.copy_(torch.from_numpy(oracle.run(src.numpy(), offs, w, 1)))
 
-    sl = NcclSlabHostLoop(nz, ny, nx, r, rank, world, step, lambda s: torch.zeros(s, dtype=torch.float64))
+    sl = NcclSlabHostLoop(shape, r, rank, world, step, lambda s: torch.zeros(s, dtype=torch.float64))
     sl.load(torch.from_numpy(u0[sl.z0:sl.z1]))
     out = sl.run(steps).numpy().copy()
     q.put((rank, sl.z0, sl.z1, out))
@@ -95,7 +94,10 @@ def _nccl_slab_worker(rank, world, port, q, name, shape, steps):
 
 
 @pytest.mark.parametrize("world,name,shape,steps", [(2, "3d7pt", (9, 6, 7), 5), (3, "3d27pt", (11, 5, 6), 4),
-                                                     (2, "3d13pt", (12, 7, 7), 3)])
+                                                     (2, "3d13pt", (12, 7, 7), 3),
+                                                     # 2D: y-slabs, radius 1 and 3
+                                                     (2, "2d9pt", (13, 10), 6), (3, "2d5pt", (14, 9), 5),
+                                                     (2, "2d13pt", (17, 12), 4)])
 def test_nccl_slab_hostloop_matches_global_oracle(world, name, shape, steps):
     import numpy as np
     import torch.multiprocessing as mp

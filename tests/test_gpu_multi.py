@@ -76,7 +76,6 @@ def _nccl_worker(rank, world, port, q, name, shape, steps, dtype):
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device(f"cuda:{rank}"))
     offs, w = si.preset(name)
     radius = max(max(abs(v) for v in o) for o in offs)
-    nz, ny, nx = shape
     u0 = si.field(shape, dtype=dtype)
     holder = {}
 
@@ -88,7 +87,7 @@ def _nccl_worker(rank, world, port, q, name, shape, steps, dtype):
             holder["st"] = Stencil(tuple(src.shape), offs, w, dtype=dtype, device=rank)
         holder["st"].run(src, 1, "hostloop", out=dst)
 
-    sl = NcclSlabHostLoop(nz, ny, nx, radius, rank, world, step, empty)
+    sl = NcclSlabHostLoop(shape, radius, rank, world, step, empty)
     sl.load(torch.from_numpy(u0[sl.z0:sl.z1]).to(f"cuda:{rank}"))
     out = sl.run(steps).cpu().numpy().copy()
     q.put((rank, sl.z0, sl.z1, out))
@@ -96,12 +95,13 @@ def _nccl_worker(rank, world, port, q, name, shape, steps, dtype):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,dtype", [("3d7pt", np.float64), ("3d27pt", np.float32)])
-def test_nccl_slab_hostloop_two_gpus(name, dtype):
+@pytest.mark.parametrize("name,dtype,shape", [("3d7pt", np.float64, (24, 20, 32)), ("3d27pt", np.float32, (24, 20, 32)),
+                                              ("2d9pt", np.float32, (40, 64))])
+def test_nccl_slab_hostloop_two_gpus(name, dtype, shape):
     _need_two()
     import torch.multiprocessing as mp
 
-    world, shape, steps = 2, (24, 20, 32), 6
+    world, steps = 2, 6
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
