@@ -115,21 +115,26 @@ struct Tiles2 {
   int ntx, nty;
 };
 
-// Sliding-window rows of the compute body.  Scalar: x-1 .. x+V of one row.  Packed (fp32, V = 4,
-// PERKS_FFMA2): the four stride-2 pairs (w0,w2), (w1,w3), (w2,w4), (w3,w5) of w = x-1 .. x+4, so
-// the output pairs (n0,n2) and (n1,n3) take every chain operand as one register pair (an FFMA2
-// per term for two cells; neighbours dx = -1, 0, +1 of (n0,n2) are pairs 0, 1, 2, of (n1,n3)
-// pairs 1, 2, 3).  A cached row is stored in the matching order {v0, v2, v1, v3}.
+// Sliding-window rows of the compute body.  Scalar: x-1 .. x+V of one row.  Packed (fp32, V = 4k,
+// PERKS_FFMA2): per group g of 4 cells (b = 4g), the four stride-2 pairs (w_b,w_b+2),
+// (w_b+1,w_b+3), (w_b+2,w_b+4), (w_b+3,w_b+5) of w = x-1 .. x+V, so the group's output pairs
+// (n_b,n_b+2) and (n_b+1,n_b+3) take every chain operand as one register pair (an FFMA2 per term
+// for two cells; neighbours dx = -1, 0, +1 of (n_b,n_b+2) are the group's pairs 0, 1, 2, of
+// (n_b+1,n_b+3) pairs 1, 2, 3).  A cached row is stored in the matching order {v_b, v_b+2, v_b+1,
+// v_b+3} per group.
 template <typename T, int V> struct SWin {
   T w[V + 2];
 };
-struct PWin {
-  f32x2 p[4];
+template <int V> struct PWin {
+  f32x2 p[V / 4][4];
 };
 // storage order of a cached row <-> natural order (self-inverse)
 template <bool PK, typename T, int V> PERKS_DEVINL void perm_row(const T (&a)[V], T (&b)[V]) {
   if constexpr (PK) {
-    b[0] = a[0]; b[1] = a[2]; b[2] = a[1]; b[3] = a[3];
+#pragma unroll
+    for (int g = 0; g < V / 4; g++) {
+      b[4 * g] = a[4 * g]; b[4 * g + 1] = a[4 * g + 2]; b[4 * g + 2] = a[4 * g + 1]; b[4 * g + 3] = a[4 * g + 3];
+    }
   } else {
 #pragma unroll
     for (int i = 0; i < V; i++) b[i] = a[i];
@@ -149,8 +154,8 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
   // an unroll of 3, profiles/r02_c2_ffma2.txt)
   constexpr int SROW_UNROLL = PERKS_P2D_SUNROLL ? PERKS_P2D_SUNROLL : (G::RS > 1 ? G::RS : 1);
   // packed-pair body (FFMA2): fp32 with 4 cells per thread-row
-  constexpr bool PK = PERKS_FFMA2 && sizeof(T) == 4 && V == 4 && RR <= 8;  // (16 register rows + pair windows spill)
-  using Win = typename std::conditional<PK, PWin, SWin<T, V>>::type;
+  constexpr bool PK = PERKS_FFMA2 && sizeof(T) == 4 && V % 4 == 0 && RR <= 8;  // (16 register rows + pair windows spill)
+  using Win = typename std::conditional<PK, PWin<V>, SWin<T, V>>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T *const sm = reinterpret_cast<T *>(smem_raw);
   // shared-memory map (element offsets):
@@ -394,10 +399,14 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
         pcr = sm[pc + o_rdR + r + 1];
         const T left = is_l ? cl : l, right = is_r ? cr : rr;
         if constexpr (PK) {
-          w.p[0] = pack2(left, n[1]);
-          w.p[1] = pack2(v[0], v[1]);  // (n0, n2): the stored pair as is
-          w.p[2] = pack2(v[2], v[3]);  // (n1, n3)
-          w.p[3] = pack2(n[2], right);
+#pragma unroll
+          for (int g = 0; g < V / 4; g++) {
+            const int b = 4 * g;
+            w.p[g][0] = pack2(b == 0 ? left : n[b - 1], n[b + 1]);
+            w.p[g][1] = pack2(v[b], v[b + 1]);      // (n_b, n_b+2): the stored pair as is
+            w.p[g][2] = pack2(v[b + 2], v[b + 3]);  // (n_b+1, n_b+3)
+            w.p[g][3] = pack2(n[b + 2], b + 4 < V ? n[b + 4] : right);
+          }
         } else {
           w.w[0] = left;
           w.w[V + 1] = right;
@@ -412,7 +421,9 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
         for (int i = 0; i < V + 2; i++) h[i] = sm[off + i];
         if constexpr (PK) {
 #pragma unroll
-          for (int j = 0; j < 4; j++) w.p[j] = pack2(h[j], h[j + 2]);
+          for (int g = 0; g < V / 4; g++)
+#pragma unroll
+            for (int j = 0; j < 4; j++) w.p[g][j] = pack2(h[4 * g + j], h[4 * g + j + 2]);
         } else {
 #pragma unroll
           for (int i = 0; i < V + 2; i++) w.w[i] = h[i];
@@ -424,18 +435,25 @@ __global__ void __launch_bounds__(G::NT, 1) perks2d_kernel(const T *__restrict__
       auto finish_row = [&](int r, T (&ns)[V], bool maybe_edge_row = true) {
         T nv[V], cv[V];  // natural order: new values, old values (frame cells keep them)
         if constexpr (PK) {
-          f32x2 A = 0, B = 0;  // cells (0, 2), (1, 3)
+          f32x2 A[V / 4], B[V / 4];  // per group: cells (b, b+2), (b+1, b+3)
 #pragma unroll
           for (int p = 0; p < Shape<S>::N; p++) {
             const int dy = Shape<S>::dy(p), dx = Shape<S>::dx(p);
             const Win &src = dy < 0 ? prev : (dy > 0 ? nxt : cur);
-            A = (p == 0) ? mul2_rn(c.w[0], src.p[1 + dx]) : fma2_rn(c.w[p], src.p[1 + dx], A);
-            B = (p == 0) ? mul2_rn(c.w[0], src.p[2 + dx]) : fma2_rn(c.w[p], src.p[2 + dx], B);
+#pragma unroll
+            for (int g = 0; g < V / 4; g++) {
+              A[g] = (p == 0) ? mul2_rn(c.w[0], src.p[g][1 + dx]) : fma2_rn(c.w[p], src.p[g][1 + dx], A[g]);
+              B[g] = (p == 0) ? mul2_rn(c.w[0], src.p[g][2 + dx]) : fma2_rn(c.w[p], src.p[g][2 + dx], B[g]);
+            }
           }
-          unpack2(A, nv[0], nv[2]);
-          unpack2(B, nv[1], nv[3]);
-          unpack2(cur.p[1], cv[0], cv[2]);
-          unpack2(cur.p[2], cv[1], cv[3]);
+#pragma unroll
+          for (int g = 0; g < V / 4; g++) {
+            const int b = 4 * g;
+            unpack2(A[g], nv[b], nv[b + 2]);
+            unpack2(B[g], nv[b + 1], nv[b + 3]);
+            unpack2(cur.p[g][1], cv[b], cv[b + 2]);
+            unpack2(cur.p[g][2], cv[b + 1], cv[b + 3]);
+          }
         } else {
 #pragma unroll
           for (int i = 0; i < V; i++) {
