@@ -777,7 +777,8 @@ cudaError_t run3(const Problem &p, const Plan &pl, const void *in, void *out, vo
   // runtime caps tcgen05.alloc kernels at one CTA per SM, see occupancy_ignoring_tmem): it is
   // launched normally with a grid of exactly the co-resident capacity computed by the planner
   // (shared memory padded so no further CTA fits an SM), which the block scheduler places all at
-  // once on an idle device.
+  // once on an idle device.  Opt-in only (PERKS_P3D_CACHE=1) and it needs exclusive use of the GPU:
+  // a concurrent kernel holding SMs would leave CTAs unscheduled until the watchdog traps.
   const bool tmem_multi = pl.cache_kernel && pl.ctas_per_sm > 1;
   return L.persistent(steps, s, !(dr && dr->noncoop) && !tmem_multi && !env_int("PERKS_NONCOOP", 0));
 }
