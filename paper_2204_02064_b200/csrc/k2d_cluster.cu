@@ -227,7 +227,9 @@ Plan plan_perks2d_cluster(const Problem &p) {
   if (32 * v < p.nx) { pl.why = "perks2d_cluster: nx too wide"; return pl; }
   // warps per CTA: smallest WY whose cluster (<= 16 CTAs) covers ny
   int wy = -1, csize = 0;
+  const int force_wy = env_int("PERKS_KC_WY", 0);  // sweeps only
   for (int w : {1, 2, 4, 8}) {
+    if (force_wy && w != force_wy) continue;
     const int64_t rows = (int64_t)w * KC_R;
     const int64_t cs = (p.ny + rows - 1) / rows;
     if (cs <= KC_MAX_CLUSTER) { wy = w; csize = (int)cs; break; }
