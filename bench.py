@@ -416,6 +416,7 @@ def run_mine(args):
     # --- roofline of the dominant kernel (the one launch per step for PERKS / persistent)
     peaks = _peaks()
     npts = len(offs)
+    tb2 = q["kernel"].startswith("perks3d_tb2")  # PERKS-3D, two time steps per pass
     launches_per_step = st.launch_count(variant, T)
     kern_ms = ms_per / max(1, launches_per_step)
     if q["variant"] == "perks" and c["stencil"].startswith("2d"):
@@ -428,10 +429,14 @@ def run_mine(args):
         roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "peak_source": "derived: SMs x FMA/clk x 2 x sm_max_mhz"}
     else:
-        # HBM bound: algorithmic bytes = model A_gm per launch (2·S·cells·T·(1-f) + 2·S·D_cache)
+        # HBM bound: algorithmic bytes = model A_gm per launch (2·S·cells·T·(1-f) + 2·S·D_cache);
+        # two steps per pass (k3d_tb.cu): S·cells per step (perks_stencil_info.dram_bytes_per_step)
         f = ((q["cached_cells_reg"] + q["cached_cells_smem"] + q["cached_cells_tmem"]) / cells
              if q["variant"] == "perks" else 0.0)
-        alg = (2.0 * S * cells * (1 - f) * T + 2.0 * S * cells * f) / max(1, launches_per_step)
+        if tb2:
+            alg = q["dram_bytes_per_step"] * T / max(1, launches_per_step)
+        else:
+            alg = (2.0 * S * cells * (1 - f) * T + 2.0 * S * cells * f) / max(1, launches_per_step)
         achieved = alg / (kern_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
@@ -452,7 +457,17 @@ def run_mine(args):
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     f_sm = (clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)) * 1e6
     B_sm = model.b_sm(sms, 128, f_sm)
-    if c["stencil"].startswith("3d"):
+    if tb2:
+        # per two steps: the TMA box write ((TY+4)(TX+2·PAD)/(TX·TY)), stage-1 neighbourhood reads
+        # (rows (R+2)/R, x-neighbours 2/V), the IS write, stage-2 reads (own rows from registers:
+        # x-neighbours 2/V of R rows + 2 full rows), halved per step
+        V, R = (4, 4) if S == 4 else (2, 4)
+        TX, TY, PAD = 32 * V, 8 * R, 16 // S
+        k_box = (TY + 4) * (TX + 2 * PAD) / (TX * TY)
+        k_s1 = (R + 2) / R * (V + 2) / V
+        k_s2 = (2.0 / V) + 2.0 / R * (V + 2) / V
+        k_sm = 0.5 * (k_box + k_s1 + 1.0 + k_s2)
+    elif c["stencil"].startswith("3d"):
         V, R = (4, 2) if S == 4 else (2, 2)
         k_sm = 1.0 + (R + 2) * (V + 2) / (R * V)
     else:
@@ -460,7 +475,8 @@ def run_mine(args):
     D_sm = min(q["cached_cells_smem"], cells) if q["variant"] == "perks" else 0
     proj = model.project(cells, min(cached, cells), T, S, peaks["hbm_gbs"] * 1e9,
                          A_halo=q["halo_bytes_per_step"] / S * T, D_sm_cache=D_sm, B_sm=B_sm,
-                         A_sm_kernel=k_sm * cells * T)
+                         A_sm_kernel=k_sm * cells * T,
+                         A_gm_elems=(cells * T if tb2 else None))
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per, "higher_is_better": True,

@@ -161,6 +161,12 @@ const Plan &get_plan(perks_stencil_s *h, perks_variant v) {
       // plane-streaming persistent kernel on every 3D domain that fits them, because such domains
       // also fit B200's L2 (profiles/r02_brick3d.txt); default: the streaming kernel (k3d_stream.cu)
       if (env_int("PERKS_P3D_BRICK", 0) && p.nranks == 1) pl = plan_brick3d(p);
+      // two time steps per pass (k3d_tb.cu): the default for the 7-point star (PERKS_P3D_TB=-1;
+      // not when the opt-in plane-cache tiers are requested), PERKS_P3D_TB=1 for every r = 1
+      // shape, 0 off
+      const int tb = env_int("PERKS_P3D_TB", -1);
+      const bool tb_auto = tb < 0 && p.shape == SHAPE_3D7 && env_int("PERKS_P3D_CACHE", 0) == 0;
+      if (!pl.ok && p.nranks == 1 && (tb == 1 || tb_auto)) pl = plan_tb3d(p);
       if (!pl.ok) pl = plan_stream3d(p, PERKS_PERKS);
     }
     h->plans[i] = pl;
@@ -517,6 +523,8 @@ perks_status perks_stencil_run(perks_stencil_t h, perks_variant v, const void *d
                              : run_perks2d(p, pl, d_in, d_out, d_ws, steps, s);
       else if (pl.family == 6)
         e = run_brick3d(p, pl, d_in, d_out, d_ws, steps, s);
+      else if (pl.family == 7)
+        e = run_tb3d(p, pl, d_in, d_out, d_ws, steps, s);
       else
         e = run_stream3d(p, pl, d_in, d_out, d_ws, steps, s);
       break;

@@ -111,6 +111,12 @@ Plan plan_brick3d(const Problem &p);
 cudaError_t run_brick3d(const Problem &p, const Plan &pl, const void *in, void *out, void *ws, int64_t steps,
                         cudaStream_t s);
 
+// PERKS (c), 3D domains beyond the on-chip capacity: two time steps per pass, level t+1 of the planes
+// in flight kept in shared memory (k3d_tb.cu).
+Plan plan_tb3d(const Problem &p);
+cudaError_t run_tb3d(const Problem &p, const Plan &pl, const void *in, void *out, void *ws, int64_t steps,
+                     cudaStream_t s);
+
 // Any variant for general 2D point sets of radius <= 6 (k2d_wide.cu).
 Plan plan_wide2d(const Problem &p, perks_variant v);
 cudaError_t run_wide2d(const Problem &p, const Plan &pl, const void *in, void *out, void *ws, int64_t steps,

@@ -1,0 +1,567 @@
+// k3d_tb.cu — PERKS (c) for 3D domains beyond the on-chip capacity: the persistent plane-streaming
+// kernel advancing TWO time steps per pass over the domain, with the intermediate time level kept
+// on chip (Tiled PERKS, [draft] P:416-441, in its streaming form; DESIGN.md §7 reading R13).
+//
+// The paper's PERKS caches part of the domain between time steps so that it is not re-read from
+// global memory.  For a 3D domain several times the on-chip capacity (C3: 134 MB
+// vs ~70 MB of shared memory + TMEM over 148 SMs; C4: 537 MB) what can stay on chip across a time
+// step is the wavefront of planes in flight: here each CTA streams its unit (an xy tile, a z
+// range) once per PAIR of steps and keeps time level t+1 of the planes in flight in shared memory,
+// so DRAM moves 2·S bytes per cell per two steps instead of per step (A_gm halved).  The
+// draft's Tiled PERKS "has a redundant halo region to enable the execution of consecutive time
+// steps" and notes that "optimization methods related to temporal blocking are all applicable"
+// (P:433-439): the redundancy here is a one-cell ring of level t+1 around each tile.
+//
+// Per CTA (one per SM, cooperative launch, grid barrier between passes):
+//   * producer warp: TMA boxes {P, TY+4, 1} of the input planes (a two-cell halo in x and y,
+//     zero-filled outside the domain) into an NS-slot ring (full/empty mbarriers);
+//   * main warps (8): thread (lane, warp) owns V x R cells of the TX x TY output window.  Stage 1
+//     applies plane p's chain terms to level t+1 of planes p-1..p+1 (stream3d.cuh arrival(),
+//     reading R5 order), writes the finished plane p-1 of level t+1 into one of two intermediate
+//     (IS) slots; stage 2 applies the previous tick's IS plane to level t+2 and stores the finished
+//     output plane to HBM;
+//   * halo warps: level t+1 on the one-cell ring around the window (2(TX+2) + 2TY cells per plane,
+//     one cell per lane and pass of the loop), written into the same IS slot;
+//   * one named barrier over main + halo warps per tick (IS slot written -> read next tick).
+// Frame cells (reading R1) keep their value at both levels (frame_select with the stage's own
+// centre), so the two-level result is bit-identical to two single steps.  Odd T: the first pass
+// runs one step (stage 1 stored directly).
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <type_traits>
+
+#include "internal.h"
+#include "stream3d.cuh"
+
+namespace perks {
+
+bool use_tma3(const Problem &p);
+bool encode_map3(CUtensorMap *m, const Problem &p, const void *base, int bx, int by);
+
+// Stage 2 takes its own cells from registers (1) or re-reads them from the IS slot (0: fewer live
+// registers).
+#ifndef PERKS_TB_OWN
+#define PERKS_TB_OWN 1
+#endif
+constexpr bool kTbOwn = PERKS_TB_OWN != 0;
+// 1: both stages' loads and FMA chains in one basic block per tick (after the input wait);
+// 0: stage 2 with its store, then the input wait and stage 1.
+#ifndef PERKS_TB_FUSE
+#define PERKS_TB_FUSE 0
+#endif
+constexpr bool kTbFuse = PERKS_TB_FUSE != 0;
+#ifndef PERKS_TB_NS
+#define PERKS_TB_NS 4
+#endif
+
+// Rows per thread: 4 for the 7-point star (two accumulator arrays per level: (R+2)/R = 1.5 row
+// reads per cell), 2 for the box / 19-point shapes (four arrays per level).
+template <typename T, int S> struct TbG {
+  static constexpr int V = 16 / (int)sizeof(T), R = S == SHAPE_3D7 ? 4 : 2, NWARP = 8, NS = PERKS_TB_NS;
+  using G = Geo3D<T, V, R, NWARP, NS>;  // compute geometry (IS slot = G::SLOT: TY+2 rows of pitch P)
+  static constexpr int TX = G::TX, TY = G::TY, P = G::P, PAD = G::PAD;
+  static_assert(PAD >= 2, "two-cell x halo inside the row padding");
+  static constexpr int RI = TY + 4;  // input box rows (two-cell y halo)
+  static constexpr int IN_SLOT = (RI * P * (int)sizeof(T) + 127) / 128 * 128 / (int)sizeof(T);
+  static constexpr unsigned IN_BOX_BYTES = (unsigned)(RI * P * sizeof(T));
+  static constexpr int RING = 2 * (TX + 2) + 2 * TY;  // level t+1 cells around the window
+  // halo warps: 3, so that main + halo + producer = 12 warps = 3 per SM sub-partition (a 13th warp
+  // would cap the register budget at 128 per thread: 4 warps x 128 x 32 = one 16K-entry SMSP file)
+  static constexpr int NHW = 3;
+  static constexpr int HC = (RING + 32 * NHW - 1) / (32 * NHW);
+  static constexpr int NCW = NWARP + NHW;  // consumer warps (main + halo)
+  static constexpr int NTHR = 32 * (NCW + 1);
+  static constexpr size_t IS_OFF = (size_t)NS * IN_SLOT * sizeof(T);
+  static constexpr size_t BAR_OFF = IS_OFF + 2 * G::SLOT_BYTES;
+  static constexpr size_t SMEM = BAR_OFF + 2 * NS * 8;
+};
+
+struct TbMaps {
+  CUtensorMap m[3];  // in, out, tmp: box {P, TY+4, 1}
+};
+struct TbUnits {
+  int tx, ty, nzc, zc, rev;
+};
+
+// Single-cell geometry for the halo warps' chain (apply_terms needs only R and V).
+struct G11 {
+  static constexpr int R = 1, V = 1;
+};
+
+// arrival() of stream3d.cuh for one cell whose 3x3 neighbourhood in plane q is already loaded.
+template <typename T, int S>
+PERKS_DEVINL void arrival_cell(StreamState<T, G11> &st, const T (&nb)[3][3], const Coef<T, Shape<S>::N> &c,
+                               T &out, T &center_q) {
+  constexpr int e0 = stage_end<S>(0), e1 = stage_end<S>(1), e2 = stage_end<S>(2);
+  center_q = nb[1][1];
+  apply_terms<T, S, G11, e1, e2, 1>(st.accC, nb, st.cm1, c);
+  out = st.accC[0][0];
+  apply_terms<T, S, G11, e0, e1, 0>(st.accB, nb, st.cm1, c);
+  apply_terms<T, S, G11, 0, e0, -1>(st.accA, nb, st.cm1, c);
+  st.accC[0][0] = st.accB[0][0];
+  st.accB[0][0] = st.accA[0][0];
+}
+
+// Producer's wait for a free slot: try_wait with a suspend-time hint (the thread sleeps until the
+// phase completes or ~hint ns pass instead of re-polling and taking issue slots from the SMSP's
+// consumer warps); watchdog as mbar_wait.
+PERKS_DEVINL void mbar_wait_sleep(uint64_t *b, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      ".reg .u64 t0, t1;\n"
+      "mov.u64 t0, %%globaltimer;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %3;\n"
+      "@p bra DONE_%=;\n"
+      "mov.u64 t1, %%globaltimer;\n"
+      "sub.u64 t1, t1, t0;\n"
+      "setp.gt.u64 p, t1, %2;\n"
+      "@p trap;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity), "l"((unsigned long long)PERKS_WATCHDOG_NS), "r"(20000u)
+      : "memory");
+}
+
+template <class B> PERKS_DEVINL void tb_consumers_sync() {
+  asm volatile("bar.sync 1, %0;\n" ::"n"(32 * B::NCW) : "memory");
+}
+
+// Stage 2's input neighbourhood: the thread's own R x V cells of the IS plane are the level t+1
+// values it computed (and wrote) one tick earlier, kept in registers; only the x-neighbours of
+// those rows and the rows above / below come from shared memory.
+template <typename T, class G>
+PERKS_DEVINL void read_nb_own(const T *slot, const T (&own)[G::R][G::V], T (&nb)[G::R + 2][G::V + 2]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < G::R + 2; j++) {
+    const T *row = slot + (warp * G::R + j) * G::P + G::PAD + lane * G::V;
+    nb[j][0] = row[-1];
+    nb[j][G::V + 1] = row[G::V];
+    if (j == 0 || j == G::R + 1) {
+      T v[G::V];
+      vload<T, G::V>(v, row);
+#pragma unroll
+      for (int i = 0; i < G::V; i++) nb[j][i + 1] = v[i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < G::V; i++) nb[j][i + 1] = own[j - 1][i];
+    }
+  }
+}
+
+// arrival() of stream3d.cuh with the plane-q neighbourhood already in registers.
+template <typename T, int S, class G>
+PERKS_DEVINL void arrival_nb(StreamState<T, G> &st, const T (&nb)[G::R + 2][G::V + 2], const Coef<T, Shape<S>::N> &c,
+                             T (&out)[G::R][G::V], T (&center_q)[G::R][G::V]) {
+  constexpr int e0 = stage_end<S>(0), e1 = stage_end<S>(1), e2 = stage_end<S>(2);
+#pragma unroll
+  for (int r = 0; r < G::R; r++)
+#pragma unroll
+    for (int i = 0; i < G::V; i++) center_q[r][i] = nb[r + 1][i + 1];
+  apply_terms<T, S, G, e1, e2, 1>(st.accC, nb, st.cm1, c);
+#pragma unroll
+  for (int r = 0; r < G::R; r++)
+#pragma unroll
+    for (int i = 0; i < G::V; i++) out[r][i] = st.accC[r][i];
+  apply_terms<T, S, G, e0, e1, 0>(st.accB, nb, st.cm1, c);
+  apply_terms<T, S, G, 0, e0, -1>(st.accA, nb, st.cm1, c);
+#pragma unroll
+  for (int r = 0; r < G::R; r++)
+#pragma unroll
+    for (int i = 0; i < G::V; i++) {
+      st.accC[r][i] = st.accB[r][i];
+      st.accB[r][i] = st.accA[r][i];
+    }
+}
+
+template <typename T, int S>
+__global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
+    tb3d_kernel(const T *__restrict__ in, T *out, T *tmp, const __grid_constant__ TbMaps maps, Dom3 d, TbUnits u,
+                int64_t steps, unsigned *bar, Coef<T, Shape<S>::N> c) {
+  using B = TbG<T, S>;
+  using G = typename B::G;
+  unsigned char *sm = dyn_smem();
+  T *const in_slots = reinterpret_cast<T *>(sm);
+  T *const is_slots = reinterpret_cast<T *>(sm + B::IS_OFF);
+  uint64_t *const bars = reinterpret_cast<uint64_t *>(sm + B::BAR_OFF);
+  auto in_slot = [&](unsigned k) { return in_slots + (size_t)(k % B::NS) * B::IN_SLOT; };
+  auto is_slot = [&](int b) { return is_slots + (size_t)b * G::SLOT; };
+  auto fullb = [&](unsigned k) { return bars + (k % B::NS); };
+  auto emptyb = [&](unsigned k) { return bars + B::NS + (k % B::NS); };
+
+  const int warp = (int)(threadIdx.x >> 5), lane = (int)(threadIdx.x & 31);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < B::NS; i++) {
+      mbar_init(bars + i, 1);
+      mbar_init(bars + B::NS + i, B::NCW);
+    }
+    mbar_fence_init();
+  }
+  // zero the IS slots once: cells outside window + ring are never written (nor read for kept cells)
+  for (int i = threadIdx.x; i < 2 * G::SLOT; i += blockDim.x) is_slots[i] = T(0);
+  __syncthreads();
+
+  const int tiles = u.tx * u.ty;
+  const int nunits = tiles * u.nzc;
+  const int nmine = (int)blockIdx.x < nunits ? (nunits - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const size_t plane = (size_t)d.nx * d.ny;
+  const int64_t npass = (steps + 1) / 2;
+  unsigned gk = 0;  // input arrivals so far (slot = gk % NS, phase = (gk / NS) & 1)
+
+  for (int64_t ps = 0; ps < npass; ps++) {
+    const int nst = (ps == 0 && (steps & 1)) ? 1 : 2;
+    const bool src_out = ps > 0 && ((npass - ps) & 1) == 0;
+    const T *src = ps == 0 ? in : (src_out ? out : tmp);
+    const int src_idx = ps == 0 ? 0 : (src_out ? 1 : 2);
+    T *dst = ((npass - 1 - ps) & 1) == 0 ? out : tmp;
+    (void)src;
+    const bool rev = u.rev && (ps & 1);  // L2-aware traversal (zig-zag, [draft] P:395-404)
+    for (int jj = 0; jj < nmine; jj++) {
+      const int j = rev ? nmine - 1 - jj : jj;
+      const int id = (int)blockIdx.x + j * (int)gridDim.x;
+      const int t = id % tiles, zci = id / tiles;
+      const int x0 = (t % u.tx) * B::TX, y0 = (t / u.tx) * B::TY;
+      const int zs = zci * u.zc, ze = min(zs + u.zc, d.nz);
+      const int zc = ze - zs;
+      const int nin = nst == 2 ? zc + 4 : zc + 2;  // input planes zs-2..ze+1 (zs-1..ze)
+      const int q0 = nst == 2 ? zs - 2 : zs - 1;
+      const unsigned k0 = gk;
+      gk += (unsigned)nin;
+      if (warp == B::NCW) {  // ---------------------------------------------------------- producer
+        if (lane == 0) {
+          if (jj == 0) fence_proxy_async_global();  // previous pass's generic stores -> TMA reads
+          for (int k = 0; k < nin; k++) {
+            const unsigned kk = k0 + (unsigned)k;
+            if (kk >= (unsigned)B::NS) mbar_wait_sleep(emptyb(kk), ((kk / B::NS) + 1) & 1u);
+            fence_proxy_async();
+            mbar_arrive_tx(fullb(kk), B::IN_BOX_BYTES);
+            tma_load_3d(in_slot(kk), &maps.m[src_idx], x0 - B::PAD, y0 - 2, q0 + k, fullb(kk));
+          }
+        }
+        __syncwarp();
+        continue;
+      }
+      auto release = [&](unsigned kk) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive_release(emptyb(kk));
+      };
+      if (warp < B::NWARP) {  // -------------------------------------------------------- main warps
+        ThreadTile<G> tt;
+        tt.init(d, x0, y0);
+        StreamState<T, G> s1, s2;
+        s1.zero();
+        s2.zero();
+        T own[G::R][G::V];  // this thread's cells of the IS plane written last tick
+        T *sp = dst + (size_t)zs * plane + tt.off(d);
+        auto store = [&](int o, const T (&v)[G::R][G::V]) {
+          if (tt.full) {
+#pragma unroll
+            for (int r = 0; r < G::R; r++) vstore<T, G::V>(sp + (size_t)r * d.nx, v[r]);
+          } else {
+            store_cells<T, G>(dst, d, tt, o, v);
+          }
+          sp += plane;
+        };
+        if (nst == 1) {
+          for (int k = 0; k < nin; k++) {
+            const unsigned kk = k0 + (unsigned)k;
+            mbar_wait(fullb(kk), (kk / B::NS) & 1u);
+            T o1[G::R][G::V], c1[G::R][G::V];
+            arrival<T, S, G>(s1, in_slot(kk) + G::P, c, o1, c1);
+            release(kk);
+            if (k >= 2) {
+              frame_select<T, G>(d, tt, zs - 2 + k, o1, s1.cm1);
+              store(zs - 2 + k, o1);
+            }
+#pragma unroll
+            for (int r = 0; r < G::R; r++)
+#pragma unroll
+              for (int i = 0; i < G::V; i++) s1.cm1[r][i] = c1[r][i];
+          }
+          continue;
+        }
+        // One tick: stage 2 on the IS plane written last tick (A2; ST: store its output), stage 1 on
+        // input plane zs-2+k (A1; W1: write its output to the IS slot); order per kTbFuse.
+        auto tick = [&](int k, auto a1, auto a2, auto st, auto w1) {
+          constexpr bool A1 = decltype(a1)::value, A2 = decltype(a2)::value;
+          constexpr bool ST = decltype(st)::value, W1 = decltype(w1)::value;
+          const unsigned kk = k0 + (unsigned)k;
+          T o2[G::R][G::V], c2[G::R][G::V], o1[G::R][G::V], c1[G::R][G::V];
+          auto stage2 = [&]() {
+            T nb[G::R + 2][G::V + 2];
+            if constexpr (kTbOwn) read_nb_own<T, G>(is_slot((k - 1) & 1), own, nb);
+            else read_nb<T, G>(is_slot((k - 1) & 1), nb);
+            arrival_nb<T, S, G>(s2, nb, c, o2, c2);
+          };
+          auto stage2_out = [&]() {
+            if constexpr (ST) {
+              frame_select<T, G>(d, tt, zs - 5 + k, o2, s2.cm1);
+              store(zs - 5 + k, o2);
+            }
+#pragma unroll
+            for (int r = 0; r < G::R; r++)
+#pragma unroll
+              for (int i = 0; i < G::V; i++) s2.cm1[r][i] = c2[r][i];
+          };
+          auto stage1 = [&]() {
+            T nb[G::R + 2][G::V + 2];
+            read_nb<T, G>(in_slot(kk) + G::P, nb);
+            arrival_nb<T, S, G>(s1, nb, c, o1, c1);
+          };
+          auto stage1_out = [&]() {
+            if constexpr (W1) {
+              frame_select<T, G>(d, tt, zs - 3 + k, o1, s1.cm1);
+              write_own<T, G>(is_slot(k & 1), o1);
+              if constexpr (kTbOwn) {
+#pragma unroll
+                for (int r = 0; r < G::R; r++)
+#pragma unroll
+                  for (int i = 0; i < G::V; i++) own[r][i] = o1[r][i];
+              }
+            }
+#pragma unroll
+            for (int r = 0; r < G::R; r++)
+#pragma unroll
+              for (int i = 0; i < G::V; i++) s1.cm1[r][i] = c1[r][i];
+          };
+          if constexpr (kTbFuse) {  // input wait, both stages in one basic block, then outputs
+            if constexpr (A1) mbar_wait(fullb(kk), (kk / B::NS) & 1u);
+            if constexpr (A2) stage2();
+            if constexpr (A1) stage1();
+            if constexpr (A1) release(kk);
+            if constexpr (A2) stage2_out();
+            if constexpr (A1) stage1_out();
+          } else {  // stage 2 and its store, then the input wait and stage 1
+            if constexpr (A2) {
+              stage2();
+              stage2_out();
+            }
+            if constexpr (A1) {
+              mbar_wait(fullb(kk), (kk / B::NS) & 1u);
+              stage1();
+              release(kk);
+              stage1_out();
+            }
+          }
+          tb_consumers_sync<B>();
+        };
+        using Y = std::true_type;
+        using N = std::false_type;
+        // ticks 0..4 (pipeline fill), 5..zc+3 (steady state), zc+4 (drain): K = zc + 5 ticks
+        tick(0, Y{}, N{}, N{}, N{});
+        tick(1, Y{}, N{}, N{}, N{});
+        tick(2, Y{}, N{}, N{}, Y{});
+        tick(3, Y{}, Y{}, N{}, Y{});
+        tick(4, Y{}, Y{}, N{}, Y{});
+        for (int k = 5; k < zc + 4; k++) tick(k, Y{}, Y{}, Y{}, Y{});
+        tick(zc + 4, N{}, Y{}, Y{}, N{});
+        continue;
+      }
+      // ------------------------------------------------------------------------------ halo warps
+      if (nst == 1) {
+        for (int k = 0; k < nin; k++) {
+          const unsigned kk = k0 + (unsigned)k;
+          mbar_wait(fullb(kk), (kk / B::NS) & 1u);
+          release(kk);
+        }
+        continue;
+      }
+      int ioff[B::HC], soff[B::HC];
+      unsigned hmask = 0, fmask = 0;  // bit j: cell j exists / is an x-y frame cell (or outside)
+      const int hl = (warp - B::NWARP) * 32 + lane;
+#pragma unroll
+      for (int j = 0; j < B::HC; j++) {
+        const int cc = hl + j * 32 * B::NHW;
+        int hx, hy;
+        if (cc < B::TX + 2) { hx = cc - 1; hy = -1; }
+        else if (cc < 2 * (B::TX + 2)) { hx = cc - (B::TX + 2) - 1; hy = B::TY; }
+        else if (cc < 2 * (B::TX + 2) + B::TY) { hx = -1; hy = cc - 2 * (B::TX + 2); }
+        else { hx = B::TX; hy = cc - 2 * (B::TX + 2) - B::TY; }
+        ioff[j] = (hy + 2) * B::P + B::PAD + hx;
+        soff[j] = (hy + 1) * B::P + B::PAD + hx;
+        hmask |= (unsigned)(cc < B::RING) << j;
+        const int gx = x0 + hx, gy = y0 + hy;
+        fmask |= (unsigned)!(gx >= 1 && gx <= d.nx - 2 && gy >= 1 && gy <= d.ny - 2) << j;
+      }
+      StreamState<T, G11> hs[B::HC];
+#pragma unroll
+      for (int j = 0; j < B::HC; j++) hs[j].zero();
+      const int K = zc + 5;
+      for (int k = 0; k < K; k++) {
+        if (k < zc + 4) {
+          const unsigned kk = k0 + (unsigned)k;
+          mbar_wait(fullb(kk), (kk / B::NS) & 1u);
+          const T *sl = in_slot(kk);
+          T ho[B::HC], hc[B::HC];
+#pragma unroll
+          for (int j = 0; j < B::HC; j++) {
+            if ((hmask >> j) & 1u) {
+              T nb[3][3];
+#pragma unroll
+              for (int dy = 0; dy < 3; dy++)
+#pragma unroll
+                for (int dx = 0; dx < 3; dx++) nb[dy][dx] = sl[ioff[j] + (dy - 1) * B::P + dx - 1];
+              arrival_cell<T, S>(hs[j], nb, c, ho[j], hc[j]);
+            } else {
+              ho[j] = hc[j] = T(0);
+            }
+          }
+          release(kk);
+          if (k >= 2) {
+            const int o = zs - 3 + k;
+            const bool zint = o >= d.zlo && o <= d.zhi;
+            T *is = is_slot(k & 1);
+#pragma unroll
+            for (int j = 0; j < B::HC; j++)
+              if ((hmask >> j) & 1u) is[soff[j]] = (zint && !((fmask >> j) & 1u)) ? ho[j] : hs[j].cm1[0][0];
+          }
+#pragma unroll
+          for (int j = 0; j < B::HC; j++) hs[j].cm1[0][0] = hc[j];
+        }
+        tb_consumers_sync<B>();
+      }
+    }
+    if (ps + 1 < npass) grid_barrier(bar, (unsigned)(ps + 1));
+  }
+}
+
+namespace {
+template <typename T> void *tb_kernel(int shape) {
+  return shape == SHAPE_3D7    ? (void *)tb3d_kernel<T, SHAPE_3D7>
+         : shape == SHAPE_3D19 ? (void *)tb3d_kernel<T, SHAPE_3D19>
+                               : (void *)tb3d_kernel<T, SHAPE_3D27>;
+}
+struct TbInfo {
+  int TX, TY, NT, P, RI;
+  size_t smem;
+};
+template <typename T, int S> TbInfo tb_info_s() {
+  using B = TbG<T, S>;
+  return TbInfo{B::TX, B::TY, B::NTHR, B::P, B::RI, B::SMEM};
+}
+template <typename T> TbInfo tb_info(int shape) {
+  return shape == SHAPE_3D7 ? tb_info_s<T, SHAPE_3D7>() : shape == SHAPE_3D19 ? tb_info_s<T, SHAPE_3D19>()
+                                                                              : tb_info_s<T, SHAPE_3D27>();
+}
+}  // namespace
+
+Plan plan_tb3d(const Problem &p) {
+  Plan pl;
+  pl.variant = PERKS_PERKS;
+  if (p.ndim != 3 || (p.shape != SHAPE_3D7 && p.shape != SHAPE_3D27 && p.shape != SHAPE_3D19) ||
+      p.bc != PERKS_BC_FRAME || p.nranks != 1) {
+    pl.why = "tb3d: needs single-GPU 3D 7pt/19pt/27pt FRAME";
+    return pl;
+  }
+  if (!use_tma3(p)) { pl.why = "tb3d: needs TMA (nx*S % 16 == 0)"; return pl; }
+  const bool f32 = p.dtype == PERKS_F32;
+  const TbInfo ti = f32 ? tb_info<float>(p.shape) : tb_info<double>(p.shape);
+  const int TX = ti.TX, TY = ti.TY, NT = ti.NT;
+  const size_t smem = ti.smem;
+  void *k = f32 ? tb_kernel<float>(p.shape) : tb_kernel<double>(p.shape);
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    cudaGetLastError();
+    pl.why = "tb3d: cudaFuncSetAttribute";
+    return pl;
+  }
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, k) != cudaSuccess) { cudaGetLastError(); pl.why = "cudaFuncGetAttributes"; return pl; }
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NT, smem);
+  if (occ < 1) { pl.why = "tb3d: not resident"; return pl; }
+  occ = 1;  // one CTA per SM (launch bounds)
+  const int tx = (int)((p.nx + TX - 1) / TX), ty = (int)((p.ny + TY - 1) / TY);
+  const int64_t tiles = (int64_t)tx * ty;
+  const int64_t resident = (int64_t)occ * p.num_sms;
+  // z chunks: minimise the busiest CTA's ticks per pass, ceil(units / grid) * (chunk + 5)
+  int nzc = 1;
+  int64_t best = -1;
+  for (int n = 1; n <= std::max<int64_t>(1, p.nz / 4); n++) {
+    const int64_t zcn = (p.nz + n - 1) / n, nn = (p.nz + zcn - 1) / zcn;
+    if (nn != n) continue;
+    const int64_t un = tiles * n, g = std::min<int64_t>(un, resident);
+    const int64_t cost = ((un + g - 1) / g) * (zcn + 5);
+    if (best < 0 || cost < best) { best = cost; nzc = n; }
+  }
+  if (env_int("PERKS_TB_NZC", 0) > 0) nzc = std::min<int>(env_int("PERKS_TB_NZC", 0), (int)p.nz);
+  const int zc = (int)((p.nz + nzc - 1) / nzc);
+  nzc = (int)((p.nz + zc - 1) / zc);
+  pl.units = tiles * nzc;
+  pl.zchunk = zc;
+  pl.grid = (int)std::min<int64_t>(pl.units, resident);
+  pl.block = NT;
+  pl.ctas_per_sm = occ;
+  pl.tile[0] = TX; pl.tile[1] = TY; pl.tile[2] = zc;
+  pl.regs = fa.numRegs;
+  pl.smem = (int)smem;
+  pl.cfg = 1;
+  pl.family = 7;  // (3D PERKS, two time steps per pass)
+  const double S = (double)p.elem();
+  pl.cached_smem = 0;  // level t+1 is on chip only while its planes are in flight (no resident cells)
+  pl.dram_bytes_step = S * (double)p.cells();  // 2·S·cells per pass of two steps
+  // halo through L2 per step: the input box beyond the tile, once per two steps
+  const int RI = ti.RI, PB = ti.P;
+  pl.halo_bytes_step = 0.5 * S * (double)(RI * PB - TX * TY) * (double)tiles * (double)(p.nz + 4 * nzc);
+  pl.ws_bytes = align256((size_t)p.cells() * p.elem()) + 256;
+  snprintf(pl.name, sizeof(pl.name), "perks3d_tb2_%s_%s_t%dx%d_z%d",
+           p.shape == SHAPE_3D7 ? "7pt" : p.shape == SHAPE_3D19 ? "19pt" : "27pt", f32 ? "f32" : "f64", TX, TY, zc);
+  pl.ok = true;
+  return pl;
+}
+
+namespace {
+template <typename T, int S>
+cudaError_t launch_tb(const Problem &p, const Plan &pl, const T *in, T *out, void *ws, int64_t steps,
+                      cudaStream_t s) {
+  using B = TbG<T, S>;
+  Coef<T, Shape<S>::N> c;
+  for (int i = 0; i < Shape<S>::N; i++) c.w[i] = sizeof(T) == 4 ? (T)p.wf[i] : (T)p.wd[i];
+  Dom3 d{(int)p.nx, (int)p.ny, (int)p.nz, 1, (int)p.nz - 2};
+  TbUnits u{(int)((p.nx + B::TX - 1) / B::TX), (int)((p.ny + B::TY - 1) / B::TY), 0, pl.zchunk,
+            env_int("PERKS_ZIGZAG", 1)};
+  u.nzc = (int)((p.nz + u.zc - 1) / u.zc);
+  char *w = (char *)ws;
+  T *tmp = (T *)w;
+  unsigned *bar = (unsigned *)(w + align256((size_t)p.cells() * p.elem()));
+  TbMaps maps;
+  std::memset(&maps, 0, sizeof(maps));
+  const void *b[3] = {in, out, tmp};
+  for (int i = 0; i < 3; i++)
+    if (!encode_map3(&maps.m[i], p, b[i], B::P, B::RI)) return cudaErrorInvalidValue;
+  cudaError_t e = reset_grid_barrier(bar, s);
+  if (e != cudaSuccess) return e;
+  void *k = (void *)tb3d_kernel<T, S>;
+  void *args[] = {(void *)&in, (void *)&out, (void *)&tmp, (void *)&maps, (void *)&d, (void *)&u,
+                  (void *)&steps, (void *)&bar, (void *)&c};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(pl.grid);
+  cfg.blockDim = dim3(pl.block);
+  cfg.dynamicSmemBytes = (size_t)pl.smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, k, args);
+}
+}  // namespace
+
+cudaError_t run_tb3d(const Problem &p, const Plan &pl, const void *in, void *out, void *ws, int64_t steps,
+                     cudaStream_t s) {
+  if (p.dtype == PERKS_F32)
+    return p.shape == SHAPE_3D7    ? launch_tb<float, SHAPE_3D7>(p, pl, (const float *)in, (float *)out, ws, steps, s)
+           : p.shape == SHAPE_3D19 ? launch_tb<float, SHAPE_3D19>(p, pl, (const float *)in, (float *)out, ws, steps, s)
+                                   : launch_tb<float, SHAPE_3D27>(p, pl, (const float *)in, (float *)out, ws, steps, s);
+  return p.shape == SHAPE_3D7    ? launch_tb<double, SHAPE_3D7>(p, pl, (const double *)in, (double *)out, ws, steps, s)
+         : p.shape == SHAPE_3D19 ? launch_tb<double, SHAPE_3D19>(p, pl, (const double *)in, (double *)out, ws, steps, s)
+                                 : launch_tb<double, SHAPE_3D27>(p, pl, (const double *)in, (double *)out, ws, steps, s);
+}
+
+}  // namespace perks

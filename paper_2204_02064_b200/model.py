@@ -84,9 +84,10 @@ class Projection:
 
 
 def project(D, D_cache, N, S, B_gm, A_halo=0.0, D_sm_cache=0.0, B_sm=float("inf"),
-            A_sm_kernel=0.0) -> Projection:
-    """ℙ for one configuration (Eqs. basic…maxpeak)."""
-    tg = T_gm(D, D_cache, N, S, B_gm)
+            A_sm_kernel=0.0, A_gm_elems=None) -> Projection:
+    """ℙ for one configuration (Eqs. basic…maxpeak).  ``A_gm_elems`` replaces Eq. when a
+    kernel's global traffic is not of the cached-fraction form (two steps per pass: N·D)."""
+    tg = T_gm(D, D_cache, N, S, B_gm) if A_gm_elems is None else A_gm_elems * S / B_gm
     th = T_halo(A_halo, S, B_gm)
     ts = T_sm(D_sm_cache, N, S, B_sm, A_sm_kernel) if B_sm != float("inf") else 0.0
     tp = T_perks(tg, th, ts)
