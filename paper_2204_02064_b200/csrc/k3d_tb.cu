@@ -53,14 +53,34 @@ constexpr bool kTbOwn = PERKS_TB_OWN != 0;
 #define PERKS_TB_FUSE 0
 #endif
 constexpr bool kTbFuse = PERKS_TB_FUSE != 0;
+// Intermediate (IS) planes: 1 = an NI-slot ring with per-slot written / read mbarriers (warps drift
+// up to NI-2 ticks apart); 0 = two slots and one named barrier over the consumer warps per tick.
+#ifndef PERKS_TB_MBAR
+#define PERKS_TB_MBAR 1
+#endif
+constexpr bool kTbMbar = PERKS_TB_MBAR != 0;
+#ifndef PERKS_TB_NI
+#define PERKS_TB_NI 3
+#endif
 #ifndef PERKS_TB_NS
 #define PERKS_TB_NS 4
 #endif
 
 // Rows per thread: 4 for the 7-point star (two accumulator arrays per level: (R+2)/R = 1.5 row
 // reads per cell), 2 for the box / 19-point shapes (four arrays per level).
+#ifndef PERKS_TB_R7
+#define PERKS_TB_R7 4
+#endif
+#ifndef PERKS_TB_NW7
+#define PERKS_TB_NW7 8
+#endif
+#ifndef PERKS_TB_UNROLL
+#define PERKS_TB_UNROLL 1
+#endif
+constexpr int kTbUnroll = PERKS_TB_UNROLL;  // steady-state ticks unrolled (state rotation -> renaming)
 template <typename T, int S> struct TbG {
-  static constexpr int V = 16 / (int)sizeof(T), R = S == SHAPE_3D7 ? 4 : 2, NWARP = 8, NS = PERKS_TB_NS;
+  static constexpr int V = 16 / (int)sizeof(T), R = S == SHAPE_3D7 ? PERKS_TB_R7 : 2;
+  static constexpr int NWARP = S == SHAPE_3D7 ? PERKS_TB_NW7 : 8, NS = PERKS_TB_NS;
   using G = Geo3D<T, V, R, NWARP, NS>;  // compute geometry (IS slot = G::SLOT: TY+2 rows of pitch P)
   static constexpr int TX = G::TX, TY = G::TY, P = G::P, PAD = G::PAD;
   static_assert(PAD >= 2, "two-cell x halo inside the row padding");
@@ -74,9 +94,11 @@ template <typename T, int S> struct TbG {
   static constexpr int HC = (RING + 32 * NHW - 1) / (32 * NHW);
   static constexpr int NCW = NWARP + NHW;  // consumer warps (main + halo)
   static constexpr int NTHR = 32 * (NCW + 1);
+  static constexpr int NI = kTbMbar ? PERKS_TB_NI : 2;  // IS slots
   static constexpr size_t IS_OFF = (size_t)NS * IN_SLOT * sizeof(T);
-  static constexpr size_t BAR_OFF = IS_OFF + 2 * G::SLOT_BYTES;
-  static constexpr size_t SMEM = BAR_OFF + 2 * NS * 8;
+  static constexpr size_t BAR_OFF = IS_OFF + (size_t)NI * G::SLOT_BYTES;
+  // full[NS], empty[NS] (input ring), written[NI] (NCW arrivals), read[NI] (NWARP arrivals)
+  static constexpr size_t SMEM = BAR_OFF + (2 * NS + 2 * NI) * 8;
 };
 
 struct TbMaps {
@@ -191,9 +213,10 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
   T *const is_slots = reinterpret_cast<T *>(sm + B::IS_OFF);
   uint64_t *const bars = reinterpret_cast<uint64_t *>(sm + B::BAR_OFF);
   auto in_slot = [&](unsigned k) { return in_slots + (size_t)(k % B::NS) * B::IN_SLOT; };
-  auto is_slot = [&](int b) { return is_slots + (size_t)b * G::SLOT; };
   auto fullb = [&](unsigned k) { return bars + (k % B::NS); };
   auto emptyb = [&](unsigned k) { return bars + B::NS + (k % B::NS); };
+  auto isw = [&](unsigned q) { return bars + 2 * B::NS + (q % B::NI); };          // IS q written
+  auto isr = [&](unsigned q) { return bars + 2 * B::NS + B::NI + (q % B::NI); };  // IS q read
 
   const int warp = (int)(threadIdx.x >> 5), lane = (int)(threadIdx.x & 31);
   if (threadIdx.x == 0) {
@@ -201,10 +224,14 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
       mbar_init(bars + i, 1);
       mbar_init(bars + B::NS + i, B::NCW);
     }
+    for (int i = 0; i < B::NI; i++) {
+      mbar_init(bars + 2 * B::NS + i, B::NCW);
+      mbar_init(bars + 2 * B::NS + B::NI + i, B::NWARP);
+    }
     mbar_fence_init();
   }
   // zero the IS slots once: cells outside window + ring are never written (nor read for kept cells)
-  for (int i = threadIdx.x; i < 2 * G::SLOT; i += blockDim.x) is_slots[i] = T(0);
+  for (int i = threadIdx.x; i < B::NI * G::SLOT; i += blockDim.x) is_slots[i] = T(0);
   __syncthreads();
 
   const int tiles = u.tx * u.ty;
@@ -213,6 +240,7 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
   const size_t plane = (size_t)d.nx * d.ny;
   const int64_t npass = (steps + 1) / 2;
   unsigned gk = 0;  // input arrivals so far (slot = gk % NS, phase = (gk / NS) & 1)
+  unsigned gi = 0;  // IS planes written so far (kTbMbar: slot = q % NI, phase = (q / NI) & 1)
 
   for (int64_t ps = 0; ps < npass; ps++) {
     const int nst = (ps == 0 && (steps & 1)) ? 1 : 2;
@@ -233,6 +261,31 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
       const int q0 = nst == 2 ? zs - 2 : zs - 1;
       const unsigned k0 = gk;
       gk += (unsigned)nin;
+      const unsigned i0 = gi;  // IS plane of tick k: written i0 + k - 2, read by stage 2 at tick k + 1
+      if (nst == 2) gi += (unsigned)(zc + 2);
+      // IS plane q: slot / wait before writing (its previous use read) / publish / consume
+      auto is_of = [&](unsigned q) { return is_slots + (size_t)(kTbMbar ? q % B::NI : q & 1u) * G::SLOT; };
+      auto is_acquire_w = [&](unsigned q) {
+        if (kTbMbar && q >= (unsigned)B::NI) mbar_wait(isr(q), ((q / B::NI) + 1) & 1u);
+      };
+      auto is_publish = [&](unsigned q) {
+        if constexpr (kTbMbar) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive_release(isw(q));
+        }
+      };
+      auto is_acquire_r = [&](unsigned q) {
+        if constexpr (kTbMbar) mbar_wait(isw(q), (q / B::NI) & 1u);
+      };
+      auto is_done_r = [&](unsigned q) {
+        if constexpr (kTbMbar) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive_release(isr(q));
+        }
+      };
+      auto tick_sync = [&]() {
+        if constexpr (!kTbMbar) tb_consumers_sync<B>();
+      };
       if (warp == B::NCW) {  // ---------------------------------------------------------- producer
         if (lane == 0) {
           if (jj == 0) fence_proxy_async_global();  // previous pass's generic stores -> TMA reads
@@ -295,8 +348,11 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
           T o2[G::R][G::V], c2[G::R][G::V], o1[G::R][G::V], c1[G::R][G::V];
           auto stage2 = [&]() {
             T nb[G::R + 2][G::V + 2];
-            if constexpr (kTbOwn) read_nb_own<T, G>(is_slot((k - 1) & 1), own, nb);
-            else read_nb<T, G>(is_slot((k - 1) & 1), nb);
+            const unsigned q = i0 + (unsigned)(k - 3);
+            is_acquire_r(q);
+            if constexpr (kTbOwn) read_nb_own<T, G>(is_of(q), own, nb);
+            else read_nb<T, G>(is_of(q), nb);
+            is_done_r(q);
             arrival_nb<T, S, G>(s2, nb, c, o2, c2);
           };
           auto stage2_out = [&]() {
@@ -317,7 +373,10 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
           auto stage1_out = [&]() {
             if constexpr (W1) {
               frame_select<T, G>(d, tt, zs - 3 + k, o1, s1.cm1);
-              write_own<T, G>(is_slot(k & 1), o1);
+              const unsigned q = i0 + (unsigned)(k - 2);
+              is_acquire_w(q);
+              write_own<T, G>(is_of(q), o1);
+              is_publish(q);
               if constexpr (kTbOwn) {
 #pragma unroll
                 for (int r = 0; r < G::R; r++)
@@ -349,7 +408,7 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
               stage1_out();
             }
           }
-          tb_consumers_sync<B>();
+          tick_sync();
         };
         using Y = std::true_type;
         using N = std::false_type;
@@ -359,6 +418,7 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
         tick(2, Y{}, N{}, N{}, Y{});
         tick(3, Y{}, Y{}, N{}, Y{});
         tick(4, Y{}, Y{}, N{}, Y{});
+#pragma unroll kTbUnroll
         for (int k = 5; k < zc + 4; k++) tick(k, Y{}, Y{}, Y{}, Y{});
         tick(zc + 4, N{}, Y{}, Y{}, N{});
         continue;
@@ -416,15 +476,18 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
           if (k >= 2) {
             const int o = zs - 3 + k;
             const bool zint = o >= d.zlo && o <= d.zhi;
-            T *is = is_slot(k & 1);
+            const unsigned q = i0 + (unsigned)(k - 2);
+            is_acquire_w(q);
+            T *is = is_of(q);
 #pragma unroll
             for (int j = 0; j < B::HC; j++)
               if ((hmask >> j) & 1u) is[soff[j]] = (zint && !((fmask >> j) & 1u)) ? ho[j] : hs[j].cm1[0][0];
+            is_publish(q);
           }
 #pragma unroll
           for (int j = 0; j < B::HC; j++) hs[j].cm1[0][0] = hc[j];
         }
-        tb_consumers_sync<B>();
+        tick_sync();
       }
     }
     if (ps + 1 < npass) grid_barrier(bar, (unsigned)(ps + 1));
