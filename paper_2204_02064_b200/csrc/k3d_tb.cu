@@ -62,6 +62,26 @@ constexpr bool kTbMbar = PERKS_TB_MBAR != 0;
 #ifndef PERKS_TB_NI
 #define PERKS_TB_NI 3
 #endif
+// Tick order: 1 = stage 1 (input plane -> IS) then stage 2 (previous IS plane -> output); 0 = the reverse.
+#ifndef PERKS_TB_S1FIRST
+#define PERKS_TB_S1FIRST 0
+#endif
+constexpr bool kTbS1First = PERKS_TB_S1FIRST != 0;
+// Halo warps (which finish their tick early) wait with the suspend-hint try_wait (1) instead of
+// polling (0), leaving the issue slots to the main warps.
+#ifndef PERKS_TB_HSLEEP
+#define PERKS_TB_HSLEEP 0
+#endif
+constexpr bool kTbHaloSleep = PERKS_TB_HSLEEP != 0;
+// Stage 2 of the z-major shapes (19/27-point: list = dz -1 terms, then 0, then +1) evaluated
+// directly from three resident IS planes (no accumulator state across ticks: frees the registers
+// of a second set of three accumulators); the 7-point star keeps the arrival form.
+#ifndef PERKS_TB_D2
+#define PERKS_TB_D2 1
+#endif
+#ifndef PERKS_TB_R27
+#define PERKS_TB_R27 4
+#endif
 #ifndef PERKS_TB_NS
 #define PERKS_TB_NS 4
 #endif
@@ -78,8 +98,20 @@ constexpr bool kTbMbar = PERKS_TB_MBAR != 0;
 #define PERKS_TB_UNROLL 1
 #endif
 constexpr int kTbUnroll = PERKS_TB_UNROLL;  // steady-state ticks unrolled (state rotation -> renaming)
+template <int S> constexpr bool z_major() {
+  for (int p = 1; p < Shape<S>::N; p++)
+    if (Shape<S>::dz(p) < Shape<S>::dz(p - 1)) return false;
+  return true;
+}
+template <int S> constexpr int first_dz_at_least(int z) {
+  int p = 0;
+  while (p < Shape<S>::N && Shape<S>::dz(p) < z) p++;
+  return p;
+}
+template <int S> constexpr bool tb_direct2() { return PERKS_TB_D2 != 0 && S != SHAPE_3D7 && z_major<S>(); }
+
 template <typename T, int S> struct TbG {
-  static constexpr int V = 16 / (int)sizeof(T), R = S == SHAPE_3D7 ? PERKS_TB_R7 : 2;
+  static constexpr int V = 16 / (int)sizeof(T), R = S == SHAPE_3D7 ? PERKS_TB_R7 : PERKS_TB_R27;
   static constexpr int NWARP = S == SHAPE_3D7 ? PERKS_TB_NW7 : 8, NS = PERKS_TB_NS;
   using G = Geo3D<T, V, R, NWARP, NS>;  // compute geometry (IS slot = G::SLOT: TY+2 rows of pitch P)
   static constexpr int TX = G::TX, TY = G::TY, P = G::P, PAD = G::PAD;
@@ -94,7 +126,8 @@ template <typename T, int S> struct TbG {
   static constexpr int HC = (RING + 32 * NHW - 1) / (32 * NHW);
   static constexpr int NCW = NWARP + NHW;  // consumer warps (main + halo)
   static constexpr int NTHR = 32 * (NCW + 1);
-  static constexpr int NI = kTbMbar ? PERKS_TB_NI : 2;  // IS slots
+  // IS slots (direct stage 2: three resident + one being written)
+  static constexpr int NI = !kTbMbar ? 2 : (tb_direct2<S>() && PERKS_TB_NI < 4) ? 4 : PERKS_TB_NI;
   static constexpr size_t IS_OFF = (size_t)NS * IN_SLOT * sizeof(T);
   static constexpr size_t BAR_OFF = IS_OFF + (size_t)NI * G::SLOT_BYTES;
   // full[NS], empty[NS] (input ring), written[NI] (NCW arrivals), read[NI] (NWARP arrivals)
@@ -174,6 +207,35 @@ PERKS_DEVINL void read_nb_own(const T *slot, const T (&own)[G::R][G::V], T (&nb)
 #pragma unroll
       for (int i = 0; i < G::V; i++) nb[j][i + 1] = own[j - 1][i];
     }
+  }
+}
+
+// One output plane of a z-major shape from its three input planes (slots of planes o-1, o, o+1),
+// the chain in list order (reading R5), each plane's neighbourhood read once; `cen` = plane o's own
+// cells (the frame rule's old values).
+template <typename T, int S, class G>
+PERKS_DEVINL void direct_plane(const T *sm1, const T *s0, const T *sp1, const Coef<T, Shape<S>::N> &c,
+                               T (&out)[G::R][G::V], T (&cen)[G::R][G::V]) {
+  constexpr int z0 = first_dz_at_least<S>(0), z1 = first_dz_at_least<S>(1);
+  static_assert(z_major<S>() && z0 > 0, "direct_plane: z-major list starting with dz = -1 terms");
+  {
+    T nb[G::R + 2][G::V + 2];
+    read_nb<T, G>(sm1, nb);
+    apply_terms<T, S, G, 0, z0, -1>(out, nb, cen, c);
+  }
+  {
+    T nb[G::R + 2][G::V + 2];
+    read_nb<T, G>(s0, nb);
+#pragma unroll
+    for (int r = 0; r < G::R; r++)
+#pragma unroll
+      for (int i = 0; i < G::V; i++) cen[r][i] = nb[r + 1][i + 1];
+    apply_terms<T, S, G, z0, z1, 0>(out, nb, cen, c);
+  }
+  {
+    T nb[G::R + 2][G::V + 2];
+    read_nb<T, G>(sp1, nb);
+    apply_terms<T, S, G, z1, Shape<S>::N, 1>(out, nb, cen, c);
   }
 }
 
@@ -266,7 +328,10 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
       // IS plane q: slot / wait before writing (its previous use read) / publish / consume
       auto is_of = [&](unsigned q) { return is_slots + (size_t)(kTbMbar ? q % B::NI : q & 1u) * G::SLOT; };
       auto is_acquire_w = [&](unsigned q) {
-        if (kTbMbar && q >= (unsigned)B::NI) mbar_wait(isr(q), ((q / B::NI) + 1) & 1u);
+        if (kTbMbar && q >= (unsigned)B::NI) {
+          if (kTbHaloSleep && warp >= B::NWARP) mbar_wait_sleep(isr(q), ((q / B::NI) + 1) & 1u);
+          else mbar_wait(isr(q), ((q / B::NI) + 1) & 1u);
+        }
       };
       auto is_publish = [&](unsigned q) {
         if constexpr (kTbMbar) {
@@ -311,6 +376,7 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
         s1.zero();
         s2.zero();
         T own[G::R][G::V];  // this thread's cells of the IS plane written last tick
+        T own_next[kTbS1First ? G::R : 1][G::V];  // (stage-1-first order: this tick's, until stage 2 ran)
         T *sp = dst + (size_t)zs * plane + tt.off(d);
         auto store = [&](int o, const T (&v)[G::R][G::V]) {
           if (tt.full) {
@@ -347,23 +413,41 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
           const unsigned kk = k0 + (unsigned)k;
           T o2[G::R][G::V], c2[G::R][G::V], o1[G::R][G::V], c1[G::R][G::V];
           auto stage2 = [&]() {
-            T nb[G::R + 2][G::V + 2];
-            const unsigned q = i0 + (unsigned)(k - 3);
-            is_acquire_r(q);
-            if constexpr (kTbOwn) read_nb_own<T, G>(is_of(q), own, nb);
-            else read_nb<T, G>(is_of(q), nb);
-            is_done_r(q);
-            arrival_nb<T, S, G>(s2, nb, c, o2, c2);
+            if constexpr (tb_direct2<S>()) {  // output plane zs-5+k from IS planes zs-6+k .. zs-4+k
+              if constexpr (ST) {
+                const unsigned qa = i0 + (unsigned)(k - 5);
+                is_acquire_r(qa);
+                is_acquire_r(qa + 1);
+                is_acquire_r(qa + 2);
+                direct_plane<T, S, G>(is_of(qa), is_of(qa + 1), is_of(qa + 2), c, o2, c2);
+                is_done_r(qa);  // plane zs-6+k: its last read
+              }
+            } else {
+              T nb[G::R + 2][G::V + 2];
+              const unsigned q = i0 + (unsigned)(k - 3);
+              is_acquire_r(q);
+              if constexpr (kTbOwn) read_nb_own<T, G>(is_of(q), own, nb);
+              else read_nb<T, G>(is_of(q), nb);
+              is_done_r(q);
+              arrival_nb<T, S, G>(s2, nb, c, o2, c2);
+            }
           };
           auto stage2_out = [&]() {
-            if constexpr (ST) {
-              frame_select<T, G>(d, tt, zs - 5 + k, o2, s2.cm1);
-              store(zs - 5 + k, o2);
+            if constexpr (tb_direct2<S>()) {
+              if constexpr (ST) {
+                frame_select<T, G>(d, tt, zs - 5 + k, o2, c2);
+                store(zs - 5 + k, o2);
+              }
+            } else {
+              if constexpr (ST) {
+                frame_select<T, G>(d, tt, zs - 5 + k, o2, s2.cm1);
+                store(zs - 5 + k, o2);
+              }
+#pragma unroll
+              for (int r = 0; r < G::R; r++)
+#pragma unroll
+                for (int i = 0; i < G::V; i++) s2.cm1[r][i] = c2[r][i];
             }
-#pragma unroll
-            for (int r = 0; r < G::R; r++)
-#pragma unroll
-              for (int i = 0; i < G::V; i++) s2.cm1[r][i] = c2[r][i];
           };
           auto stage1 = [&]() {
             T nb[G::R + 2][G::V + 2];
@@ -381,7 +465,7 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
 #pragma unroll
                 for (int r = 0; r < G::R; r++)
 #pragma unroll
-                  for (int i = 0; i < G::V; i++) own[r][i] = o1[r][i];
+                  for (int i = 0; i < G::V; i++) (kTbS1First ? own_next : own)[r][i] = o1[r][i];
               }
             }
 #pragma unroll
@@ -396,6 +480,26 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
             if constexpr (A1) release(kk);
             if constexpr (A2) stage2_out();
             if constexpr (A1) stage1_out();
+          } else if constexpr (kTbS1First) {
+            // stage 1 first: it needs only the input plane (in flight for several ticks), and the
+            // IS plane stage 2 then reads was published one tick earlier by every warp, so no
+            // warp waits on another's just-finished work within a tick
+            if constexpr (A1) {
+              mbar_wait(fullb(kk), (kk / B::NS) & 1u);
+              stage1();
+              release(kk);
+              stage1_out();
+            }
+            if constexpr (A2) {
+              stage2();
+              stage2_out();
+            }
+            if constexpr (A1 && W1 && kTbOwn) {
+#pragma unroll
+              for (int r = 0; r < G::R; r++)
+#pragma unroll
+                for (int i = 0; i < G::V; i++) own[r][i] = own_next[r][i];
+            }
           } else {  // stage 2 and its store, then the input wait and stage 1
             if constexpr (A2) {
               stage2();
@@ -421,6 +525,10 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
 #pragma unroll kTbUnroll
         for (int k = 5; k < zc + 4; k++) tick(k, Y{}, Y{}, Y{}, Y{});
         tick(zc + 4, N{}, Y{}, Y{}, N{});
+        if constexpr (tb_direct2<S>()) {  // IS planes ze-1, ze: read (as o, o+1) but never as o-1
+          is_done_r(i0 + (unsigned)zc);
+          is_done_r(i0 + (unsigned)zc + 1);
+        }
         continue;
       }
       // ------------------------------------------------------------------------------ halo warps
@@ -456,7 +564,8 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
       for (int k = 0; k < K; k++) {
         if (k < zc + 4) {
           const unsigned kk = k0 + (unsigned)k;
-          mbar_wait(fullb(kk), (kk / B::NS) & 1u);
+          if constexpr (kTbHaloSleep) mbar_wait_sleep(fullb(kk), (kk / B::NS) & 1u);
+          else mbar_wait(fullb(kk), (kk / B::NS) & 1u);
           const T *sl = in_slot(kk);
           T ho[B::HC], hc[B::HC];
 #pragma unroll
