@@ -83,7 +83,7 @@ constexpr bool kTbHaloSleep = PERKS_TB_HSLEEP != 0;
 #define PERKS_TB_R27 4
 #endif
 #ifndef PERKS_TB_TALL_R
-#define PERKS_TB_TALL_R 8
+#define PERKS_TB_TALL_R 5
 #endif
 #ifndef PERKS_TB_TALL_DEFAULT
 #define PERKS_TB_TALL_DEFAULT 0
