@@ -82,13 +82,6 @@ constexpr bool kTbHaloSleep = PERKS_TB_HSLEEP != 0;
 #ifndef PERKS_TB_R27
 #define PERKS_TB_R27 4
 #endif
-#ifndef PERKS_TB_TALL_R
-#define PERKS_TB_TALL_R 5
-#endif
-#ifndef PERKS_TB_TALL_DEFAULT
-#define PERKS_TB_TALL_DEFAULT 0
-#endif
-constexpr int kTbTallDefault = PERKS_TB_TALL_DEFAULT;
 #ifndef PERKS_TB_NS
 #define PERKS_TB_NS 4
 #endif
@@ -610,220 +603,6 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
   }
 }
 
-// ------------------------------------------------------------------------------------------------
-// The tall-tile form for the 7-point star (PERKS_TB_TALL=1): 8 warps own a TX x 64 window (8 rows
-// per thread: the per-tick fixed costs — waits, addressing, row-edge loads — spread over twice the
-// cells), the level t+1 ring is computed by the same warps (one or two scalar cells per thread),
-// and thread 0 issues the TMA boxes itself (no producer / halo warps: 8 warps per CTA leave each
-// thread the full register budget).  Same ticks, IS ring and frame rule as tb3d_kernel.
-template <typename T> struct TbTall {
-  static constexpr int V = 16 / (int)sizeof(T), R = PERKS_TB_TALL_R, NWARP = 8, NS = 3, NI = 2;
-  using G = Geo3D<T, V, R, NWARP, NS>;
-  static constexpr int TX = G::TX, TY = G::TY, P = G::P, PAD = G::PAD;
-  static constexpr int RI = TY + 4;
-  static constexpr int IN_SLOT = (RI * P * (int)sizeof(T) + 127) / 128 * 128 / (int)sizeof(T);
-  static constexpr unsigned IN_BOX_BYTES = (unsigned)(RI * P * sizeof(T));
-  static constexpr int RING = 2 * (TX + 2) + 2 * TY;
-  static constexpr int HC = (RING + 32 * NWARP - 1) / (32 * NWARP);
-  static constexpr int NTHR = 32 * NWARP;
-  static constexpr size_t IS_OFF = (size_t)NS * IN_SLOT * sizeof(T);
-  static constexpr size_t BAR_OFF = IS_OFF + (size_t)NI * G::SLOT_BYTES;
-  static constexpr size_t SMEM = BAR_OFF + (2 * NS + 2 * NI) * 8;
-};
-
-template <typename T, int S>
-__global__ void __launch_bounds__(TbTall<T>::NTHR, 1)
-    tb3d_tall_kernel(const T *__restrict__ in, T *out, T *tmp, const __grid_constant__ TbMaps maps, Dom3 d,
-                     TbUnits u, int64_t steps, unsigned *bar, Coef<T, Shape<S>::N> c) {
-  using B = TbTall<T>;
-  using G = typename B::G;
-  unsigned char *sm = dyn_smem();
-  T *const in_slots = reinterpret_cast<T *>(sm);
-  T *const is_slots = reinterpret_cast<T *>(sm + B::IS_OFF);
-  uint64_t *const bars = reinterpret_cast<uint64_t *>(sm + B::BAR_OFF);
-  auto in_slot = [&](unsigned k) { return in_slots + (size_t)(k % B::NS) * B::IN_SLOT; };
-  auto fullb = [&](unsigned k) { return bars + (k % B::NS); };
-  auto emptyb = [&](unsigned k) { return bars + B::NS + (k % B::NS); };
-  auto isw = [&](unsigned q) { return bars + 2 * B::NS + (q % B::NI); };
-  auto isr = [&](unsigned q) { return bars + 2 * B::NS + B::NI + (q % B::NI); };
-  auto is_of = [&](unsigned q) { return is_slots + (size_t)(q % B::NI) * G::SLOT; };
-  const int warp = (int)(threadIdx.x >> 5), lane = (int)(threadIdx.x & 31);
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < B::NS; i++) {
-      mbar_init(bars + i, 1);
-      mbar_init(bars + B::NS + i, B::NWARP);
-    }
-    for (int i = 0; i < B::NI; i++) {
-      mbar_init(bars + 2 * B::NS + i, B::NWARP);
-      mbar_init(bars + 2 * B::NS + B::NI + i, B::NWARP);
-    }
-    mbar_fence_init();
-  }
-  for (int i = threadIdx.x; i < B::NI * G::SLOT; i += blockDim.x) is_slots[i] = T(0);
-  __syncthreads();
-
-  const int tiles = u.tx * u.ty;
-  const int nunits = tiles * u.nzc;
-  const int nmine = (int)blockIdx.x < nunits ? (nunits - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-  const size_t plane = (size_t)d.nx * d.ny;
-  const int64_t npass = (steps + 1) / 2;
-  unsigned gk = 0, gi = 0;
-  auto warp_arrive = [&](uint64_t *b) {
-    __syncwarp();
-    if (lane == 0) mbar_arrive_release(b);
-  };
-
-  for (int64_t ps = 0; ps < npass; ps++) {
-    const int nst = (ps == 0 && (steps & 1)) ? 1 : 2;
-    const bool src_out = ps > 0 && ((npass - ps) & 1) == 0;
-    const int src_idx = ps == 0 ? 0 : (src_out ? 1 : 2);
-    T *dst = ((npass - 1 - ps) & 1) == 0 ? out : tmp;
-    const bool rev = u.rev && (ps & 1);
-    if (threadIdx.x == 0) fence_proxy_async_global();  // previous pass's generic stores -> TMA reads
-    for (int jj = 0; jj < nmine; jj++) {
-      const int j = rev ? nmine - 1 - jj : jj;
-      const int id = (int)blockIdx.x + j * (int)gridDim.x;
-      const int t = id % tiles, zci = id / tiles;
-      const int x0 = (t % u.tx) * B::TX, y0 = (t / u.tx) * B::TY;
-      const int zs = zci * u.zc, ze = min(zs + u.zc, d.nz);
-      const int zc = ze - zs;
-      const int nin = nst == 2 ? zc + 4 : zc + 2;
-      const int q0 = nst == 2 ? zs - 2 : zs - 1;
-      const unsigned k0 = gk, i0 = gi;
-      gk += (unsigned)nin;
-      if (nst == 2) gi += (unsigned)(zc + 2);
-      // thread 0: arrival a of this unit into the ring (its slot's previous use released by all warps)
-      auto issue = [&](int a) {
-        if (threadIdx.x == 0 && a < nin) {
-          const unsigned kk = k0 + (unsigned)a;
-          if (kk >= (unsigned)B::NS) mbar_wait(emptyb(kk), ((kk / B::NS) + 1) & 1u);
-          fence_proxy_async();
-          mbar_arrive_tx(fullb(kk), B::IN_BOX_BYTES);
-          tma_load_3d(in_slot(kk), &maps.m[src_idx], x0 - B::PAD, y0 - 2, q0 + a, fullb(kk));
-        }
-      };
-      for (int a = 0; a < B::NS - 1; a++) issue(a);
-      ThreadTile<G> tt;
-      tt.init(d, x0, y0);
-      StreamState<T, G> s1, s2;
-      s1.zero();
-      s2.zero();
-      T *sp = dst + (size_t)zs * plane + tt.off(d);
-      auto store = [&](int o, const T (&v)[G::R][G::V]) {
-        if (tt.full) {
-#pragma unroll
-          for (int r = 0; r < G::R; r++) vstore<T, G::V>(sp + (size_t)r * d.nx, v[r]);
-        } else {
-          store_cells<T, G>(dst, d, tt, o, v);
-        }
-        sp += plane;
-      };
-      if (nst == 1) {
-        for (int k = 0; k < nin; k++) {
-          issue(k + B::NS - 1);
-          const unsigned kk = k0 + (unsigned)k;
-          mbar_wait(fullb(kk), (kk / B::NS) & 1u);
-          T o1[G::R][G::V], c1[G::R][G::V];
-          arrival<T, S, G>(s1, in_slot(kk) + G::P, c, o1, c1);
-          warp_arrive(emptyb(kk));
-          if (k >= 2) {
-            frame_select<T, G>(d, tt, zs - 2 + k, o1, s1.cm1);
-            store(zs - 2 + k, o1);
-          }
-#pragma unroll
-          for (int r = 0; r < G::R; r++)
-#pragma unroll
-            for (int i = 0; i < G::V; i++) s1.cm1[r][i] = c1[r][i];
-        }
-        continue;
-      }
-      // ring cells of level t+1 owned by this thread (HC slots, most threads one)
-      int ioff[B::HC], soff[B::HC];
-      unsigned hmask = 0, fmask = 0;
-#pragma unroll
-      for (int h = 0; h < B::HC; h++) {
-        const int cc = (int)threadIdx.x + h * B::NTHR;
-        int hx, hy;
-        if (cc < B::TX + 2) { hx = cc - 1; hy = -1; }
-        else if (cc < 2 * (B::TX + 2)) { hx = cc - (B::TX + 2) - 1; hy = B::TY; }
-        else if (cc < 2 * (B::TX + 2) + B::TY) { hx = -1; hy = cc - 2 * (B::TX + 2); }
-        else { hx = B::TX; hy = cc - 2 * (B::TX + 2) - B::TY; }
-        ioff[h] = (hy + 2) * B::P + B::PAD + hx;
-        soff[h] = (hy + 1) * B::P + B::PAD + hx;
-        hmask |= (unsigned)(cc < B::RING) << h;
-        const int gx = x0 + hx, gy = y0 + hy;
-        fmask |= (unsigned)!(gx >= 1 && gx <= d.nx - 2 && gy >= 1 && gy <= d.ny - 2) << h;
-      }
-      StreamState<T, G11> hs[B::HC];
-#pragma unroll
-      for (int h = 0; h < B::HC; h++) hs[h].zero();
-      const int K = zc + 5;
-      for (int k = 0; k < K; k++) {
-        if (k >= 3) {  // stage 2: IS plane i0 + k - 3 (written last tick by every warp)
-          const unsigned q = i0 + (unsigned)(k - 3);
-          mbar_wait(isw(q), (q / B::NI) & 1u);
-          issue(k + B::NS - 1);  // (every warp has released arrival k-1: it published IS q after)
-          T o2[G::R][G::V], c2[G::R][G::V];
-          arrival<T, S, G>(s2, is_of(q), c, o2, c2);
-          warp_arrive(isr(q));
-          if (k >= 5) {
-            frame_select<T, G>(d, tt, zs - 5 + k, o2, s2.cm1);
-            store(zs - 5 + k, o2);
-          }
-#pragma unroll
-          for (int r = 0; r < G::R; r++)
-#pragma unroll
-            for (int i = 0; i < G::V; i++) s2.cm1[r][i] = c2[r][i];
-        } else {
-          issue(k + B::NS - 1);
-        }
-        if (k < zc + 4) {  // stage 1: input plane zs-2+k, window cells and ring cells
-          const unsigned kk = k0 + (unsigned)k;
-          mbar_wait(fullb(kk), (kk / B::NS) & 1u);
-          const T *sl = in_slot(kk);
-          T o1[G::R][G::V], c1[G::R][G::V];
-          arrival<T, S, G>(s1, sl + G::P, c, o1, c1);
-          T ho[B::HC], hc[B::HC];
-#pragma unroll
-          for (int h = 0; h < B::HC; h++) {
-            if ((hmask >> h) & 1u) {
-              T nb[3][3];
-#pragma unroll
-              for (int dy = 0; dy < 3; dy++)
-#pragma unroll
-                for (int dx = 0; dx < 3; dx++) nb[dy][dx] = sl[ioff[h] + (dy - 1) * B::P + dx - 1];
-              arrival_cell<T, S>(hs[h], nb, c, ho[h], hc[h]);
-            } else {
-              ho[h] = hc[h] = T(0);
-            }
-          }
-          warp_arrive(emptyb(kk));
-          if (k >= 2) {
-            const unsigned q = i0 + (unsigned)(k - 2);
-            if (q >= (unsigned)B::NI) mbar_wait(isr(q), ((q / B::NI) + 1) & 1u);
-            T *is = is_of(q);
-            frame_select<T, G>(d, tt, zs - 3 + k, o1, s1.cm1);
-            write_own<T, G>(is, o1);
-            const int o = zs - 3 + k;
-            const bool zint = o >= d.zlo && o <= d.zhi;
-#pragma unroll
-            for (int h = 0; h < B::HC; h++)
-              if ((hmask >> h) & 1u) is[soff[h]] = (zint && !((fmask >> h) & 1u)) ? ho[h] : hs[h].cm1[0][0];
-            warp_arrive(isw(q));
-          }
-#pragma unroll
-          for (int r = 0; r < G::R; r++)
-#pragma unroll
-            for (int i = 0; i < G::V; i++) s1.cm1[r][i] = c1[r][i];
-#pragma unroll
-          for (int h = 0; h < B::HC; h++) hs[h].cm1[0][0] = hc[h];
-        }
-      }
-    }
-    if (ps + 1 < npass) grid_barrier(bar, (unsigned)(ps + 1));
-  }
-}
-
 namespace {
 template <typename T> void *tb_kernel(int shape) {
   return shape == SHAPE_3D7    ? (void *)tb3d_kernel<T, SHAPE_3D7>
@@ -836,10 +615,6 @@ struct TbInfo {
 };
 template <typename T, int S> TbInfo tb_info_s() {
   using B = TbG<T, S>;
-  return TbInfo{B::TX, B::TY, B::NTHR, B::P, B::RI, B::SMEM};
-}
-template <typename T> TbInfo tb_info_tall() {
-  using B = TbTall<T>;
   return TbInfo{B::TX, B::TY, B::NTHR, B::P, B::RI, B::SMEM};
 }
 template <typename T> TbInfo tb_info(int shape) {
@@ -858,14 +633,10 @@ Plan plan_tb3d(const Problem &p) {
   }
   if (!use_tma3(p)) { pl.why = "tb3d: needs TMA (nx*S % 16 == 0)"; return pl; }
   const bool f32 = p.dtype == PERKS_F32;
-  // tall-tile form for the 7-point star (8 warps x 8 rows, no producer / halo warps): PERKS_TB_TALL=1
-  const bool tall = p.shape == SHAPE_3D7 && env_int("PERKS_TB_TALL", kTbTallDefault) != 0;
-  const TbInfo ti = tall ? (f32 ? tb_info_tall<float>() : tb_info_tall<double>())
-                         : (f32 ? tb_info<float>(p.shape) : tb_info<double>(p.shape));
+  const TbInfo ti = f32 ? tb_info<float>(p.shape) : tb_info<double>(p.shape);
   const int TX = ti.TX, TY = ti.TY, NT = ti.NT;
   const size_t smem = ti.smem;
-  void *k = tall ? (f32 ? (void *)tb3d_tall_kernel<float, SHAPE_3D7> : (void *)tb3d_tall_kernel<double, SHAPE_3D7>)
-                 : (f32 ? tb_kernel<float>(p.shape) : tb_kernel<double>(p.shape));
+  void *k = f32 ? tb_kernel<float>(p.shape) : tb_kernel<double>(p.shape);
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
     cudaGetLastError();
     pl.why = "tb3d: cudaFuncSetAttribute";
@@ -901,7 +672,7 @@ Plan plan_tb3d(const Problem &p) {
   pl.tile[0] = TX; pl.tile[1] = TY; pl.tile[2] = zc;
   pl.regs = fa.numRegs;
   pl.smem = (int)smem;
-  pl.cfg = tall ? 2 : 1;
+  pl.cfg = 1;
   pl.family = 7;  // (3D PERKS, two time steps per pass)
   const double S = (double)p.elem();
   pl.cached_smem = 0;  // level t+1 is on chip only while its planes are in flight (no resident cells)
@@ -910,14 +681,14 @@ Plan plan_tb3d(const Problem &p) {
   const int RI = ti.RI, PB = ti.P;
   pl.halo_bytes_step = 0.5 * S * (double)(RI * PB - TX * TY) * (double)tiles * (double)(p.nz + 4 * nzc);
   pl.ws_bytes = align256((size_t)p.cells() * p.elem()) + 256;
-  snprintf(pl.name, sizeof(pl.name), "perks3d_tb2%s_%s_%s_t%dx%d_z%d", tall ? "_tall" : "",
+  snprintf(pl.name, sizeof(pl.name), "perks3d_tb2_%s_%s_t%dx%d_z%d",
            p.shape == SHAPE_3D7 ? "7pt" : p.shape == SHAPE_3D19 ? "19pt" : "27pt", f32 ? "f32" : "f64", TX, TY, zc);
   pl.ok = true;
   return pl;
 }
 
 namespace {
-template <typename T, int S, class B, bool TALL>
+template <typename T, int S, class B>
 cudaError_t launch_tb_g(const Problem &p, const Plan &pl, const T *in, T *out, void *ws, int64_t steps,
                         cudaStream_t s) {
   Coef<T, Shape<S>::N> c;
@@ -936,9 +707,7 @@ cudaError_t launch_tb_g(const Problem &p, const Plan &pl, const T *in, T *out, v
     if (!encode_map3(&maps.m[i], p, b[i], B::P, B::RI)) return cudaErrorInvalidValue;
   cudaError_t e = reset_grid_barrier(bar, s);
   if (e != cudaSuccess) return e;
-  void *k;
-  if constexpr (TALL) k = (void *)tb3d_tall_kernel<T, S>;
-  else k = (void *)tb3d_kernel<T, S>;
+  void *k = (void *)tb3d_kernel<T, S>;
   void *args[] = {(void *)&in, (void *)&out, (void *)&tmp, (void *)&maps, (void *)&d, (void *)&u,
                   (void *)&steps, (void *)&bar, (void *)&c};
   cudaLaunchConfig_t cfg = {};
@@ -957,9 +726,7 @@ cudaError_t launch_tb_g(const Problem &p, const Plan &pl, const T *in, T *out, v
 template <typename T, int S>
 cudaError_t launch_tb(const Problem &p, const Plan &pl, const T *in, T *out, void *ws, int64_t steps,
                       cudaStream_t s) {
-  if constexpr (S == SHAPE_3D7)
-    if (pl.cfg == 2) return launch_tb_g<T, S, TbTall<T>, true>(p, pl, in, out, ws, steps, s);
-  return launch_tb_g<T, S, TbG<T, S>, false>(p, pl, in, out, ws, steps, s);
+  return launch_tb_g<T, S, TbG<T, S>>(p, pl, in, out, ws, steps, s);
 }
 }  // namespace
 
