@@ -11,7 +11,11 @@
  *                        device-wide barrier between steps (Fig. 3 right);
  *   PERKS_PERKS      (c) (b) plus caching of the domain in registers and shared memory across
  *                        steps, halo-only re-reads through L2 (§3.3 P:342-356,
- *                        Fig. 6).
+ *                        Fig. 6).  For 3D domains beyond the on-chip capacity the
+ *                        7-point star's plan keeps the next time level of the planes in flight on
+ *                        chip instead and advances two steps per pass over the domain (Tiled
+ *                        PERKS in streaming form, [draft] P:416-441, reading R15;
+ *                        kernel names perks3d_tb2_*; dram_bytes_per_step = S·cells).
  * All variants produce bit-identical results (the scheme "does not touch on the compute part",
  * P:285): each cell is  acc = w_0*x(c+d_0) rounded, then acc = fma(w_p, x(c+d_p), acc)
  * in list order (reading R5), in the storage dtype (R6).
