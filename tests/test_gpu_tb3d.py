@@ -75,3 +75,17 @@ def test_tb3d_random_weights_and_default(dtype):
         ref = oracle.run(u0, offs, w, T, nthreads=4)
         _check(_run_gpu(u0, "3d7pt", w, T, "perks"), ref, u0, dtype)
         _check(_run_gpu(u0, "3d7pt", w, T, "auto"), ref, u0, dtype)
+
+
+def test_tb3d_grid_barrier_counter_wrap(monkeypatch):
+    """The pass barrier's 32-bit counter wraps mid-run (started 700 below 2^32; 96 CTAs x 11 pass
+    barriers) and the two-steps-per-pass run stays bit-exact."""
+    _need_gpu()
+    monkeypatch.setenv("PERKS_TEST_BAR_BASE", str(2**32 - 700))
+    shape = (64, 96, 128)
+    q = _kernel("3d7pt", shape, np.float64)
+    assert q["kernel"].startswith("perks3d_tb2") and q["grid"] * 11 > 700, q
+    u0 = si.field(shape, dtype=np.float64, seed=1111)
+    offs, w = si.preset("3d7pt")
+    ref = oracle.run(u0, offs, w, 24, nthreads=8)
+    _check(_run_gpu(u0, "3d7pt", w, 24, "perks"), ref, u0, np.float64)
