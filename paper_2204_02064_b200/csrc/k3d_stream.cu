@@ -330,17 +330,25 @@ bool tma_available() {
 }
 
 // 3D map of a dense [nz][ny][nx] buffer with box {bx, by, 1}; OOB cells read as zero.
-bool encode_map3(CUtensorMap *m, const Problem &p, const void *base, int bx, int by) {
+bool encode_map3(CUtensorMap *m, const Problem &p, const void *base, int bx, int by, int promo) {
   if (!tma_available()) return false;
   const cuuint64_t dims[3] = {(cuuint64_t)p.nx, (cuuint64_t)p.ny, (cuuint64_t)p.nz};
   const cuuint64_t strides[2] = {(cuuint64_t)(p.nx * p.elem()), (cuuint64_t)(p.nx * p.ny * p.elem())};
   const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
   const cuuint32_t es[3] = {1, 1, 1};
+  const CUtensorMapL2promotion pr = promo == 0    ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                    : promo == 64  ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                    : promo == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                   : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   CUresult r = g_encode(m, p.dtype == PERKS_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                         3, const_cast<void *>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        CU_TENSOR_MAP_SWIZZLE_NONE, pr, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+// L2 promotion of the box fetches: 256 B (sweeps: PERKS_TMA_L2PROMO = 0 / 64 / 128 / 256 bytes)
+bool encode_map3(CUtensorMap *m, const Problem &p, const void *base, int bx, int by) {
+  return encode_map3(m, p, base, bx, by, env_int("PERKS_TMA_L2PROMO", 256));
 }
 
 // TMA needs 16-byte aligned row strides (and 16-byte aligned bases, checked by run()).

@@ -39,7 +39,7 @@
 namespace perks {
 
 bool use_tma3(const Problem &p);
-bool encode_map3(CUtensorMap *m, const Problem &p, const void *base, int bx, int by);
+bool encode_map3(CUtensorMap *m, const Problem &p, const void *base, int bx, int by, int promo);
 
 // Stage 2 takes its own cells from registers (1) or re-reads them from the IS slot (0: fewer live
 // registers).
@@ -703,8 +703,11 @@ cudaError_t launch_tb_g(const Problem &p, const Plan &pl, const T *in, T *out, v
   TbMaps maps;
   std::memset(&maps, 0, sizeof(maps));
   const void *b[3] = {in, out, tmp};
+  // 64-byte L2 promotion: a box's two-cell x halo then costs one 64-B granule per row edge instead
+  // of a 256-B block (C5: DRAM reads 1.40 -> 1.12 x S·cells per step, profiles/r02_tb3d_l2promo.txt)
+  const int promo = env_int("PERKS_TMA_L2PROMO", 64);
   for (int i = 0; i < 3; i++)
-    if (!encode_map3(&maps.m[i], p, b[i], B::P, B::RI)) return cudaErrorInvalidValue;
+    if (!encode_map3(&maps.m[i], p, b[i], B::P, B::RI, promo)) return cudaErrorInvalidValue;
   cudaError_t e = reset_grid_barrier(bar, s);
   if (e != cudaSuccess) return e;
   void *k = (void *)tb3d_kernel<T, S>;
