@@ -67,6 +67,13 @@ constexpr bool kTbMbar = PERKS_TB_MBAR != 0;
 #define PERKS_TB_S1FIRST 0
 #endif
 constexpr bool kTbS1First = PERKS_TB_S1FIRST != 0;
+// fp64: stage 1 first with stage 2's own cells re-read from the IS slot (PERKS_TB_F64_S1FIRST=1,
+// measured 4 % faster on C3, profiles/r02_tb3d_variants4.txt "s1o0"; fp32 spills in that form)
+#ifndef PERKS_TB_F64_S1FIRST
+#define PERKS_TB_F64_S1FIRST 1
+#endif
+template <typename T> constexpr bool tb_s1first() { return sizeof(T) == 8 ? PERKS_TB_F64_S1FIRST != 0 : kTbS1First; }
+template <typename T> constexpr bool tb_own() { return sizeof(T) == 8 && PERKS_TB_F64_S1FIRST != 0 ? false : kTbOwn; }
 // Halo warps (which finish their tick early) wait with the suspend-hint try_wait (1) instead of
 // polling (0), leaving the issue slots to the main warps.
 #ifndef PERKS_TB_HSLEEP
@@ -376,7 +383,7 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
         s1.zero();
         s2.zero();
         T own[G::R][G::V];  // this thread's cells of the IS plane written last tick
-        T own_next[kTbS1First ? G::R : 1][G::V];  // (stage-1-first order: this tick's, until stage 2 ran)
+        T own_next[tb_s1first<T>() ? G::R : 1][G::V];  // (stage-1-first order: this tick's, until stage 2 ran)
         T *sp = dst + (size_t)zs * plane + tt.off(d);
         auto store = [&](int o, const T (&v)[G::R][G::V]) {
           if (tt.full) {
@@ -426,7 +433,7 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
               T nb[G::R + 2][G::V + 2];
               const unsigned q = i0 + (unsigned)(k - 3);
               is_acquire_r(q);
-              if constexpr (kTbOwn) read_nb_own<T, G>(is_of(q), own, nb);
+              if constexpr (tb_own<T>()) read_nb_own<T, G>(is_of(q), own, nb);
               else read_nb<T, G>(is_of(q), nb);
               is_done_r(q);
               arrival_nb<T, S, G>(s2, nb, c, o2, c2);
@@ -461,11 +468,11 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
               is_acquire_w(q);
               write_own<T, G>(is_of(q), o1);
               is_publish(q);
-              if constexpr (kTbOwn) {
+              if constexpr (tb_own<T>()) {
 #pragma unroll
                 for (int r = 0; r < G::R; r++)
 #pragma unroll
-                  for (int i = 0; i < G::V; i++) (kTbS1First ? own_next : own)[r][i] = o1[r][i];
+                  for (int i = 0; i < G::V; i++) (tb_s1first<T>() ? own_next : own)[r][i] = o1[r][i];
               }
             }
 #pragma unroll
@@ -480,7 +487,7 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
             if constexpr (A1) release(kk);
             if constexpr (A2) stage2_out();
             if constexpr (A1) stage1_out();
-          } else if constexpr (kTbS1First) {
+          } else if constexpr (tb_s1first<T>()) {
             // stage 1 first: it needs only the input plane (in flight for several ticks), and the
             // IS plane stage 2 then reads was published one tick earlier by every warp, so no
             // warp waits on another's just-finished work within a tick
@@ -494,7 +501,7 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
               stage2();
               stage2_out();
             }
-            if constexpr (A1 && W1 && kTbOwn) {
+            if constexpr (A1 && W1 && tb_own<T>()) {
 #pragma unroll
               for (int r = 0; r < G::R; r++)
 #pragma unroll
