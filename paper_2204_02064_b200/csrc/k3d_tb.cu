@@ -47,18 +47,6 @@ bool encode_map3(CUtensorMap *m, const Problem &p, const void *base, int bx, int
 #define PERKS_TB_OWN 1
 #endif
 constexpr bool kTbOwn = PERKS_TB_OWN != 0;
-// 1: both stages' loads and FMA chains in one basic block per tick (after the input wait);
-// 0: stage 2 with its store, then the input wait and stage 1.
-#ifndef PERKS_TB_FUSE
-#define PERKS_TB_FUSE 0
-#endif
-constexpr bool kTbFuse = PERKS_TB_FUSE != 0;
-// Intermediate (IS) planes: 1 = an NI-slot ring with per-slot written / read mbarriers (warps drift
-// up to NI-2 ticks apart); 0 = two slots and one named barrier over the consumer warps per tick.
-#ifndef PERKS_TB_MBAR
-#define PERKS_TB_MBAR 1
-#endif
-constexpr bool kTbMbar = PERKS_TB_MBAR != 0;
 #ifndef PERKS_TB_NI
 #define PERKS_TB_NI 3
 #endif
@@ -74,12 +62,6 @@ constexpr bool kTbS1First = PERKS_TB_S1FIRST != 0;
 #endif
 template <typename T> constexpr bool tb_s1first() { return sizeof(T) == 8 ? PERKS_TB_F64_S1FIRST != 0 : kTbS1First; }
 template <typename T> constexpr bool tb_own() { return sizeof(T) == 8 && PERKS_TB_F64_S1FIRST != 0 ? false : kTbOwn; }
-// Halo warps (which finish their tick early) wait with the suspend-hint try_wait (1) instead of
-// polling (0), leaving the issue slots to the main warps.
-#ifndef PERKS_TB_HSLEEP
-#define PERKS_TB_HSLEEP 0
-#endif
-constexpr bool kTbHaloSleep = PERKS_TB_HSLEEP != 0;
 // Stage 2 of the z-major shapes (19/27-point: list = dz -1 terms, then 0, then +1) evaluated
 // directly from three resident IS planes (no accumulator state across ticks: frees the registers
 // of a second set of three accumulators); the 7-point star keeps the arrival form.
@@ -101,10 +83,6 @@ constexpr bool kTbHaloSleep = PERKS_TB_HSLEEP != 0;
 #ifndef PERKS_TB_NW7
 #define PERKS_TB_NW7 8
 #endif
-#ifndef PERKS_TB_UNROLL
-#define PERKS_TB_UNROLL 1
-#endif
-constexpr int kTbUnroll = PERKS_TB_UNROLL;  // steady-state ticks unrolled (state rotation -> renaming)
 template <int S> constexpr bool z_major() {
   for (int p = 1; p < Shape<S>::N; p++)
     if (Shape<S>::dz(p) < Shape<S>::dz(p - 1)) return false;
@@ -134,7 +112,7 @@ template <typename T, int S> struct TbG {
   static constexpr int NCW = NWARP + NHW;  // consumer warps (main + halo)
   static constexpr int NTHR = 32 * (NCW + 1);
   // IS slots (direct stage 2: three resident + one being written)
-  static constexpr int NI = !kTbMbar ? 2 : (tb_direct2<S>() && PERKS_TB_NI < 4) ? 4 : PERKS_TB_NI;
+  static constexpr int NI = (tb_direct2<S>() && PERKS_TB_NI < 4) ? 4 : PERKS_TB_NI;
   static constexpr size_t IS_OFF = (size_t)NS * IN_SLOT * sizeof(T);
   static constexpr size_t BAR_OFF = IS_OFF + (size_t)NI * G::SLOT_BYTES;
   // full[NS], empty[NS] (input ring), written[NI] (NCW arrivals), read[NI] (NWARP arrivals)
@@ -188,10 +166,6 @@ PERKS_DEVINL void mbar_wait_sleep(uint64_t *b, unsigned parity) {
       "}\n" ::"r"(smem_u32(b)),
       "r"(parity), "l"((unsigned long long)PERKS_WATCHDOG_NS), "r"(20000u)
       : "memory");
-}
-
-template <class B> PERKS_DEVINL void tb_consumers_sync() {
-  asm volatile("bar.sync 1, %0;\n" ::"n"(32 * B::NCW) : "memory");
 }
 
 // Stage 2's input neighbourhood: the thread's own R x V cells of the IS plane are the level t+1
@@ -309,7 +283,7 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
   const size_t plane = (size_t)d.nx * d.ny;
   const int64_t npass = (steps + 1) / 2;
   unsigned gk = 0;  // input arrivals so far (slot = gk % NS, phase = (gk / NS) & 1)
-  unsigned gi = 0;  // IS planes written so far (kTbMbar: slot = q % NI, phase = (q / NI) & 1)
+  unsigned gi = 0;  // IS planes written so far (slot = q % NI, phase = (q / NI) & 1)
 
   for (int64_t ps = 0; ps < npass; ps++) {
     const int nst = (ps == 0 && (steps & 1)) ? 1 : 2;
@@ -333,30 +307,20 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
       const unsigned i0 = gi;  // IS plane of tick k: written i0 + k - 2, read by stage 2 at tick k + 1
       if (nst == 2) gi += (unsigned)(zc + 2);
       // IS plane q: slot / wait before writing (its previous use read) / publish / consume
-      auto is_of = [&](unsigned q) { return is_slots + (size_t)(kTbMbar ? q % B::NI : q & 1u) * G::SLOT; };
+      auto is_of = [&](unsigned q) { return is_slots + (size_t)(q % B::NI) * G::SLOT; };
       auto is_acquire_w = [&](unsigned q) {
-        if (kTbMbar && q >= (unsigned)B::NI) {
-          if (kTbHaloSleep && warp >= B::NWARP) mbar_wait_sleep(isr(q), ((q / B::NI) + 1) & 1u);
-          else mbar_wait(isr(q), ((q / B::NI) + 1) & 1u);
-        }
+        if (q >= (unsigned)B::NI) mbar_wait(isr(q), ((q / B::NI) + 1) & 1u);
       };
       auto is_publish = [&](unsigned q) {
-        if constexpr (kTbMbar) {
-          __syncwarp();
-          if (lane == 0) mbar_arrive_release(isw(q));
-        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_release(isw(q));
       };
       auto is_acquire_r = [&](unsigned q) {
-        if constexpr (kTbMbar) mbar_wait(isw(q), (q / B::NI) & 1u);
+        mbar_wait(isw(q), (q / B::NI) & 1u);
       };
       auto is_done_r = [&](unsigned q) {
-        if constexpr (kTbMbar) {
-          __syncwarp();
-          if (lane == 0) mbar_arrive_release(isr(q));
-        }
-      };
-      auto tick_sync = [&]() {
-        if constexpr (!kTbMbar) tb_consumers_sync<B>();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_release(isr(q));
       };
       if (warp == B::NCW) {  // ---------------------------------------------------------- producer
         if (lane == 0) {
@@ -413,7 +377,7 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
           continue;
         }
         // One tick: stage 2 on the IS plane written last tick (A2; ST: store its output), stage 1 on
-        // input plane zs-2+k (A1; W1: write its output to the IS slot); order per kTbFuse.
+        // input plane zs-2+k (A1; W1: write its output to the IS slot); order per tb_s1first.
         auto tick = [&](int k, auto a1, auto a2, auto st, auto w1) {
           constexpr bool A1 = decltype(a1)::value, A2 = decltype(a2)::value;
           constexpr bool ST = decltype(st)::value, W1 = decltype(w1)::value;
@@ -480,14 +444,7 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
 #pragma unroll
               for (int i = 0; i < G::V; i++) s1.cm1[r][i] = c1[r][i];
           };
-          if constexpr (kTbFuse) {  // input wait, both stages in one basic block, then outputs
-            if constexpr (A1) mbar_wait(fullb(kk), (kk / B::NS) & 1u);
-            if constexpr (A2) stage2();
-            if constexpr (A1) stage1();
-            if constexpr (A1) release(kk);
-            if constexpr (A2) stage2_out();
-            if constexpr (A1) stage1_out();
-          } else if constexpr (tb_s1first<T>()) {
+          if constexpr (tb_s1first<T>()) {
             // stage 1 first: it needs only the input plane (in flight for several ticks), and the
             // IS plane stage 2 then reads was published one tick earlier by every warp, so no
             // warp waits on another's just-finished work within a tick
@@ -519,7 +476,6 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
               stage1_out();
             }
           }
-          tick_sync();
         };
         using Y = std::true_type;
         using N = std::false_type;
@@ -529,7 +485,6 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
         tick(2, Y{}, N{}, N{}, Y{});
         tick(3, Y{}, Y{}, N{}, Y{});
         tick(4, Y{}, Y{}, N{}, Y{});
-#pragma unroll kTbUnroll
         for (int k = 5; k < zc + 4; k++) tick(k, Y{}, Y{}, Y{}, Y{});
         tick(zc + 4, N{}, Y{}, Y{}, N{});
         if constexpr (tb_direct2<S>()) {  // IS planes ze-1, ze: read (as o, o+1) but never as o-1
@@ -571,8 +526,7 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
       for (int k = 0; k < K; k++) {
         if (k < zc + 4) {
           const unsigned kk = k0 + (unsigned)k;
-          if constexpr (kTbHaloSleep) mbar_wait_sleep(fullb(kk), (kk / B::NS) & 1u);
-          else mbar_wait(fullb(kk), (kk / B::NS) & 1u);
+          mbar_wait(fullb(kk), (kk / B::NS) & 1u);
           const T *sl = in_slot(kk);
           T ho[B::HC], hc[B::HC];
 #pragma unroll
@@ -603,7 +557,6 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
 #pragma unroll
           for (int j = 0; j < B::HC; j++) hs[j].cm1[0][0] = hc[j];
         }
-        tick_sync();
       }
     }
     if (ps + 1 < npass) grid_barrier(bar, (unsigned)(ps + 1));
