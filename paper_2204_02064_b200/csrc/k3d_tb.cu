@@ -48,7 +48,7 @@ bool encode_map3(CUtensorMap *m, const Problem &p, const void *base, int bx, int
 #endif
 constexpr bool kTbOwn = PERKS_TB_OWN != 0;
 #ifndef PERKS_TB_NI
-#define PERKS_TB_NI 3
+#define PERKS_TB_NI 4
 #endif
 // Tick order: 1 = stage 1 (input plane -> IS) then stage 2 (previous IS plane -> output); 0 = the reverse.
 #ifndef PERKS_TB_S1FIRST
@@ -112,7 +112,11 @@ template <typename T, int S> struct TbG {
   static constexpr int NCW = NWARP + NHW;  // consumer warps (main + halo)
   static constexpr int NTHR = 32 * (NCW + 1);
   // IS slots (direct stage 2: three resident + one being written)
-  static constexpr int NI = (tb_direct2<S>() && PERKS_TB_NI < 4) ? 4 : PERKS_TB_NI;
+  static constexpr int NI = PERKS_TB_NI;
+  // The input arrival and IS plane counters are 32-bit and wrap on very long runs: slot = k % N and
+  // phase = (k / N) & 1 stay continuous across the wrap only when N divides 2^31.
+  static_assert((NS & (NS - 1)) == 0 && (NI & (NI - 1)) == 0, "ring depths must be powers of two");
+  static_assert(!tb_direct2<S>() || NI >= 4, "direct stage 2: three resident IS planes + one being written");
   static constexpr size_t IS_OFF = (size_t)NS * IN_SLOT * sizeof(T);
   static constexpr size_t BAR_OFF = IS_OFF + (size_t)NI * G::SLOT_BYTES;
   // full[NS], empty[NS] (input ring), written[NI] (NCW arrivals), read[NI] (NWARP arrivals)

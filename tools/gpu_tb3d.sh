@@ -1,13 +1,8 @@
 #!/bin/bash
-# TB3D fp64 tick order A/B (with 64-B L2 promotion) + parity of the new default.
+# TB3D with 4-slot IS ring: parity (TB tests, full-size C3/C5) + timing.
 mkdir -p gpurun_out
-PERKS_LIB_PATH=build/var_f64s1/libperks_stencil.so timeout 600 python -m pytest tests/test_gpu_tb3d.py -x -q 2>&1 | tail -3 > gpurun_out/tb3d_tests.log
-for rep in 1 2; do
-for lib in f64old f64s1; do
-  export PERKS_LIB_PATH=build/var_$lib/libperks_stencil.so
-  echo "== $lib"
-  timeout 300 python tools/run_shape.py 256,256,256 f64 3d7pt 1000 perks | tail -1
-  timeout 300 python tools/run_shape.py 1024,1024,1024 f64 3d7pt 20 perks | tail -1
-  timeout 300 python tools/run_shape.py 512,512,512 f64 3d7pt 200 perks | tail -1
-done
-done > gpurun_out/tb3d_timing7.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_tb3d.py tests/test_gpu_fullsize.py -x -q -k "tb3d or C3 or C5" 2>&1 | tail -3 > gpurun_out/tb3d_tests.log
+for cfg in "256,256,256 f64 3d7pt 1000" "1024,1024,1024 f64 3d7pt 20" "256,256,256 f32 3d7pt 1000"; do
+  set -- $cfg
+  timeout 300 python tools/run_shape.py $1 $2 $3 $4 perks 2>&1 | tail -1
+done > gpurun_out/tb3d_timing8.log 2>&1
