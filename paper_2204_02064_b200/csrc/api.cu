@@ -50,7 +50,9 @@ struct DistState {
   size_t ghost_bytes = 0, alloc_bytes = 0;
   void *lo_base = nullptr, *hi_base = nullptr;  // neighbours' allocations mapped here
   bool lo_ipc = false, hi_ipc = false;          // opened with cudaIpcOpenMemHandle
-  unsigned long long xbase = 0;   // exchanges done so far (each run of T steps does T + 1)
+  unsigned long long xbase = 0;   // exchanges done so far, in plane units (a one-step-per-pass run
+                                  // of T steps does T + 1; a two-steps-per-pass run 2 + 2 * passes)
+  unsigned long long tbx = 0;     // two-steps-per-pass exchanges so far (their ghost parity)
 };
 
 // Connection blob (PERKS_DIST_BLOB_BYTES): what a neighbour needs to map our ghost planes.
@@ -166,7 +168,10 @@ const Plan &get_plan(perks_stencil_s *h, perks_variant v) {
       // shape, 0 off
       const int tb = env_int("PERKS_P3D_TB", -1);
       const bool tb_auto = tb < 0 && p.shape == SHAPE_3D7 && env_int("PERKS_P3D_CACHE", 0) == 0;
-      if (!pl.ok && p.nranks == 1 && (tb == 1 || tb_auto)) pl = plan_tb3d(p);
+      // multi-GPU slabs: the two-deep ghost exchange per pass (k3d_tb.cu), PERKS_TB_DIST=0 keeps the
+      // one-step slab kernel
+      const bool tb_slabs = p.nranks == 1 || env_int("PERKS_TB_DIST", 1) != 0;
+      if (!pl.ok && tb_slabs && (tb == 1 || tb_auto)) pl = plan_tb3d(p);
       if (!pl.ok) pl = plan_stream3d(p, PERKS_PERKS);
     }
     h->plans[i] = pl;
@@ -186,7 +191,20 @@ perks_variant resolve(perks_stencil_s *h, perks_variant v) {
   return PERKS_PERSISTENT;
 }
 
-bool dist_perks_ok(perks_stencil_s *h) { return get_plan(h, PERKS_PERKS).ok && get_plan(h, PERKS_PERKS).family == 2; }
+bool dist_perks_ok(perks_stencil_s *h) {
+  const Plan &pl = get_plan(h, PERKS_PERKS);
+  return pl.ok && (pl.family == 2 || pl.family == 7);
+}
+// Exchange bookkeeping after a slab run of `steps` with plan `pl` (plane units, see DistState).
+void dist_advance(DistState &ds, const Plan &pl, int64_t steps) {
+  if (pl.family == 7) {
+    const unsigned long long passes = (unsigned long long)((steps + 1) / 2);
+    ds.xbase += 2ull + 2ull * passes;
+    ds.tbx += 1ull + passes;
+  } else {
+    ds.xbase += (unsigned long long)steps + 1;  // prologue exchange + one per step
+  }
+}
 
 DistRun dist_run(perks_stencil_s *h) {
   DistRun r;
@@ -201,6 +219,7 @@ DistRun dist_run(perks_stencil_s *h) {
   r.has_lo = p.rank > 0;
   r.has_hi = p.rank < p.nranks - 1;
   r.xbase = ds.xbase;
+  r.tbx = ds.tbx;
   return r;
 }
 
@@ -342,7 +361,8 @@ perks_status perks_stencil_create_dist(const perks_stencil_desc *d, int device, 
   DistState &ds = h->dist;
   ds.on = true;
   DeviceGuard g(device);
-  ds.ghost_bytes = align256((size_t)4 * h->p.nx * h->p.ny * h->p.elem());
+  // G[12][ny][nx]: planes 0..3 for the one-step slab kernels, 4..11 for the two-steps-per-pass kernel
+  ds.ghost_bytes = align256((size_t)12 * h->p.nx * h->p.ny * h->p.elem());
   ds.alloc_bytes = ds.ghost_bytes + 256;
   cudaError_t e = cudaMalloc(&ds.alloc, ds.alloc_bytes);
   if (e == cudaSuccess) e = cudaMemset(ds.alloc, 0, ds.alloc_bytes);
@@ -496,9 +516,10 @@ perks_status perks_stencil_run(perks_stencil_t h, perks_variant v, const void *d
   if (h->dist.on) {
     if (!h->dist.connected) return PERKS_ERR_COMM;
     DistRun dr = dist_run(h);
-    e = run_stream3d(p, pl, d_in, d_out, d_ws, steps, s, &dr);
+    e = pl.family == 7 ? run_tb3d(p, pl, d_in, d_out, d_ws, steps, s, &dr)
+                       : run_stream3d(p, pl, d_in, d_out, d_ws, steps, s, &dr);
     if (e != cudaSuccess) return cuda_fail(e);
-    h->dist.xbase += (unsigned long long)steps + 1;  // prologue exchange + one per step
+    dist_advance(h->dist, pl, steps);
     return PERKS_OK;
   }
   if (pl.family == 5 && p.ndim == 2) {  // Tiled PERKS (2D, beyond the on-chip capacity)
@@ -612,10 +633,14 @@ perks_status perks_stencil_run_group(const perks_stencil_t *hs, int n, perks_var
   if (rv != PERKS_HOSTLOOP) {
     // every slab's persistent grid spins on its neighbours: all grids must be resident at once
     // (a grid that cannot start would leave the others waiting until the watchdog trap)
+    // (capacity of the whole device: the slabs' plans may each see only PERKS_NUM_SMS of its SMs)
+    int dev_sms = 0;
+    if (cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, hs[0]->p.device) != cudaSuccess)
+      return cuda_fail(cudaGetLastError());
     int64_t sum = 0, cap = INT64_MAX;
     for (int i = 0; i < n; i++) {
       sum += pls[i]->grid;
-      cap = std::min<int64_t>(cap, (int64_t)pls[i]->ctas_per_sm * ps[i]->num_sms);
+      cap = std::min<int64_t>(cap, (int64_t)pls[i]->ctas_per_sm * dev_sms);
     }
     if (sum > cap) return PERKS_ERR_NOT_CORESIDENT;
   }
@@ -636,7 +661,8 @@ perks_status perks_stencil_run_group(const perks_stencil_t *hs, int n, perks_var
       }
       cudaStream_t gs = h->g_streams[0];
       cudaStreamWaitEvent(gs, fork, 0);
-      e = run_stream3d(*ps[i], *pls[i], d_in[i], d_out[i], d_ws[i], steps, gs, &drs[i]);
+      e = pls[i]->family == 7 ? run_tb3d(*ps[i], *pls[i], d_in[i], d_out[i], d_ws[i], steps, gs, &drs[i])
+                              : run_stream3d(*ps[i], *pls[i], d_in[i], d_out[i], d_ws[i], steps, gs, &drs[i]);
       if (e != cudaSuccess) break;
       cudaEventCreateWithFlags(&joins[i], cudaEventDisableTiming);
       cudaEventRecord(joins[i], gs);
@@ -646,7 +672,7 @@ perks_status perks_stencil_run_group(const perks_stencil_t *hs, int n, perks_var
     cudaEventDestroy(fork);
   }
   if (e != cudaSuccess) return cuda_fail(e);
-  for (int i = 0; i < n; i++) hs[i]->dist.xbase += (unsigned long long)steps + 1;
+  for (int i = 0; i < n; i++) dist_advance(hs[i]->dist, *pls[i], steps);
   return PERKS_OK;
 }
 

@@ -67,7 +67,8 @@ struct DistRun {
   unsigned long long *ctr = nullptr;          // local arrival counters [2]
   void *lo_ghost = nullptr, *hi_ghost = nullptr;  // neighbours' G (mapped into this process)
   unsigned long long *lo_ctr = nullptr, *hi_ctr = nullptr;  // neighbours' counters [2]
-  unsigned long long xbase = 0;               // exchange index of this run's input
+  unsigned long long xbase = 0;               // exchange index of this run's input (plane units)
+  unsigned long long tbx = 0;                 // two-steps-per-pass exchanges done so far (k3d_tb.cu)
   int has_lo = 0, has_hi = 0;
   int noncoop = 0;                            // launch persistent kernels non-cooperatively
                                               // (several slabs resident on ONE device)
@@ -115,7 +116,7 @@ cudaError_t run_brick3d(const Problem &p, const Plan &pl, const void *in, void *
 // in flight kept in shared memory (k3d_tb.cu).
 Plan plan_tb3d(const Problem &p);
 cudaError_t run_tb3d(const Problem &p, const Plan &pl, const void *in, void *out, void *ws, int64_t steps,
-                     cudaStream_t s);
+                     cudaStream_t s, const DistRun *dr = nullptr);
 
 // Any variant for general 2D point sets of radius <= 6 (k2d_wide.cu).
 Plan plan_wide2d(const Problem &p, perks_variant v);

@@ -40,6 +40,7 @@ namespace perks {
 
 bool use_tma3(const Problem &p);
 bool encode_map3(CUtensorMap *m, const Problem &p, const void *base, int bx, int by, int promo);
+DistK make_distk(const DistRun *dr);
 
 // Stage 2 takes its own cells from registers (1) or re-reads them from the IS slot (0: fewer live
 // registers).
@@ -125,7 +126,17 @@ template <typename T, int S> struct TbG {
 
 struct TbMaps {
   CUtensorMap m[3];  // in, out, tmp: box {P, TY+4, 1}
+  CUtensorMap ghost; // multi-GPU slabs: the ghost planes G[12][ny][nx], same box
 };
+// Multi-GPU slabs: ghost planes 4..11 of the library-owned G hold this kernel's
+// exchanges, two planes per face and parity: plane 4 + parity*4 + side*2 + j, side 0 = planes -2, -1
+// (j = 0, 1) from the lower neighbour, side 1 = planes nz, nz+1 from the upper neighbour (planes
+// 0..3 belong to the one-step slab kernels).  Exchange k (0 = the run's input, k = pass + 1 = that
+// pass's output) carries two planes per face; the arrival counters count cells, so exchange k is
+// complete when a side's counter reaches (xbase + 2k + 2) * nx*ny (xbase in plane units).
+PERKS_DEVINL int tb_ghost_plane(unsigned long long ex, int side, int j) {
+  return 4 + (int)(ex & 1ull) * 4 + side * 2 + j;
+}
 struct TbUnits {
   int tx, ty, nzc, zc, rev;
 };
@@ -249,10 +260,11 @@ PERKS_DEVINL void arrival_nb(StreamState<T, G> &st, const T (&nb)[G::R + 2][G::V
     }
 }
 
-template <typename T, int S>
+template <typename T, int S, bool DIST>
 __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
     tb3d_kernel(const T *__restrict__ in, T *out, T *tmp, const __grid_constant__ TbMaps maps, Dom3 d, TbUnits u,
-                int64_t steps, unsigned *bar, Coef<T, Shape<S>::N> c) {
+                int64_t steps, unsigned *bar, Coef<T, Shape<S>::N> c, const __grid_constant__ DistK dk,
+                unsigned long long xbase, unsigned long long tbx) {
   using B = TbG<T, S>;
   using G = typename B::G;
   unsigned char *sm = dyn_smem();
@@ -332,9 +344,19 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
           for (int k = 0; k < nin; k++) {
             const unsigned kk = k0 + (unsigned)k;
             if (kk >= (unsigned)B::NS) mbar_wait_sleep(emptyb(kk), ((kk / B::NS) + 1) & 1u);
+            const int q = q0 + k;
+            const int gs = DIST ? ((q < 0 && dk.has_lo) ? 0 : ((q >= d.nz && dk.has_hi) ? 1 : -1)) : -1;
+            if (gs >= 0) {  // a neighbour's plane: wait until exchange ps fully arrived
+              wait_counter_sys(dk.ctr + gs, (xbase + 2ull * (unsigned long long)ps + 2ull) * plane);
+              fence_proxy_async_global();
+            }
             fence_proxy_async();
             mbar_arrive_tx(fullb(kk), B::IN_BOX_BYTES);
-            tma_load_3d(in_slot(kk), &maps.m[src_idx], x0 - B::PAD, y0 - 2, q0 + k, fullb(kk));
+            if (gs >= 0)
+              tma_load_3d(in_slot(kk), &maps.ghost, x0 - B::PAD, y0 - 2,
+                          tb_ghost_plane(tbx + (unsigned long long)ps, gs, gs == 0 ? q + 2 : q - d.nz), fullb(kk));
+            else
+              tma_load_3d(in_slot(kk), &maps.m[src_idx], x0 - B::PAD, y0 - 2, q, fullb(kk));
           }
         }
         __syncwarp();
@@ -361,6 +383,22 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
             store_cells<T, G>(dst, d, tt, o, v);
           }
           sp += plane;
+          if constexpr (DIST) {  // face planes of this pass's output to the neighbours' ghosts
+            const bool lo = dk.has_lo && o <= 1, hi = dk.has_hi && o >= d.nz - 2;
+            if (lo || hi) {
+              const unsigned long long ex = tbx + (unsigned long long)ps + 1ull;
+              if (lo) store_cells<T, G>(reinterpret_cast<T *>(dk.send_lo), d, tt, tb_ghost_plane(ex, 1, o), v);
+              if (hi) store_cells<T, G>(reinterpret_cast<T *>(dk.send_hi), d, tt, tb_ghost_plane(ex, 0, o - (d.nz - 2)), v);
+              __threadfence_system();
+              asm volatile("bar.sync 2, %0;\n" ::"n"(32 * B::NWARP) : "memory");
+              if (threadIdx.x == 0) {
+                const unsigned long long cells =
+                    (unsigned long long)min(B::TX, d.nx - x0) * (unsigned long long)min(B::TY, d.ny - y0);
+                if (lo) red_release_sys_add_u64(dk.peer_ctr_lo, cells);
+                if (hi) red_release_sys_add_u64(dk.peer_ctr_hi, cells);
+              }
+            }
+          }
         };
         if (nst == 1) {
           for (int k = 0; k < nin; k++) {
@@ -569,9 +607,9 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
 
 namespace {
 template <typename T> void *tb_kernel(int shape) {
-  return shape == SHAPE_3D7    ? (void *)tb3d_kernel<T, SHAPE_3D7>
-         : shape == SHAPE_3D19 ? (void *)tb3d_kernel<T, SHAPE_3D19>
-                               : (void *)tb3d_kernel<T, SHAPE_3D27>;
+  return shape == SHAPE_3D7    ? (void *)tb3d_kernel<T, SHAPE_3D7, false>
+         : shape == SHAPE_3D19 ? (void *)tb3d_kernel<T, SHAPE_3D19, false>
+                               : (void *)tb3d_kernel<T, SHAPE_3D27, false>;
 }
 struct TbInfo {
   int TX, TY, NT, P, RI;
@@ -591,8 +629,8 @@ Plan plan_tb3d(const Problem &p) {
   Plan pl;
   pl.variant = PERKS_PERKS;
   if (p.ndim != 3 || (p.shape != SHAPE_3D7 && p.shape != SHAPE_3D27 && p.shape != SHAPE_3D19) ||
-      p.bc != PERKS_BC_FRAME || p.nranks != 1) {
-    pl.why = "tb3d: needs single-GPU 3D 7pt/19pt/27pt FRAME";
+      p.bc != PERKS_BC_FRAME || (p.nranks > 1 && (p.shape != SHAPE_3D7 || p.nz < 2))) {
+    pl.why = "tb3d: needs 3D 7pt/19pt/27pt FRAME (multi-GPU slabs: 7pt, >= 2 planes)";
     return pl;
   }
   if (!use_tma3(p)) { pl.why = "tb3d: needs TMA (nx*S % 16 == 0)"; return pl; }
@@ -601,6 +639,8 @@ Plan plan_tb3d(const Problem &p) {
   const int TX = ti.TX, TY = ti.TY, NT = ti.NT;
   const size_t smem = ti.smem;
   void *k = f32 ? tb_kernel<float>(p.shape) : tb_kernel<double>(p.shape);
+  if (p.nranks > 1)  // the slab kernel (7-point star, checked above)
+    k = f32 ? (void *)tb3d_kernel<float, SHAPE_3D7, true> : (void *)tb3d_kernel<double, SHAPE_3D7, true>;
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
     cudaGetLastError();
     pl.why = "tb3d: cudaFuncSetAttribute";
@@ -652,12 +692,42 @@ Plan plan_tb3d(const Problem &p) {
 }
 
 namespace {
+// Multi-GPU prologue of a run: the input's two bottom / top planes into the neighbours' ghosts as
+// exchange 0 (parity tbx); blockIdx.y = side (0: planes 0, 1 to the lower neighbour's side 1;
+// 1: planes nz-2, nz-1 to the upper neighbour's side 0), blockIdx.z = plane j, 8 rows per CTA.  Before
+// writing, wait until every exchange of the previous run from that neighbour arrived (it produced
+// its last one after reading ours: no write-after-read across runs).
+template <typename T>
+__global__ void __launch_bounds__(256) tb_dist_prologue_kernel(const T *__restrict__ in, DistK dk, int nx, int ny,
+                                                               int nz, unsigned long long xbase,
+                                                               unsigned long long tbx) {
+  const int side = blockIdx.y, j = blockIdx.z;
+  if (side == 0 ? !dk.has_lo : !dk.has_hi) return;
+  const unsigned long long plane = (unsigned long long)nx * ny;
+  if (threadIdx.x == 0) wait_counter_sys(dk.ctr + side, xbase * plane);
+  __syncthreads();
+  const int y0 = blockIdx.x * 8, y1 = min(y0 + 8, ny);
+  const int zsrc = side == 0 ? j : nz - 2 + j;
+  const T *srcp = in + (size_t)zsrc * plane + (size_t)y0 * nx;
+  T *dstp = reinterpret_cast<T *>(side == 0 ? dk.send_lo : dk.send_hi) +
+            (size_t)tb_ghost_plane(tbx, side == 0 ? 1 : 0, j) * plane + (size_t)y0 * nx;
+  const int n16 = (int)((size_t)(y1 - y0) * nx * sizeof(T) / 16);  // nx*S % 16 == 0 (TMA)
+  const uint4 *s4 = reinterpret_cast<const uint4 *>(srcp);
+  uint4 *d4 = reinterpret_cast<uint4 *>(dstp);
+  for (int i = threadIdx.x; i < n16; i += blockDim.x) d4[i] = s4[i];
+  signal_counter_sys(side == 0 ? dk.peer_ctr_lo : dk.peer_ctr_hi, (unsigned long long)(y1 - y0) * nx);
+}
+
 template <typename T, int S, class B>
 cudaError_t launch_tb_g(const Problem &p, const Plan &pl, const T *in, T *out, void *ws, int64_t steps,
-                        cudaStream_t s) {
+                        cudaStream_t s, const DistRun *dr) {
   Coef<T, Shape<S>::N> c;
   for (int i = 0; i < Shape<S>::N; i++) c.w[i] = sizeof(T) == 4 ? (T)p.wf[i] : (T)p.wd[i];
-  Dom3 d{(int)p.nx, (int)p.ny, (int)p.nz, 1, (int)p.nz - 2};
+  const bool dist = dr != nullptr && p.nranks > 1;
+  // slab faces with a neighbour are interior (reading R12); so are the neighbours' planes -1 / nz,
+  // whose level t+1 this kernel computes redundantly from the two-deep ghosts
+  Dom3 d{(int)p.nx, (int)p.ny, (int)p.nz, (dist && p.rank > 0) ? -1 : 1,
+         (dist && p.rank < p.nranks - 1) ? (int)p.nz : (int)p.nz - 2};
   TbUnits u{(int)((p.nx + B::TX - 1) / B::TX), (int)((p.ny + B::TY - 1) / B::TY), 0, pl.zchunk,
             env_int("PERKS_ZIGZAG", 1)};
   u.nzc = (int)((p.nz + u.zc - 1) / u.zc);
@@ -672,11 +742,27 @@ cudaError_t launch_tb_g(const Problem &p, const Plan &pl, const T *in, T *out, v
   const int promo = env_int("PERKS_TMA_L2PROMO", 64);
   for (int i = 0; i < 3; i++)
     if (!encode_map3(&maps.m[i], p, b[i], B::P, B::RI, promo)) return cudaErrorInvalidValue;
+  DistK dk = make_distk(dist ? dr : nullptr);
+  unsigned long long xbase = dist ? dr->xbase : 0, tbx = dist ? dr->tbx : 0;
+  if (dist) {
+    Problem g = p;
+    g.nz = 12;  // G[12][ny][nx]
+    if (!encode_map3(&maps.ghost, g, dr->ghost, B::P, B::RI, promo)) return cudaErrorInvalidValue;
+  }
   cudaError_t e = reset_grid_barrier(bar, s);
   if (e != cudaSuccess) return e;
-  void *k = (void *)tb3d_kernel<T, S>;
-  void *args[] = {(void *)&in, (void *)&out, (void *)&tmp, (void *)&maps, (void *)&d, (void *)&u,
-                  (void *)&steps, (void *)&bar, (void *)&c};
+  if (dist) {
+    tb_dist_prologue_kernel<T><<<dim3((unsigned)((p.ny + 7) / 8), 2, 2), 256, 0, s>>>(
+        in, dk, (int)p.nx, (int)p.ny, (int)p.nz, xbase, tbx);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  void *k = (void *)tb3d_kernel<T, S, false>;
+  if constexpr (S == SHAPE_3D7) {  // (slabs: the 7-point star only)
+    if (dist) k = (void *)tb3d_kernel<T, S, true>;
+  }
+  void *args[] = {(void *)&in,  (void *)&out,   (void *)&tmp,  (void *)&maps, (void *)&d,
+                  (void *)&u,   (void *)&steps, (void *)&bar,  (void *)&c,    (void *)&dk,
+                  (void *)&xbase, (void *)&tbx};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(pl.grid);
   cfg.blockDim = dim3(pl.block);
@@ -686,26 +772,29 @@ cudaError_t launch_tb_g(const Problem &p, const Plan &pl, const T *in, T *out, v
   at[0].id = cudaLaunchAttributeCooperative;
   at[0].val.cooperative = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = (dist && dr->noncoop) ? 0 : 1;  // (several slabs resident on one device: run_group)
   return cudaLaunchKernelExC(&cfg, k, args);
 }
 
 template <typename T, int S>
 cudaError_t launch_tb(const Problem &p, const Plan &pl, const T *in, T *out, void *ws, int64_t steps,
-                      cudaStream_t s) {
-  return launch_tb_g<T, S, TbG<T, S>>(p, pl, in, out, ws, steps, s);
+                      cudaStream_t s, const DistRun *dr) {
+  if constexpr (S != SHAPE_3D7) {
+    if (dr != nullptr && p.nranks > 1) return cudaErrorNotSupported;
+  }
+  return launch_tb_g<T, S, TbG<T, S>>(p, pl, in, out, ws, steps, s, dr);
 }
 }  // namespace
 
 cudaError_t run_tb3d(const Problem &p, const Plan &pl, const void *in, void *out, void *ws, int64_t steps,
-                     cudaStream_t s) {
+                     cudaStream_t s, const DistRun *dr) {
   if (p.dtype == PERKS_F32)
-    return p.shape == SHAPE_3D7    ? launch_tb<float, SHAPE_3D7>(p, pl, (const float *)in, (float *)out, ws, steps, s)
-           : p.shape == SHAPE_3D19 ? launch_tb<float, SHAPE_3D19>(p, pl, (const float *)in, (float *)out, ws, steps, s)
-                                   : launch_tb<float, SHAPE_3D27>(p, pl, (const float *)in, (float *)out, ws, steps, s);
-  return p.shape == SHAPE_3D7    ? launch_tb<double, SHAPE_3D7>(p, pl, (const double *)in, (double *)out, ws, steps, s)
-         : p.shape == SHAPE_3D19 ? launch_tb<double, SHAPE_3D19>(p, pl, (const double *)in, (double *)out, ws, steps, s)
-                                 : launch_tb<double, SHAPE_3D27>(p, pl, (const double *)in, (double *)out, ws, steps, s);
+    return p.shape == SHAPE_3D7    ? launch_tb<float, SHAPE_3D7>(p, pl, (const float *)in, (float *)out, ws, steps, s, dr)
+           : p.shape == SHAPE_3D19 ? launch_tb<float, SHAPE_3D19>(p, pl, (const float *)in, (float *)out, ws, steps, s, dr)
+                                   : launch_tb<float, SHAPE_3D27>(p, pl, (const float *)in, (float *)out, ws, steps, s, dr);
+  return p.shape == SHAPE_3D7    ? launch_tb<double, SHAPE_3D7>(p, pl, (const double *)in, (double *)out, ws, steps, s, dr)
+         : p.shape == SHAPE_3D19 ? launch_tb<double, SHAPE_3D19>(p, pl, (const double *)in, (double *)out, ws, steps, s, dr)
+                                 : launch_tb<double, SHAPE_3D27>(p, pl, (const double *)in, (double *)out, ws, steps, s, dr);
 }
 
 }  // namespace perks

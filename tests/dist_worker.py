@@ -1,7 +1,7 @@
 """Single-GPU emulation of the multi-GPU slab decomposition (run in a child process by
 tests/test_gpu_dist.py so that a watchdog trap cannot poison the test process).
 
-usage: python dist_worker.py OUT.npy NAME NZ NY NX DTYPE NRANKS VARIANT T1 [T2 ...]
+usage: python dist_worker.py OUT.npy NAME NZ NY NX DTYPE NRANKS VARIANT[,VARIANT...] T1 [T2 ...]
 Splits the seeded global field into NRANKS z-slabs (one Stencil handle each, all on cuda:0),
 connects the chain, runs T1, then T2, ... steps back to back (each run feeds the next), and saves
 the concatenated global result."""
@@ -37,9 +37,10 @@ def main(argv):
     blobs = [st.export_blob() for st in sts]
     for r, st in enumerate(sts):
         st.connect(blobs[r - 1] if r > 0 else None, blobs[r + 1] if r < n - 1 else None)
-    for T in Ts:
+    variants = variant.split(",")  # one variant for every run, or one per run (mixed on the same handles)
+    for i, T in enumerate(Ts):
         outs = [torch.full_like(x, float("nan")) for x in xs]
-        run_group(sts, xs, T, variant, outs=outs)
+        run_group(sts, xs, T, variants[i % len(variants)], outs=outs)
         torch.cuda.synchronize()
         xs = outs
     res = np.concatenate([x.cpu().numpy() for x in xs], axis=0)

@@ -95,3 +95,38 @@ def test_two_process_ipc_slabs(tmp_path):
     offs, w = si.preset(name)
     ref = oracle.run(si.field(shape, dtype=dtype, seed=505), offs, w, 5, nthreads=4)
     assert np.array_equal(got, ref), f"{int(np.sum(got != ref))} cells differ"
+
+
+@pytest.mark.parametrize("n", [2, 3])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_slabs_two_steps_per_pass(tmp_path, n, dtype):
+    """The 7-point star's slab plan is the two-steps-per-pass kernel (k3d_tb.cu): two-deep ghost planes
+    exchanged once per pass, the neighbours' planes -1 / nz computed redundantly.  Bit-exact vs the
+    global oracle for odd / even T, and with one-step-per-pass runs interleaved on the same handles
+    (exchange bookkeeping in plane units, separate ghost planes)."""
+    _need_gpu()
+    from paper_2204_02064_b200 import Stencil
+    offs, w = si.preset("3d7pt")
+    st = Stencil((9, 40, 64), offs, w, dtype=dtype, rank=0, nranks=n)
+    q = st.query("perks")
+    st.close()
+    assert q["kernel"].startswith("perks3d_tb2"), q
+    shape = (9 * n + 2, 40, 64)
+    u0 = si.field(shape, dtype=dtype, seed=505)  # (dist_worker.py seeds the global field with 505)
+    Ts = [5, 4, 3, 6]
+    got = _dist(tmp_path, "3d7pt", shape, dtype, n, "perks,persistent,perks,hostloop", Ts)
+    ref = oracle.run(u0, offs, w, sum(Ts), nthreads=4)
+    assert not np.isnan(got).any()
+    assert np.array_equal(got, ref), f"{int(np.sum(got != ref))} cells differ"
+
+
+def test_slabs_two_deep_ghosts_minimum_planes(tmp_path):
+    """Slabs of 2 and 3 planes: a face plane goes to both neighbours in the same pass."""
+    _need_gpu()
+    offs, w = si.preset("3d7pt")
+    shape = (7, 24, 64)  # slab_bounds(7, 3): 3 / 2 / 2 planes
+    u0 = si.field(shape, dtype=np.float64, seed=505)
+    Ts = [4, 5]
+    got = _dist(tmp_path, "3d7pt", shape, np.float64, 3, "perks", Ts)
+    ref = oracle.run(u0, offs, w, sum(Ts), nthreads=4)
+    assert np.array_equal(got, ref), f"{int(np.sum(got != ref))} cells differ"
