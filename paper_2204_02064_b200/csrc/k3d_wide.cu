@@ -120,13 +120,16 @@ __device__ void unit3(const T *__restrict__ src, T *__restrict__ dst, int nx, in
   const int cell = (ly + r) * PX + (lx + r);  // this thread's centre within a plane
   const bool per = c.per != 0;
   const PlaneCopy pc = plane_copy(nx, ny, x0, y0, r, per);
+  // every warp has finished reading the previous unit's planes before the prefill overwrites their
+  // slots (persistent kernels run several units per CTA back to back; this barrier used to follow
+  // the prefill, a rare race: one failure of the C3-size PERIODIC persistent Fourier test in ~30)
+  __syncthreads();
   // ring slot of input plane zz: (zz - (z0 - r)) mod NP; planes z0-r .. z0+r+LA-1 first (one
   // commit group each; planes past the chunk's last need are empty groups)
   for (int q = 0; q < 2 * r + KW3_LA; q++) {
     if (z0 - r + q < z1 + r) load_plane3(src, ring + q * PXY, pc, nx, ny, nz, z0 - r + q, per);
     else cp_async_commit();
   }
-  __syncthreads();  // the previous unit's last plane is read by every warp before its slots refill
   int base = 0;     // slot of plane z - r
   constexpr bool COL = PS != 0 && column_only_dz<PS != 0 ? PS : 1>();
   constexpr int CR = PS != 0 ? WideSet3<PS != 0 ? PS : 1>::R : 0;
