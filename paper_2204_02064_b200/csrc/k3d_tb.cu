@@ -139,6 +139,9 @@ PERKS_DEVINL int tb_ghost_plane(unsigned long long ex, int side, int j) {
 }
 struct TbUnits {
   int tx, ty, nzc, zc, rev;
+  int range;  // 1: CTA b owns the contiguous run [b W / G, (b+1) W / G) of the W = tiles * nz
+              // (tile, plane) sequence, split at tile boundaries (balanced work, one pipeline fill
+              // per tile touched); 0: units of zc planes strided over the grid
 };
 
 // Single-cell geometry for the halo warps' chain (apply_terms needs only R and V).
@@ -295,7 +298,11 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
 
   const int tiles = u.tx * u.ty;
   const int nunits = tiles * u.nzc;
-  const int nmine = (int)blockIdx.x < nunits ? (nunits - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const long long W = (long long)tiles * d.nz;
+  const long long rlo = W * (long long)blockIdx.x / (long long)gridDim.x;
+  const long long rhi = W * ((long long)blockIdx.x + 1) / (long long)gridDim.x;
+  const int nmine = u.range ? (rhi > rlo ? (int)((rhi - 1) / d.nz - rlo / d.nz) + 1 : 0)
+                            : ((int)blockIdx.x < nunits ? (nunits - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0);
   const size_t plane = (size_t)d.nx * d.ny;
   const int64_t npass = (steps + 1) / 2;
   unsigned gk = 0;  // input arrivals so far (slot = gk % NS, phase = (gk / NS) & 1)
@@ -311,10 +318,18 @@ __global__ void __launch_bounds__(TbG<T, S>::NTHR, 1)
     const bool rev = u.rev && (ps & 1);  // L2-aware traversal (zig-zag, [draft] P:395-404)
     for (int jj = 0; jj < nmine; jj++) {
       const int j = rev ? nmine - 1 - jj : jj;
-      const int id = (int)blockIdx.x + j * (int)gridDim.x;
-      const int t = id % tiles, zci = id / tiles;
+      int t, zs, ze;
+      if (u.range) {
+        t = (int)(rlo / d.nz) + j;
+        zs = j == 0 ? (int)(rlo % d.nz) : 0;
+        ze = j == nmine - 1 ? (int)((rhi - 1) % d.nz) + 1 : d.nz;
+      } else {
+        const int id = (int)blockIdx.x + j * (int)gridDim.x;
+        t = id % tiles;
+        zs = (id / tiles) * u.zc;
+        ze = min(zs + u.zc, d.nz);
+      }
       const int x0 = (t % u.tx) * B::TX, y0 = (t / u.tx) * B::TY;
-      const int zs = zci * u.zc, ze = min(zs + u.zc, d.nz);
       const int zc = ze - zs;
       const int nin = nst == 2 ? zc + 4 : zc + 2;  // input planes zs-2..ze+1 (zs-1..ze)
       const int q0 = nst == 2 ? zs - 2 : zs - 1;
@@ -671,12 +686,29 @@ Plan plan_tb3d(const Problem &p) {
   pl.units = tiles * nzc;
   pl.zchunk = zc;
   pl.grid = (int)std::min<int64_t>(pl.units, resident);
+  // balanced contiguous runs instead (TbUnits.range, opt-in PERKS_TB_RANGE=1 or -1 = by tick count):
+  // a run of ceil(W/G) planes touches at most ceil(len/nz)+1 tiles, each costing a 5-tick pipeline
+  // fill.  Measured slower than the strided units despite fewer ticks (C3 30.96 vs 30.45, C5 1739 vs
+  // 1626 us/step, profiles/r02_tb3d_range.txt): concurrently running CTAs then sit at unrelated z, so
+  // the tiles' overlapping halo rows no longer meet in L2.
+  {
+    const int64_t W = tiles * p.nz, G = std::min<int64_t>(resident, std::max<int64_t>(1, W / 8));
+    const int64_t len = (W + G - 1) / G, fills = std::min<int64_t>(tiles, (len + p.nz - 1) / p.nz + 1);
+    const int64_t ticks_range = len + 5 * fills, ticks_units = best;
+    const int force = env_int("PERKS_TB_RANGE", 0);
+    if (force == 1 || (force < 0 && ticks_range < ticks_units)) {
+      pl.cfg = 2;  // (range mode)
+      pl.grid = (int)G;
+      pl.units = G;
+      pl.zchunk = (int)std::min<int64_t>(len, p.nz);
+    }
+  }
   pl.block = NT;
   pl.ctas_per_sm = occ;
   pl.tile[0] = TX; pl.tile[1] = TY; pl.tile[2] = zc;
   pl.regs = fa.numRegs;
   pl.smem = (int)smem;
-  pl.cfg = 1;
+  if (pl.cfg != 2) pl.cfg = 1;
   pl.family = 7;  // (3D PERKS, two time steps per pass)
   const double S = (double)p.elem();
   pl.cached_smem = 0;  // level t+1 is on chip only while its planes are in flight (no resident cells)
@@ -729,7 +761,7 @@ cudaError_t launch_tb_g(const Problem &p, const Plan &pl, const T *in, T *out, v
   Dom3 d{(int)p.nx, (int)p.ny, (int)p.nz, (dist && p.rank > 0) ? -1 : 1,
          (dist && p.rank < p.nranks - 1) ? (int)p.nz : (int)p.nz - 2};
   TbUnits u{(int)((p.nx + B::TX - 1) / B::TX), (int)((p.ny + B::TY - 1) / B::TY), 0, pl.zchunk,
-            env_int("PERKS_ZIGZAG", 1)};
+            env_int("PERKS_ZIGZAG", 1), pl.cfg == 2 ? 1 : 0};
   u.nzc = (int)((p.nz + u.zc - 1) / u.zc);
   char *w = (char *)ws;
   T *tmp = (T *)w;

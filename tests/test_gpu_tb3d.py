@@ -42,16 +42,20 @@ def test_tb3d_parity(monkeypatch, name, dtype, shape):
         _check(_run_gpu(u0, name, w, T, "perks"), ref, u0, dtype)
 
 
-@pytest.mark.parametrize("nsm,nzc,zigzag", [("3", "0", "1"), ("5", "7", "0"), ("2", "3", "1"), ("0", "11", "1")])
+@pytest.mark.parametrize("nsm,nzc,zigzag,rng", [("3", "0", "1", "0"), ("5", "7", "0", "0"), ("2", "3", "1", "0"),
+                                              ("0", "11", "1", "0"), ("3", "0", "1", "1"), ("7", "0", "0", "1"),
+                                              ("0", "0", "1", "1"), ("13", "0", "1", "1")])
 @pytest.mark.parametrize("name,dtype", [("3d7pt", np.float64), ("3d27pt", np.float32), ("3d19pt", np.float64)])
-def test_tb3d_units_and_chunks(monkeypatch, nsm, nzc, zigzag, name, dtype):
-    """Several units per CTA (PERKS_NUM_SMS), forced z chunking, zig-zag on/off."""
+def test_tb3d_units_and_chunks(monkeypatch, nsm, nzc, zigzag, rng, name, dtype):
+    """Several units per CTA (PERKS_NUM_SMS), forced z chunking, zig-zag on/off; balanced contiguous
+    runs of (tile, plane) split at tile boundaries (PERKS_TB_RANGE=1), also over several tiles."""
     _need_gpu()
     monkeypatch.setenv("PERKS_P3D_TB", "1")
     if nsm != "0":
         monkeypatch.setenv("PERKS_NUM_SMS", nsm)
     monkeypatch.setenv("PERKS_TB_NZC", nzc)
     monkeypatch.setenv("PERKS_ZIGZAG", zigzag)
+    monkeypatch.setenv("PERKS_TB_RANGE", rng)
     shape = (45, 50, 136)
     assert _kernel(name, shape, dtype)["kernel"].startswith("perks3d_tb2")
     u0 = si.field(shape, dtype=dtype, seed=909)
